@@ -1,0 +1,161 @@
+/*
+ * ce.h — C ABI of the B200-native conv_einsum executor (libce.so).
+ *
+ * The reference (`convexpr`, /root/reference/proj) is a C++20 library with no
+ * FFI: its hot path is the by-value C++ pair
+ *     ExecutionResult execute(const EvaluationPlan&, const std::vector<DenseTensor>&)
+ *                                                        (sequencer.hpp:88, sequencer.cpp:403-447)
+ *     DenseTensor pairwise_eval(const DenseTensor&, const DenseTensor&, const PairwiseOp&)
+ *                                                        (kernels.hpp:105, kernels.cpp:425-470)
+ * fed by parse (expression.hpp:78) -> make_shape_env (tensor.hpp:83) ->
+ * resolve_conv_modes (kernels.hpp:30) -> optimal/left_to_right (sequencer.hpp:44-63).
+ * These entry points are what a maintainer's FFI for that path would bind
+ * (see INTEGRATION.md for the ctypes / C++ shims).  Plain pointers and sizes,
+ * no torch types.  Tensors are FP32, dense row-major in the subscript order of
+ * the expression (input i: spec.inputs[i], output: spec.output), resident in
+ * device memory unless the function name says "host".
+ *
+ * Errors: every call returns ce_status (aligned with SPEC.md:542 exit codes:
+ * 2 parse, 3 shape, 4 numeric, 1 other; plus planner/overflow/CUDA codes);
+ * ce_last_error() gives the thread-local message of the last failure.
+ * Threading: calls on one ce_ctx are stream-ordered and not re-entrant;
+ * different contexts (GPUs) may be driven from different host threads.
+ */
+#ifndef CE_CE_H
+#define CE_CE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CE_OK = 0,
+  CE_ERR_OTHER = 1,
+  CE_ERR_PARSE = 2,    /* ParseError        expression.hpp:15-20  */
+  CE_ERR_SHAPE = 3,    /* ShapeError        tensor.hpp:16-18      */
+  CE_ERR_NUMERIC = 4,
+  CE_ERR_PLAN = 5,     /* PlanError         sequencer.hpp:14-16   */
+  CE_ERR_OVERFLOW = 6, /* OverflowError     checked_int.hpp:13-15 */
+  CE_ERR_CUDA = 7,
+  CE_ERR_NCCL = 8,
+  CE_ERR_UNSUPPORTED = 9
+} ce_status;
+
+const char* ce_last_error(void);
+const char* ce_version(void);
+
+/* ---------------------------------------------------------------- host IR -- */
+/* parse + render + classify (expression.hpp:76-83).  `rendered` gets render(spec);
+ * `classes` gets "atom:class" pairs separated by spaces in atom-name order. */
+ce_status ce_parse(const char* expr, char* rendered, size_t rendered_cap, char* classes, size_t classes_cap);
+
+/* ---------------------------------------------------------------- planner -- */
+typedef struct ce_plan ce_plan;
+
+typedef enum { CE_PLAN_OPTIMAL = 0, CE_PLAN_LEFT_TO_RIGHT = 1, CE_PLAN_OPTIMAL_CAPPED = 2 } ce_plan_strategy;
+
+/* dims: all input dims concatenated; ranks[i]: number of axes of input i.
+ * mode: "full" | "same" | "valid" | "circular" (resolve_conv_modes, kernels.cpp:38-43).
+ * cost_mode: "inference" | "training" (cost.hpp:8).
+ * Replaces: optimal()/left_to_right() (sequencer.hpp:44-63). */
+ce_status ce_plan_create(const char* expr, const int64_t* dims, const int* ranks, int n_inputs, const char* mode,
+                         const char* cost_mode, int strategy, ce_plan** out);
+/* plan_from_joins (sequencer.hpp:70-73): joins[2*j], joins[2*j+1] = (left id, right id). */
+ce_status ce_plan_from_joins(const char* expr, const int64_t* dims, const int* ranks, int n_inputs,
+                             const char* mode, const char* cost_mode, const int* joins, int n_joins,
+                             ce_plan** out);
+void ce_plan_destroy(ce_plan* plan);
+/* plan_to_json (sequencer.cpp:466-480), byte-identical to the reference. */
+ce_status ce_plan_json(const ce_plan* plan, char* buf, size_t cap);
+/* tree_encoding (sequencer.cpp:449-457); "0" for single-input plans. */
+ce_status ce_plan_tree_encoding(const ce_plan* plan, char* buf, size_t cap);
+
+typedef struct {
+  int n_inputs, n_nodes, out_rank;
+  int64_t out_dims[16];
+  uint64_t total_cost_lo, total_cost_hi;         /* plan.total_cost (u128) under the plan's mode */
+  uint64_t inference_cost_lo, inference_cost_hi; /* plan_cost(plan, Inference) */
+  uint64_t training_cost_lo, training_cost_hi;   /* plan_cost(plan, Training) */
+  uint64_t flops_actual_lo, flops_actual_hi;     /* sum of flops_actual over nodes (executed MACs) */
+  uint64_t peak_intermediate_elements;
+} ce_plan_info;
+ce_status ce_plan_get_info(const ce_plan* plan, ce_plan_info* info);
+
+/* Per-node description: "left right result_subs flops_actual_lo cost" for diagnostics. */
+ce_status ce_plan_node(const ce_plan* plan, int node, int* left, int* right, char* result_subs, size_t cap,
+                       uint64_t* flops_actual_lo, uint64_t* cost_lo);
+
+/* ----------------------------------------------------------------- layers -- */
+/* expression() (layers.hpp:71): kind name as in layer_kind_from_string (layers.cpp:29-45).
+ * With cr > 0 the ranks are solved by rank_for_compression (layers.cpp:341-366) and
+ * written to ranks_out.  dims_out/ranks_of_input receive the per-input shapes. */
+ce_status ce_layer_expression(const char* kind, const int64_t* t_factors, int n_t, const int64_t* s_factors,
+                              int n_s, int64_t filter_h, int64_t filter_w, int64_t feature_h, int64_t feature_w,
+                              int64_t batch, const int64_t* ranks, int n_ranks, double cr, char* expr_out,
+                              size_t expr_cap, int64_t* dims_out, int dims_cap, int* ranks_of_input,
+                              int* n_inputs, int64_t* ranks_out, int* n_ranks_out, uint64_t* param_count);
+
+/* ----------------------------------------------------------------- device -- */
+typedef struct ce_ctx ce_ctx;
+
+typedef enum {
+  CE_MATH_AUTO = 0,      /* tcgen05 TF32 tensor cores where the step maps onto them, FP32 SIMT elsewhere */
+  CE_MATH_FP32_SIMT = 1  /* FP32 CUDA-core kernels only (accuracy anchor) */
+} ce_math;
+
+typedef struct {
+  int math;           /* ce_math */
+  int use_graphs;     /* capture execute/backward into CUDA graphs on first call */
+  void* stream;       /* optional cudaStream_t to run on (NULL: ctx creates its own) */
+} ce_options;
+
+ce_status ce_ctx_create(int device, const ce_options* opts, ce_ctx** out);
+void ce_ctx_destroy(ce_ctx* ctx);
+void* ce_ctx_stream(ce_ctx* ctx); /* the cudaStream_t all work of this ctx is ordered on */
+ce_status ce_ctx_synchronize(ce_ctx* ctx);
+
+/* Device SplitMix64 fill (tensor.cpp:107-130): dst[i] = (float) fill_random(seed)[i]. */
+ce_status ce_fill_random(ce_ctx* ctx, float* dst, int64_t n, uint64_t seed);
+
+/* ------------------------------------------------------------ executor ----- */
+typedef struct ce_executor ce_executor;
+
+typedef struct {
+  uint64_t multiplications_lo, multiplications_hi; /* ExecutionResult.multiplications (sequencer.hpp:82) */
+  uint64_t peak_intermediate_elements;             /* ExecutionResult.peak_intermediate_elements */
+  int kernels_launched;                            /* kernels launched by the last call */
+  int tc_steps;                                    /* steps that ran on tcgen05 tensor cores */
+} ce_exec_stats;
+
+/* Binds a plan to a context and sizes its workspace (intermediates, packed
+ * operands and, with want_backward, gradient buffers). */
+ce_status ce_executor_create(ce_ctx* ctx, const ce_plan* plan, int want_backward, ce_executor** out);
+void ce_executor_destroy(ce_executor* ex);
+/* execute (sequencer.cpp:403-447): inputs[i] device FP32 dense in spec.inputs[i]
+ * order; out device FP32 dense in spec.output order.  Stream-ordered. */
+ce_status ce_execute(ce_executor* ex, const float* const* inputs, float* out, ce_exec_stats* stats);
+/* Gradients of <dout, execute(inputs)> w.r.t. each input (NULL entries skipped).
+ * Requires a preceding ce_execute on this executor with the same inputs: the
+ * intermediates it left in the workspace are reused (no recompute). */
+ce_status ce_backward(ce_executor* ex, const float* const* inputs, const float* dout, float* const* dinputs,
+                      ce_exec_stats* stats);
+/* Host-buffer convenience (e2e path): H2D copy, execute, D2H copy, synchronize. */
+ce_status ce_execute_host(ce_executor* ex, const float* const* host_inputs, float* host_out);
+
+/* ------------------------------------------------------------ pairwise ----- */
+/* pairwise_eval (kernels.cpp:425-470) for the op make_pairwise_op builds from
+ * expr "L,R->RES|convs" with keep = RES and result order RES (the planner's node
+ * construction, sequencer.cpp:118-124).  a, b, out: device FP32 dense. */
+ce_status ce_pairwise_eval(ce_ctx* ctx, const char* expr, const int64_t* dims, const int* ranks, const char* mode,
+                           const float* a, const float* b, float* out);
+/* Adjoints of the same op: da = d<dout, op(a,b)>/da, db likewise (NULL to skip). */
+ce_status ce_pairwise_grad(ce_ctx* ctx, const char* expr, const int64_t* dims, const int* ranks, const char* mode,
+                           const float* a, const float* b, const float* dout, float* da, float* db);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CE_CE_H */

@@ -1,0 +1,375 @@
+// extern "C" boundary (include/ce/ce.h) over the host planner and the device
+// executor.  Exceptions never cross the ABI: they become ce_status codes with
+// a thread-local message (SPEC.md:542 exit-code mapping).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/ce/ce.h"
+#include "cuda/ce_kernels.h"
+#include "host/ce_exec.hpp"
+#include "host/ce_layers.hpp"
+
+using namespace ce;
+
+struct ce_plan {
+  EvaluationPlan plan;
+};
+
+struct ce_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ce_options opts{};
+};
+
+struct ce_executor {
+  ce_ctx* ctx = nullptr;
+  std::unique_ptr<Executor> ex;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <class F>
+ce_status guard(F&& f) {
+  try {
+    f();
+    return CE_OK;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    return CE_ERR_PARSE;
+  } catch (const ShapeError& e) {
+    g_err = e.what();
+    return CE_ERR_SHAPE;
+  } catch (const PlanError& e) {
+    g_err = e.what();
+    return CE_ERR_PLAN;
+  } catch (const OverflowError& e) {
+    g_err = e.what();
+    return CE_ERR_OVERFLOW;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return CE_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return std::string(e.what()).rfind("CUDA error", 0) == 0 ? CE_ERR_CUDA : CE_ERR_OTHER;
+  }
+}
+
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+void copy_out(const std::string& s, char* buf, size_t cap) {
+  if (!buf || s.size() + 1 > cap) throw std::runtime_error("output buffer too small (need " + std::to_string(s.size() + 1) + ")");
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+}
+
+std::vector<std::vector<int64_t>> split_dims(const int64_t* dims, const int* ranks, int n) {
+  std::vector<std::vector<int64_t>> out;
+  int64_t pos = 0;
+  for (int i = 0; i < n; ++i) {
+    out.emplace_back(dims + pos, dims + pos + ranks[i]);
+    pos += ranks[i];
+  }
+  return out;
+}
+
+void split_u128(u128 v, uint64_t* lo, uint64_t* hi) {
+  *lo = static_cast<uint64_t>(v);
+  if (hi) *hi = static_cast<uint64_t>(v >> 64);
+}
+
+// A one-node plan for pairwise_eval with the planner's node construction.
+EvaluationPlan pairwise_plan(const char* expr, const int64_t* dims, const int* ranks, const char* mode) {
+  EvaluationPlan plan;
+  plan.spec = parse(expr);
+  if (plan.spec.inputs.size() != 2) throw ShapeError("pairwise expression must have exactly two inputs");
+  plan.env = make_shape_env(plan.spec, split_dims(dims, ranks, 2));
+  plan.modes = resolve_conv_modes(plan.spec, conv_mode_from_string(mode));
+  std::set<Atom> keep(plan.spec.output.begin(), plan.spec.output.end());
+  PlanNode node;
+  node.left = 0;
+  node.right = 1;
+  node.op = make_pairwise_op(plan.spec.inputs[0], plan.env.dims[0], plan.spec.inputs[1], plan.env.dims[1], keep,
+                             plan.modes, plan.spec.output);
+  node.cost = pairwise_cost(node.op, CostMode::Inference).total;
+  plan.total_cost = node.cost;
+  plan.root_subs = node.op.result;
+  plan.root_dims = node.op.result_dims;
+  plan.peak_intermediate_elements = static_cast<uint64_t>(node.op.result_elements());
+  plan.nodes.push_back(std::move(node));
+  return plan;
+}
+
+void fill_stats(const Executor& ex, ce_exec_stats* st, bool bwd) {
+  if (!st) return;
+  u128 m = 0;
+  for (const auto& n : ex.plan().nodes) m = add_checked(m, flops_actual(n.op));
+  split_u128(m, &st->multiplications_lo, &st->multiplications_hi);
+  st->peak_intermediate_elements = ex.plan().peak_intermediate_elements;
+  st->kernels_launched = ex.last_launches();
+  st->tc_steps = ex.tc_steps(bwd);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ce_last_error(void) { return g_err.c_str(); }
+const char* ce_version(void) { return "ce 0.1 (sm_100a, tcgen05 tf32 + fp32 simt)"; }
+
+ce_status ce_parse(const char* expr, char* rendered, size_t rendered_cap, char* classes, size_t classes_cap) {
+  return guard([&] {
+    ExpressionSpec spec = parse(expr);
+    copy_out(render(spec), rendered, rendered_cap);
+    std::string s;
+    for (const auto& [a, c] : classify(spec)) s += (s.empty() ? "" : " ") + a.name + ":" + to_string(c);
+    copy_out(s, classes, classes_cap);
+  });
+}
+
+ce_status ce_plan_create(const char* expr, const int64_t* dims, const int* ranks, int n_inputs, const char* mode,
+                         const char* cost_mode, int strategy, ce_plan** out) {
+  return guard([&] {
+    ExpressionSpec spec = parse(expr);
+    ShapeEnv env = make_shape_env(spec, split_dims(dims, ranks, n_inputs));
+    ConvModeMap modes = resolve_conv_modes(spec, conv_mode_from_string(mode));
+    CostMode cm = cost_mode_from_string(cost_mode);
+    auto p = std::make_unique<ce_plan>();
+    if (strategy == CE_PLAN_LEFT_TO_RIGHT) {
+      p->plan = left_to_right(spec, env, modes, cm);
+    } else {
+      OptimalOptions o;
+      o.cost_capped = strategy == CE_PLAN_OPTIMAL_CAPPED;
+      p->plan = optimal(spec, env, modes, cm, o);
+    }
+    *out = p.release();
+  });
+}
+
+ce_status ce_plan_from_joins(const char* expr, const int64_t* dims, const int* ranks, int n_inputs, const char* mode,
+                             const char* cost_mode, const int* joins, int n_joins, ce_plan** out) {
+  return guard([&] {
+    ExpressionSpec spec = parse(expr);
+    ShapeEnv env = make_shape_env(spec, split_dims(dims, ranks, n_inputs));
+    std::vector<std::pair<int, int>> j;
+    for (int i = 0; i < n_joins; ++i) j.push_back({joins[2 * i], joins[2 * i + 1]});
+    auto p = std::make_unique<ce_plan>();
+    p->plan = plan_from_joins(spec, env, resolve_conv_modes(spec, conv_mode_from_string(mode)),
+                              cost_mode_from_string(cost_mode), j);
+    *out = p.release();
+  });
+}
+
+void ce_plan_destroy(ce_plan* plan) { delete plan; }
+
+ce_status ce_plan_json(const ce_plan* plan, char* buf, size_t cap) {
+  return guard([&] { copy_out(plan_to_json(plan->plan), buf, cap); });
+}
+
+ce_status ce_plan_tree_encoding(const ce_plan* plan, char* buf, size_t cap) {
+  return guard([&] { copy_out(plan->plan.nodes.empty() ? std::string("0") : tree_encoding(plan->plan), buf, cap); });
+}
+
+ce_status ce_plan_get_info(const ce_plan* plan, ce_plan_info* info) {
+  return guard([&] {
+    const EvaluationPlan& p = plan->plan;
+    *info = ce_plan_info{};
+    info->n_inputs = static_cast<int>(p.spec.inputs.size());
+    info->n_nodes = static_cast<int>(p.nodes.size());
+    std::vector<int64_t> od;
+    if (p.nodes.empty()) {
+      for (const auto& a : p.spec.output) od.push_back(p.env.dim_of(p.spec, a));
+    } else {
+      const auto& op = p.nodes.back().op;
+      for (const auto& a : p.spec.output) od.push_back(op.result_dims[static_cast<std::size_t>(find_atom(op.result, a))]);
+    }
+    if (od.size() > 16) throw ShapeError("output rank above 16");
+    info->out_rank = static_cast<int>(od.size());
+    for (std::size_t i = 0; i < od.size(); ++i) info->out_dims[i] = od[i];
+    split_u128(p.total_cost, &info->total_cost_lo, &info->total_cost_hi);
+    split_u128(plan_cost(p, CostMode::Inference), &info->inference_cost_lo, &info->inference_cost_hi);
+    split_u128(plan_cost(p, CostMode::Training), &info->training_cost_lo, &info->training_cost_hi);
+    u128 f = 0;
+    for (const auto& n : p.nodes) f = add_checked(f, flops_actual(n.op));
+    split_u128(f, &info->flops_actual_lo, &info->flops_actual_hi);
+    info->peak_intermediate_elements = p.peak_intermediate_elements;
+  });
+}
+
+ce_status ce_plan_node(const ce_plan* plan, int node, int* left, int* right, char* result_subs, size_t cap,
+                       uint64_t* flops_actual_lo, uint64_t* cost_lo) {
+  return guard([&] {
+    const auto& n = plan->plan.nodes.at(static_cast<std::size_t>(node));
+    *left = n.left;
+    *right = n.right;
+    copy_out(render(n.op.result), result_subs, cap);
+    split_u128(flops_actual(n.op), flops_actual_lo, nullptr);
+    split_u128(n.cost, cost_lo, nullptr);
+  });
+}
+
+ce_status ce_layer_expression(const char* kind, const int64_t* t_factors, int n_t, const int64_t* s_factors, int n_s,
+                              int64_t filter_h, int64_t filter_w, int64_t feature_h, int64_t feature_w, int64_t batch,
+                              const int64_t* ranks, int n_ranks, double cr, char* expr_out, size_t expr_cap,
+                              int64_t* dims_out, int dims_cap, int* ranks_of_input, int* n_inputs, int64_t* ranks_out,
+                              int* n_ranks_out, uint64_t* param_count_out) {
+  return guard([&] {
+    LayerSpec l;
+    l.kind = layer_kind_from_string(kind);
+    l.t_factors.assign(t_factors, t_factors + n_t);
+    l.s_factors.assign(s_factors, s_factors + n_s);
+    l.filter_h = filter_h;
+    l.filter_w = filter_w;
+    l.feature_h = feature_h;
+    l.feature_w = feature_w;
+    l.batch = batch;
+    if (cr > 0) {
+      l.ranks.assign(rank_slot_count(l.kind, l.order()), 1);
+      l = with_compression_rank(l, cr);
+    } else {
+      l.ranks.assign(ranks, ranks + n_ranks);
+    }
+    LayerExpression ex = expression(l);
+    copy_out(render(ex.spec), expr_out, expr_cap);
+    int pos = 0;
+    for (std::size_t i = 0; i < ex.env.dims.size(); ++i) {
+      ranks_of_input[i] = static_cast<int>(ex.env.dims[i].size());
+      for (int64_t d : ex.env.dims[i]) {
+        if (pos >= dims_cap) throw std::runtime_error("dims_out too small");
+        dims_out[pos++] = d;
+      }
+    }
+    *n_inputs = static_cast<int>(ex.env.dims.size());
+    for (std::size_t i = 0; i < l.ranks.size(); ++i) ranks_out[i] = l.ranks[i];
+    *n_ranks_out = static_cast<int>(l.ranks.size());
+    split_u128(param_count(l), param_count_out, nullptr);
+  });
+}
+
+ce_status ce_ctx_create(int device, const ce_options* opts, ce_ctx** out) {
+  return guard([&] {
+    auto c = std::make_unique<ce_ctx>();
+    c->device = device;
+    if (opts) c->opts = *opts;
+    cuda_ok(cudaSetDevice(device), "cudaSetDevice");
+    if (c->opts.stream) {
+      c->stream = static_cast<cudaStream_t>(c->opts.stream);
+    } else {
+      cuda_ok(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      c->own_stream = true;
+    }
+    *out = c.release();
+  });
+}
+
+void ce_ctx_destroy(ce_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+void* ce_ctx_stream(ce_ctx* ctx) { return ctx->stream; }
+
+ce_status ce_ctx_synchronize(ce_ctx* ctx) {
+  return guard([&] { cuda_ok(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize"); });
+}
+
+ce_status ce_fill_random(ce_ctx* ctx, float* dst, int64_t n, uint64_t seed) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cuda_ok(ce_launch_fill(dst, n, seed, ctx->stream), "fill_random");
+  });
+}
+
+ce_status ce_executor_create(ce_ctx* ctx, const ce_plan* plan, int want_backward, ce_executor** out) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
+    auto e = std::make_unique<ce_executor>();
+    e->ctx = ctx;
+    ExecConfig cfg;
+    cfg.math = ctx->opts.math;
+    e->ex = std::make_unique<Executor>(plan->plan, want_backward != 0, cfg);
+    *out = e.release();
+  });
+}
+
+void ce_executor_destroy(ce_executor* ex) { delete ex; }
+
+ce_status ce_execute(ce_executor* ex, const float* const* inputs, float* out, ce_exec_stats* stats) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ex->ctx->device), "cudaSetDevice");
+    ex->ex->forward(inputs, out, ex->ctx->stream);
+    fill_stats(*ex->ex, stats, false);
+  });
+}
+
+ce_status ce_backward(ce_executor* ex, const float* const* inputs, const float* dout, float* const* dinputs,
+                      ce_exec_stats* stats) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ex->ctx->device), "cudaSetDevice");
+    ex->ex->backward(inputs, dout, dinputs, ex->ctx->stream);
+    fill_stats(*ex->ex, stats, true);
+  });
+}
+
+ce_status ce_execute_host(ce_executor* ex, const float* const* host_inputs, float* host_out) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ex->ctx->device), "cudaSetDevice");
+    const EvaluationPlan& p = ex->ex->plan();
+    cudaStream_t s = ex->ctx->stream;
+    std::vector<float*> dev(p.spec.inputs.size());
+    for (std::size_t i = 0; i < dev.size(); ++i) {
+      const size_t bytes = static_cast<size_t>(element_count(p.env.dims[i])) * 4;
+      cuda_ok(cudaMallocAsync(&dev[i], bytes, s), "cudaMallocAsync");
+      cuda_ok(cudaMemcpyAsync(dev[i], host_inputs[i], bytes, cudaMemcpyHostToDevice, s), "H2D");
+    }
+    const size_t obytes = static_cast<size_t>(element_count(ex->ex->output_dims())) * 4;
+    float* dout = nullptr;
+    cuda_ok(cudaMallocAsync(&dout, obytes, s), "cudaMallocAsync");
+    ex->ex->forward(dev.data(), dout, s);
+    cuda_ok(cudaMemcpyAsync(host_out, dout, obytes, cudaMemcpyDeviceToHost, s), "D2H");
+    for (float* d : dev) cudaFreeAsync(d, s);
+    cudaFreeAsync(dout, s);
+    cuda_ok(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  });
+}
+
+ce_status ce_pairwise_eval(ce_ctx* ctx, const char* expr, const int64_t* dims, const int* ranks, const char* mode,
+                           const float* a, const float* b, float* out) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ExecConfig cfg;
+    cfg.math = ctx->opts.math;
+    Executor ex(pairwise_plan(expr, dims, ranks, mode), false, cfg);
+    const float* ins[2] = {a, b};
+    ex.forward(ins, out, ctx->stream);
+    cuda_ok(cudaStreamSynchronize(ctx->stream), "pairwise_eval");
+  });
+}
+
+ce_status ce_pairwise_grad(ce_ctx* ctx, const char* expr, const int64_t* dims, const int* ranks, const char* mode,
+                           const float* a, const float* b, const float* dout, float* da, float* db) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ExecConfig cfg;
+    cfg.math = ctx->opts.math;
+    Executor ex(pairwise_plan(expr, dims, ranks, mode), true, cfg);
+    const float* ins[2] = {a, b};
+    float* dins[2] = {da, db};
+    // the backward of a single node reads only the operands, not the forward result
+    ex.backward(ins, dout, dins, ctx->stream);
+    cuda_ok(cudaStreamSynchronize(ctx->stream), "pairwise_grad");
+  });
+}
+
+}  // extern "C"

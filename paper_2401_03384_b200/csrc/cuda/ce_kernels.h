@@ -1,0 +1,11 @@
+// Host-side launchers for every kernel family (all stream-ordered, no syncs).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "ce_device.h"
+
+cudaError_t ce_launch_direct(const CeSimtDesc& d, const float* A, const float* B, float* C, cudaStream_t s);
+cudaError_t ce_launch_tiled(const CeSimtDesc& d, const float* A, const float* B, float* C, int a_kfast,
+                            int b_kfast, cudaStream_t s);
+cudaError_t ce_launch_fill(float* dst, int64_t n, uint64_t seed, cudaStream_t s);

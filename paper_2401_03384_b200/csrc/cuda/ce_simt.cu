@@ -1,0 +1,295 @@
+// SIMT kernel families for the generalized pairwise step (see ce_device.h).
+//
+//  * ce_direct_kernel — one thread per output element, odometer over the K
+//    vars.  Used where K is tiny (depthwise / batch-only convolutions such as
+//    CP's `bhwr,rh->bhwr`, Hadamard and outer products),
+//    for unary steps (sum_unique_modes kernels.cpp:144-187, broadcast of its
+//    adjoint, permutes) and as the universal fallback for any index map
+//    (Circular wrap, >2 conv axes).  HBM-bound by construction.
+//  * ce_tiled_kernel — 64x64x16 shared-memory tiled FP32 gather-GEMM for large-K
+//    steps the tensor-core path does not take (anchor + fallback of family a/b1).
+//  * ce_fill_kernel — SplitMix64 (reference tensor.cpp:107-130) in closed form.
+#include <cuda_runtime.h>
+
+#include "ce_device.h"
+#include "ce_kernels.h"
+
+namespace {
+
+__device__ __forceinline__ bool gather_index(const CeGather& g, int64_t p, int64_t q, int64_t* off) {
+  int64_t x = g.sp * p + g.sq * q + g.c;
+  if (g.wrap) {
+    x %= g.extent;
+    if (x < 0) x += g.extent;
+  } else if (x < 0 || x >= g.extent) {
+    return false;
+  }
+  *off = x * g.stride;
+  return true;
+}
+
+// ----------------------------------------------------------------------------- direct
+__global__ void __launch_bounds__(256) ce_direct_kernel(const CeSimtDesc d, const float* __restrict__ A,
+                                                        const float* __restrict__ B, float* __restrict__ C) {
+  const CeProblem& p = d.p;
+  const int64_t total = d.Z * d.M * d.N;
+  for (int64_t flat = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; flat < total;
+       flat += (int64_t)gridDim.x * blockDim.x) {
+    int64_t val[CE_MAX_VARS];
+    int64_t rest = flat, offA = 0, offB = 0, offC = 0;
+    for (int i = 0; i < d.nout; ++i) {
+      const int v = d.ov[i];
+      const int64_t e = p.ext[v];
+      val[v] = rest % e;
+      rest /= e;
+      offA += val[v] * p.sa[v];
+      offB += val[v] * p.sb[v];
+      offC += val[v] * p.sc[v];
+    }
+    for (int i = 0; i < d.nk; ++i) val[d.kv[i]] = 0;
+    float acc = 0.f;
+    int64_t kA = 0, kB = 0;
+    for (int64_t k = 0; k < d.K; ++k) {
+      int64_t a_off = offA + kA, b_off = offB + kB;
+      bool ok = true;
+      for (int g = 0; g < p.ng_a && ok; ++g) {
+        int64_t o;
+        ok = gather_index(p.ga[g], val[p.ga[g].pv], val[p.ga[g].qv], &o);
+        a_off += o;
+      }
+      for (int g = 0; g < p.ng_b && ok; ++g) {
+        int64_t o;
+        ok = gather_index(p.gb[g], val[p.gb[g].pv], val[p.gb[g].qv], &o);
+        b_off += o;
+      }
+      if (ok) acc += p.unary ? __ldg(A + a_off) : __ldg(A + a_off) * __ldg(B + b_off);
+      // odometer over K vars (first var fastest)
+      for (int i = 0; i < d.nk; ++i) {
+        const int v = d.kv[i];
+        if (++val[v] < p.ext[v]) {
+          kA += p.sa[v];
+          kB += p.sb[v];
+          break;
+        }
+        kA -= (p.ext[v] - 1) * p.sa[v];
+        kB -= (p.ext[v] - 1) * p.sb[v];
+        val[v] = 0;
+      }
+    }
+    if (p.accumulate)
+      C[offC] += acc;
+    else
+      C[offC] = acc;
+  }
+}
+
+// ----------------------------------------------------------------------------- tiled
+constexpr int TM = 64, TN = 64, TK = 16;
+
+__device__ __forceinline__ void decompose(int64_t x, const int32_t* vars, int n, const int64_t* ext,
+                                          int64_t* out_vals) {
+  for (int i = 0; i < n; ++i) {
+    const int64_t e = ext[vars[i]];
+    out_vals[i] = x % e;
+    x /= e;
+  }
+}
+
+__global__ void __launch_bounds__(256) ce_tiled_kernel(const CeSimtDesc d, const float* __restrict__ A,
+                                                       const float* __restrict__ B, float* __restrict__ C,
+                                                       int a_kfast, int b_kfast) {
+  const CeProblem& p = d.p;
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
+  __shared__ int64_t mOffA[TM], mOffC[TM], nOffB[TN], nOffC[TN];
+  __shared__ int64_t mP[TM][CE_MAX_GATHER], nP[TN][CE_MAX_GATHER];
+  __shared__ int64_t kOffA[TK], kOffB[TK];
+  __shared__ int64_t kQA[TK][CE_MAX_GATHER], kQB[TK][CE_MAX_GATHER];
+  __shared__ int64_t zA, zB, zC;
+
+  const int tid = threadIdx.x;
+  const int64_t m0 = (int64_t)blockIdx.x * TM, n0 = (int64_t)blockIdx.y * TN;
+  int64_t vals[CE_MAX_VARS];
+
+  for (int64_t z = blockIdx.z; z < d.Z; z += gridDim.z) {
+    __syncthreads();
+    if (tid == 0) {
+      decompose(z, d.zv, d.nz, p.ext, vals);
+      int64_t a = 0, b = 0, c = 0;
+      for (int i = 0; i < d.nz; ++i) {
+        a += vals[i] * p.sa[d.zv[i]];
+        b += vals[i] * p.sb[d.zv[i]];
+        c += vals[i] * p.sc[d.zv[i]];
+      }
+      zA = a;
+      zB = b;
+      zC = c;
+    }
+    if (tid < TM) {
+      const int64_t m = m0 + tid;
+      int64_t a = 0, c = 0;
+      if (m < d.M) {
+        decompose(m, d.mv, d.nm, p.ext, vals);
+        for (int i = 0; i < d.nm; ++i) {
+          a += vals[i] * p.sa[d.mv[i]];
+          c += vals[i] * p.sc[d.mv[i]];
+        }
+        for (int g = 0; g < p.ng_a; ++g)
+          for (int i = 0; i < d.nm; ++i)
+            if (d.mv[i] == p.ga[g].pv) mP[tid][g] = vals[i];
+      }
+      mOffA[tid] = a;
+      mOffC[tid] = c;
+    } else if (tid < TM + TN) {
+      const int j = tid - TM;
+      const int64_t n = n0 + j;
+      int64_t b = 0, c = 0;
+      if (n < d.N) {
+        decompose(n, d.nvv, d.nn, p.ext, vals);
+        for (int i = 0; i < d.nn; ++i) {
+          b += vals[i] * p.sb[d.nvv[i]];
+          c += vals[i] * p.sc[d.nvv[i]];
+        }
+        for (int g = 0; g < p.ng_b; ++g)
+          for (int i = 0; i < d.nn; ++i)
+            if (d.nvv[i] == p.gb[g].pv) nP[j][g] = vals[i];
+      }
+      nOffB[j] = b;
+      nOffC[j] = c;
+    }
+    const int tx = tid % 16, ty = tid / 16;
+    float acc[4][4] = {};
+
+    for (int64_t k0 = 0; k0 < d.K; k0 += TK) {
+      __syncthreads();
+      if (tid < TK) {
+        const int64_t k = k0 + tid;
+        int64_t a = 0, b = 0;
+        if (k < d.K) {
+          decompose(k, d.kv, d.nk, p.ext, vals);
+          for (int i = 0; i < d.nk; ++i) {
+            a += vals[i] * p.sa[d.kv[i]];
+            b += vals[i] * p.sb[d.kv[i]];
+          }
+          for (int g = 0; g < p.ng_a; ++g)
+            for (int i = 0; i < d.nk; ++i)
+              if (d.kv[i] == p.ga[g].qv) kQA[tid][g] = vals[i];
+          for (int g = 0; g < p.ng_b; ++g)
+            for (int i = 0; i < d.nk; ++i)
+              if (d.kv[i] == p.gb[g].qv) kQB[tid][g] = vals[i];
+        }
+        kOffA[tid] = a;
+        kOffB[tid] = b;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < (TM * TK) / 256; ++r) {
+        const int e = tid + r * 256;
+        const int mi = a_kfast ? e / TK : e % TM;
+        const int ki = a_kfast ? e % TK : e / TM;
+        float v = 0.f;
+        if (m0 + mi < d.M && k0 + ki < d.K) {
+          int64_t off = zA + mOffA[mi] + kOffA[ki];
+          bool ok = true;
+          for (int g = 0; g < p.ng_a && ok; ++g) {
+            int64_t o;
+            ok = gather_index(p.ga[g], mP[mi][g], kQA[ki][g], &o);
+            off += o;
+          }
+          if (ok) v = __ldg(A + off);
+        }
+        As[ki][mi] = v;
+      }
+#pragma unroll
+      for (int r = 0; r < (TN * TK) / 256; ++r) {
+        const int e = tid + r * 256;
+        const int ni = b_kfast ? e / TK : e % TN;
+        const int ki = b_kfast ? e % TK : e / TN;
+        float v = 0.f;
+        if (n0 + ni < d.N && k0 + ki < d.K) {
+          int64_t off = zB + nOffB[ni] + kOffB[ki];
+          bool ok = true;
+          for (int g = 0; g < p.ng_b && ok; ++g) {
+            int64_t o;
+            ok = gather_index(p.gb[g], nP[ni][g], kQB[ki][g], &o);
+            off += o;
+          }
+          if (ok) v = __ldg(B + off);
+        }
+        Bs[ki][ni] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < TK; ++kk) {
+        float a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int mi = ty * 4 + i;
+      if (m0 + mi >= d.M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int ni = tx * 4 + j;
+        if (n0 + ni >= d.N) continue;
+        float* dst = C + zC + mOffC[mi] + nOffC[ni];
+        if (p.accumulate)
+          *dst += acc[i][j];
+        else
+          *dst = acc[i][j];
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- fill
+__global__ void ce_fill_kernel(float* __restrict__ dst, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    const double u = (double)(z >> 11) * 0x1.0p-53;
+    dst[i] = (float)(2.0 * u - 1.0);
+  }
+}
+
+int grid_for(int64_t work, int threads) {
+  int64_t blocks = (work + threads - 1) / threads;
+  const int64_t cap = 148 * 32;  // 32 resident 256-thread waves' worth of CTAs, grid-stride beyond
+  if (blocks > cap) blocks = cap;
+  return blocks < 1 ? 1 : (int)blocks;
+}
+
+}  // namespace
+
+cudaError_t ce_launch_direct(const CeSimtDesc& d, const float* A, const float* B, float* C, cudaStream_t s) {
+  const int64_t total = d.Z * d.M * d.N;
+  if (total == 0) return cudaSuccess;
+  ce_direct_kernel<<<grid_for(total, 256), 256, 0, s>>>(d, A, B, C);
+  return cudaGetLastError();
+}
+
+cudaError_t ce_launch_tiled(const CeSimtDesc& d, const float* A, const float* B, float* C, int a_kfast,
+                            int b_kfast, cudaStream_t s) {
+  if (d.Z * d.M * d.N == 0) return cudaSuccess;
+  dim3 grid((unsigned)((d.M + TM - 1) / TM), (unsigned)((d.N + TN - 1) / TN),
+            (unsigned)(d.Z < 65535 ? d.Z : 65535));
+  if (grid.y > 65535) return cudaErrorInvalidConfiguration;
+  ce_tiled_kernel<<<grid, 256, 0, s>>>(d, A, B, C, a_kfast, b_kfast);
+  return cudaGetLastError();
+}
+
+cudaError_t ce_launch_fill(float* dst, int64_t n, uint64_t seed, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  ce_fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, n, seed);
+  return cudaGetLastError();
+}

@@ -1,0 +1,88 @@
+// Device plan executor: the B200 replacement for execute()
+// (/root/reference/proj/src/sequencer.cpp:403-447) and, per node, for
+// pairwise_eval (kernels.cpp:425-470), plus the backward pass the reference
+// does not have.  A plan is compiled ONCE into a flat list of kernel steps over
+// symbolic buffers (inputs / output / workspace offsets); each call only binds
+// pointers and launches, stream-ordered, optionally replayed as a CUDA graph.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../cuda/ce_device.h"
+#include "../cuda/ce_tc.h"
+#include "ce_lower.hpp"
+#include "ce_plan.hpp"
+
+namespace ce {
+
+struct BufRef {
+  enum Kind { kNone, kInput, kOutput, kWork, kDOut, kDInput } kind = kNone;
+  int64_t index = 0;  // input index or workspace offset (bytes)
+};
+
+struct Step {
+  enum Kind { kDirect, kTiled, kTc, kZero } kind = kDirect;
+  CeSimtDesc desc{};
+  int a_kfast = 0, b_kfast = 0;
+  TcPlan tc{};
+  BufRef a, b, c;
+  int64_t zero_elems = 0;
+  int node = -1;
+  std::string label;
+};
+
+struct ExecConfig {
+  int math = 0;  // 0 auto (tensor cores where mappable), 1 FP32 SIMT only
+};
+
+class Executor {
+ public:
+  Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cfg);
+  ~Executor();
+  Executor(const Executor&) = delete;
+  Executor& operator=(const Executor&) = delete;
+
+  void forward(const float* const* inputs, float* out, cudaStream_t s);
+  void backward(const float* const* inputs, const float* dout, float* const* dinputs, cudaStream_t s);
+
+  const EvaluationPlan& plan() const { return plan_; }
+  int64_t workspace_bytes() const { return ws_bytes_; }
+  int last_launches() const { return last_launches_; }
+  int tc_steps(bool bwd) const;
+  const std::vector<Step>& forward_steps() const { return fwd_; }
+  const std::vector<Step>& backward_steps() const { return bwd_; }
+  std::vector<int64_t> output_dims() const;
+
+ private:
+  int64_t alloc(int64_t elems);
+  void add_problem(std::vector<Step>& list, const CeProblem& p, BufRef a, BufRef b, BufRef c, int node,
+                   const std::string& label);
+  void build_forward();
+  void build_backward();
+  void run(const std::vector<Step>& steps, cudaStream_t s);
+  float* resolve(const BufRef& r) const;
+
+  EvaluationPlan plan_;
+  bool want_backward_;
+  ExecConfig cfg_;
+  int n_ = 0;
+  // per operand id (inputs then nodes): view as consumed by its node (after self-sum)
+  std::vector<View> id_view_;      // full view of operand id (inputs dense, nodes padded)
+  std::vector<BufRef> id_ref_;
+  std::vector<View> red_view_[2];  // per node, post-self-sum view of left/right
+  std::vector<BufRef> red_ref_[2];
+  std::vector<Step> fwd_, bwd_;
+  int64_t ws_bytes_ = 0;
+  char* ws_ = nullptr;
+  // bound per call
+  std::vector<const float*> inputs_;
+  float* out_ = nullptr;
+  const float* dout_ = nullptr;
+  std::vector<float*> dinputs_;
+  int last_launches_ = 0;
+};
+
+}  // namespace ce

@@ -1,0 +1,172 @@
+"""Device executor bindings (torch tensors as device-memory plumbing only).
+
+Context  -> ce_ctx   (one per GPU; work ordered on torch's current stream)
+Executor -> ce_executor (plan compiled once into kernel steps + workspace)
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .api import Plan, _dims_arg
+
+MATH = {"auto": 0, "tf32": 0, "fp32": 1, "simt": 1}
+
+
+class Context:
+    """ce_ctx_create: binds a device and a stream (default: torch's current stream)."""
+
+    def __init__(self, device: int = 0, math: str = "auto", stream: Optional[torch.cuda.Stream] = None):
+        self.device = device
+        self.math = math
+        torch.cuda.set_device(device)
+        st = stream if stream is not None else torch.cuda.current_stream(device)
+        self.torch_stream = st
+        opts = _lib.Options(MATH[math], 0, ctypes.c_void_p(st.cuda_stream))
+        h = ctypes.c_void_p()
+        check(lib().ce_ctx_create(device, ctypes.byref(opts), ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def synchronize(self):
+        check(lib().ce_ctx_synchronize(self._h))
+
+    def fill_random(self, shape: Sequence[int], seed: int) -> torch.Tensor:
+        """fill_random (tensor.cpp:125-130) evaluated on the device, rounded to FP32."""
+        t = torch.empty(list(shape), dtype=torch.float32, device=f"cuda:{self.device}")
+        check(lib().ce_fill_random(self._h, ctypes.c_void_p(t.data_ptr()), t.numel(), ctypes.c_uint64(seed)))
+        return t
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().ce_ctx_destroy(self._h)
+            self._h = None
+
+
+def _ptrs(ts):
+    arr = (ctypes.c_void_p * len(ts))(*[ctypes.c_void_p(t.data_ptr()) if t is not None else None for t in ts])
+    return ctypes.cast(arr, _lib.c_fpp), arr
+
+
+def _check_inputs(plan: Plan, inputs):
+    if len(inputs) != plan.n_inputs:
+        raise _lib.ShapeError(3, "execute: wrong number of input tensors")
+    for i, (t, d) in enumerate(zip(inputs, plan.dims)):
+        if list(t.shape) != list(d):
+            raise _lib.ShapeError(3, f"execute: input {i} shape mismatch")
+        if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+            raise TypeError(f"input {i} must be a contiguous CUDA float32 tensor")
+
+
+class Executor:
+    """execute() (sequencer.cpp:403-447) + backward on one device."""
+
+    def __init__(self, ctx: Context, plan: Plan, backward: bool = False):
+        self.ctx, self.plan = ctx, plan
+        h = ctypes.c_void_p()
+        check(lib().ce_executor_create(ctx.handle, plan._h, int(backward), ctypes.byref(h)))
+        self._h = h
+        self.stats = _lib.ExecStats()
+
+    def execute(self, inputs: Sequence[torch.Tensor], out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        _check_inputs(self.plan, inputs)
+        if out is None:
+            out = torch.empty(self.plan.out_dims, dtype=torch.float32, device=inputs[0].device)
+        p, keep = _ptrs(list(inputs))
+        check(lib().ce_execute(self._h, p, ctypes.c_void_p(out.data_ptr()), ctypes.byref(self.stats)))
+        del keep
+        return out
+
+    def backward(self, inputs: Sequence[torch.Tensor], dout: torch.Tensor,
+                 needs: Optional[Sequence[bool]] = None) -> List[Optional[torch.Tensor]]:
+        _check_inputs(self.plan, inputs)
+        needs = needs or [True] * len(inputs)
+        grads = [torch.empty_like(t) if n else None for t, n in zip(inputs, needs)]
+        p, k1 = _ptrs(list(inputs))
+        g, k2 = _ptrs(grads)
+        dout = dout.contiguous()
+        check(lib().ce_backward(self._h, p, ctypes.c_void_p(dout.data_ptr()), g, ctypes.byref(self.stats)))
+        del k1, k2
+        return grads
+
+    def execute_host(self, host_inputs: Sequence["numpy.ndarray"], host_out: "numpy.ndarray"):  # noqa: F821
+        """H2D + execute + D2H + sync through the C-ABI (the end-to-end call)."""
+        arrs = [a for a in host_inputs]
+        ptrs = (ctypes.c_void_p * len(arrs))(*[ctypes.c_void_p(a.ctypes.data) for a in arrs])
+        check(lib().ce_execute_host(self._h, ctypes.cast(ptrs, _lib.c_fpp), ctypes.c_void_p(host_out.ctypes.data)))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().ce_executor_destroy(self._h)
+            self._h = None
+
+
+def pairwise_eval(ctx: Context, expr: str, a: torch.Tensor, b: torch.Tensor, mode: str = "same") -> torch.Tensor:
+    """pairwise_eval (kernels.cpp:425-470) for expr "L,R->RES|convs" (keep = RES, order RES)."""
+    from .api import Plan as _P  # result shape via a one-node plan
+    shape = _P.optimal(expr, [list(a.shape), list(b.shape)], mode).out_dims
+    out = torch.empty(shape, dtype=torch.float32, device=a.device)
+    d, r, _ = _dims_arg([list(a.shape), list(b.shape)])
+    check(lib().ce_pairwise_eval(ctx.handle, expr.encode(), d, r, mode.encode(), ctypes.c_void_p(a.data_ptr()),
+                                 ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(out.data_ptr())))
+    return out
+
+
+def pairwise_grad(ctx: Context, expr: str, a, b, dout, mode: str = "same"):
+    da, db = torch.empty_like(a), torch.empty_like(b)
+    d, r, _ = _dims_arg([list(a.shape), list(b.shape)])
+    check(lib().ce_pairwise_grad(ctx.handle, expr.encode(), d, r, mode.encode(), ctypes.c_void_p(a.data_ptr()),
+                                 ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(dout.contiguous().data_ptr()),
+                                 ctypes.c_void_p(da.data_ptr()), ctypes.c_void_p(db.data_ptr())))
+    return da, db
+
+
+# ----------------------------------------------------------------------------- autograd
+_PLAN_CACHE: dict = {}
+_CTX_CACHE: dict = {}
+
+
+def _context(device: int, math: str) -> Context:
+    key = (device, math, torch.cuda.current_stream(device).cuda_stream)
+    if key not in _CTX_CACHE:
+        _CTX_CACHE[key] = Context(device, math)
+    return _CTX_CACHE[key]
+
+
+def _executor(expr, shapes, mode, cost_mode, device, math):
+    key = (expr, tuple(tuple(s) for s in shapes), mode, cost_mode, device, math)
+    if key not in _PLAN_CACHE:
+        plan = Plan.optimal(expr, shapes, mode, cost_mode)
+        _PLAN_CACHE[key] = Executor(_context(device, math), plan, backward=True)
+    return _PLAN_CACHE[key]
+
+
+class _ConvEinsumFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, expr, mode, math, *tensors):
+        ts = [t.contiguous() for t in tensors]
+        ex = _executor(expr, [list(t.shape) for t in ts], mode, "training", ts[0].device.index or 0, math)
+        out = ex.execute(ts)
+        ctx.ex = ex
+        ctx.save_for_backward(*ts)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        ts = ctx.saved_tensors
+        # re-run forward so the executor's intermediates match these inputs
+        ctx.ex.execute(list(ts))
+        grads = ctx.ex.backward(list(ts), dout.contiguous(), [t.requires_grad for t in ts] if False else None)
+        return (None, None, None, *grads)
+
+
+def conv_einsum(expr: str, *tensors: torch.Tensor, mode: str = "same", math: str = "auto") -> torch.Tensor:
+    """The paper's call form conv_einsum("...", T1, T2, ...), differentiable."""
+    return _ConvEinsumFn.apply(expr, mode, math, *tensors)

@@ -1,0 +1,210 @@
+"""GPU parity: every path through libce (C-ABI) against the FP64 oracle.
+
+Tolerances (normwise max |y - y*| / max |y*|, SURVEY §8(c) C4 calibration):
+  FP32 SIMT ("fp32" context)                 forward 1e-5,  gradients 1e-5
+  auto (TF32 tensor cores where mapped)      forward 5e-3,  gradients 1e-2
+Inputs are SplitMix64 (fill_random) rounded to FP32; the oracle is fed the same
+rounded values in FP64.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import np_oracle as npo
+from tests.spec_gen import random_spec
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = {"fp32": (1e-5, 1e-5), "auto": (5e-3, 1e-2)}
+
+
+def load(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def nerr(y, ref):
+    y = np.asarray(y, dtype=np.float64).ravel()
+    ref = np.asarray(ref, dtype=np.float64).ravel()
+    scale = max(np.abs(ref).max(), 1e-30)
+    return float(np.abs(y - ref).max() / scale)
+
+
+def f32(x):
+    return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+
+def dev(x):
+    return torch.tensor(np.asarray(x, dtype=np.float32), device="cuda:0").contiguous()
+
+
+@pytest.fixture(params=["fp32", "auto"])
+def any_ctx(request, ctx, ctx_simt):
+    return (ctx_simt if request.param == "fp32" else ctx), request.param
+
+
+def test_fill_random_device(ctx):
+    t = ctx.fill_random([37, 41], 1234)
+    ref = npo.fill_random([37, 41], 1234).astype(np.float32)
+    assert np.array_equal(t.cpu().numpy(), ref)
+
+
+def test_pairwise_golden(any_ctx):
+    from paper_2401_03384_b200.device import pairwise_eval
+    c_, mode = any_ctx
+    tol = TOL[mode][0]
+    for c in load("pairwise.json"):
+        if "seeds" in c:
+            a = npo.fill_random(c["ldims"], c["seeds"][0])
+            b = npo.fill_random(c["rdims"], c["seeds"][1])
+            op = npo.pairwise_from_expr(c["expr"], c["ldims"], c["rdims"], c["mode"])
+            ref = npo.pairwise_eval(op, f32(a), f32(b))
+        else:
+            a, b = np.array(c["a"], float), np.array(c["b"], float)
+            ref = np.array(c["out"]).reshape(c["rdims_out"])
+        out = pairwise_eval(c_, c["expr"], dev(a).reshape(c["ldims"]), dev(b).reshape(c["rdims"]), c["mode"])
+        torch.cuda.synchronize()
+        assert list(out.shape) == list(c["rdims_out"])
+        assert nerr(out.cpu().numpy(), ref) <= tol, (c["expr"], c["mode"])
+
+
+def test_pairwise_grad_random(any_ctx):
+    from paper_2401_03384_b200.device import pairwise_grad
+    c_, mode = any_ctx
+    tol = TOL[mode][1]
+    rng = np.random.default_rng(11)
+    n = 0
+    while n < 120:
+        expr, dims, cmode = random_spec(rng, 2, 2, dmax=6)
+        try:
+            op = npo.pairwise_from_expr(expr, dims[0], dims[1], cmode)
+        except AssertionError:
+            continue
+        if any(ax.mode == "valid" and ax.feature < ax.filter for ax in op.conv):
+            continue
+        a = f32(rng.uniform(-1, 1, dims[0]))
+        b = f32(rng.uniform(-1, 1, dims[1]))
+        dc = f32(rng.uniform(-1, 1, op.result_dims))
+        da_ref, db_ref = npo.pairwise_grad(op, a, b, dc)
+        da, db = pairwise_grad(c_, expr, dev(a).reshape(dims[0]), dev(b).reshape(dims[1]),
+                               dev(dc).reshape(op.result_dims), cmode)
+        torch.cuda.synchronize()
+        assert nerr(da.cpu().numpy(), da_ref) <= tol, (expr, cmode, "dA")
+        assert nerr(db.cpu().numpy(), db_ref) <= tol, (expr, cmode, "dB")
+        n += 1
+
+
+def _run_plan(c_, expr, dims, mode, ins, dout=None, cost_mode="inference"):
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import Executor
+    plan = ce.optimal(expr, dims, mode, cost_mode)
+    ex = Executor(c_, plan, backward=dout is not None)
+    xs = [dev(x).reshape(d) for x, d in zip(ins, dims)]
+    out = ex.execute(xs)
+    grads = ex.backward(xs, dev(dout).reshape(plan.out_dims)) if dout is not None else None
+    torch.cuda.synchronize()
+    nodes = [(n["left"], n["right"], n["result"]) for n in json.loads(plan.to_json())["nodes"]]
+    return plan, nodes, out.cpu().numpy(), grads, ex
+
+
+def test_execute_golden(any_ctx):
+    c_, mode = any_ctx
+    for c in load("execute.json"):
+        ins = [f32(npo.fill_random(d, s)) for d, s in zip(c["dims"], c["seeds"])]
+        plan, nodes, out, _, _ = _run_plan(c_, c["expr"], c["dims"], c["mode"], ins)
+        ref, _ = npo.execute(c["expr"], c["dims"], nodes, ins, c["mode"])
+        assert list(out.shape) == c["shape"]
+        assert nerr(out, ref) <= TOL[mode][0], c["expr"]
+
+
+def test_backward_random_specs(any_ctx):
+    c_, mode = any_ctx
+    rng = np.random.default_rng(21)
+    n = 0
+    while n < 60:
+        expr, dims, cmode = random_spec(rng, 1, 5, dmax=4)
+        import paper_2401_03384_b200 as ce
+        try:
+            plan = ce.optimal(expr, dims, cmode)
+        except ce.CeError:
+            continue
+        ins = [f32(rng.uniform(-1, 1, d)) for d in dims]
+        dout = f32(rng.uniform(-1, 1, plan.out_dims))
+        plan, nodes, out, grads, _ = _run_plan(c_, expr, dims, cmode, ins, dout)
+        ref_out, _ = npo.execute(expr, dims, nodes, ins, cmode)
+        ref_g = npo.backward(expr, dims, nodes, ins, dout, cmode)
+        assert nerr(out, ref_out) <= TOL[mode][0], expr
+        for i, (g, r) in enumerate(zip(grads, ref_g)):
+            assert nerr(g.cpu().numpy(), r) <= TOL[mode][1], (expr, i)
+        n += 1
+
+
+LAYER_CASES = [
+    # (name, kind, T, S, Hp, B, cr or ranks)
+    ("cfg1 CP", "cp", 64, 64, 32, 8, [16]),
+    ("cfg2 TK cr0.1", "tk", 256, 256, 14, 128, 0.1),
+    ("cfg2 TT cr0.1", "tt", 256, 256, 14, 128, 0.1),
+    ("cfg2 TK cr1.0", "tk", 256, 256, 14, 128, 1.0),
+    ("cfg2 TT cr1.0", "tt", 256, 256, 14, 128, 1.0),
+]
+
+
+def _layer(kind, T, S, Hp, B, cr):
+    import paper_2401_03384_b200 as ce
+    slots = {"cp": 1, "tk": 2, "tt": 3, "tr": 4}[kind]
+    spec = ce.LayerSpec(kind, [T], [S], 3, 3, Hp, Hp, B, cr if isinstance(cr, list) else [1] * slots)
+    return ce.expression(spec, None if isinstance(cr, list) else cr)
+
+
+@pytest.mark.parametrize("case", LAYER_CASES, ids=[c[0] for c in LAYER_CASES])
+def test_baseline_layers_full_size(any_ctx, case):
+    """Full BASELINE shapes: per-sample forward vs the oracle (exact property: sample b depends only
+    on X[b]) and gradients through the multilinear identity <dY,Y> = <dX,X> = <dW_i,W_i>."""
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import Executor
+    c_, mode = any_ctx
+    name, kind, T, S, Hp, B, cr = case
+    le = _layer(kind, T, S, Hp, B, cr)
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    ex = Executor(c_, plan, backward=True)
+    xs = [c_.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
+    dout = c_.fill_random(plan.out_dims, 2000)
+    out = ex.execute(xs)
+    grads = ex.backward(xs, dout)
+    torch.cuda.synchronize()
+    # per-sample oracle check on two samples
+    one = _layer(kind, T, S, Hp, 1, le.ranks if not isinstance(cr, list) else cr)
+    p1 = ce.optimal(one.expr, one.dims, "same", "inference")
+    nodes1 = [(n["left"], n["right"], n["result"]) for n in json.loads(p1.to_json())["nodes"]]
+    for b in (0, B - 1):
+        ins = [xs[0][b:b + 1].double().cpu().numpy()] + [x.double().cpu().numpy() for x in xs[1:]]
+        ref, _ = npo.execute(one.expr, one.dims, nodes1, ins, "same")
+        assert nerr(out[b:b + 1].cpu().numpy(), ref) <= TOL[mode][0], (name, b)
+    y_dot = float((out.double() * dout.double()).sum())
+    for i, (x, g) in enumerate(zip(xs, grads)):
+        gx = float((g.double() * x.double()).sum())
+        assert abs(gx - y_dot) <= TOL[mode][1] * max(abs(y_dot), 1e-6) * 10, (name, i, gx, y_dot)
+
+
+def test_cp_layer_gradients_vs_oracle(any_ctx):
+    """cfg1-shape CP layer at batch 2: every gradient against the FP64 adjoint oracle."""
+    c_, mode = any_ctx
+    le = _layer("cp", 64, 64, 32, 2, [16])
+    rng = np.random.default_rng(4)
+    ins = [f32(rng.uniform(-1, 1, d)) for d in le.dims]
+    import paper_2401_03384_b200 as ce
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    dout = f32(rng.uniform(-1, 1, plan.out_dims))
+    plan, nodes, out, grads, _ = _run_plan(c_, le.expr, le.dims, "same", ins, dout, "training")
+    ref_g = npo.backward(le.expr, le.dims, nodes, ins, dout)
+    for g, r in zip(grads, ref_g):
+        assert nerr(g.cpu().numpy(), r) <= TOL[mode][1]
+
+
+def test_native_library_loaded(ctx):
+    maps = open("/proc/self/maps").read()
+    assert "libce.so" in maps
