@@ -88,6 +88,10 @@ ce_status ce_plan_get_info(const ce_plan* plan, ce_plan_info* info);
 ce_status ce_plan_node(const ce_plan* plan, int node, int* left, int* right, char* result_subs, size_t cap,
                        uint64_t* flops_actual_lo, uint64_t* cost_lo);
 
+/* The kernel steps an executor would launch for this plan (no device needed):
+ * one line per step "fwd|bwd label kind details", then "workspace_bytes N". */
+ce_status ce_plan_describe_steps(const ce_plan* plan, int want_backward, int math, char* buf, size_t cap);
+
 /* ----------------------------------------------------------------- layers -- */
 /* expression() (layers.hpp:71): kind name as in layer_kind_from_string (layers.cpp:29-45).
  * With cr > 0 the ranks are solved by rank_for_compression (layers.cpp:341-366) and

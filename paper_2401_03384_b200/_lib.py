@@ -56,6 +56,8 @@ SIGNATURES = {
     "ce_plan_get_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PlanInfo)]),
     "ce_plan_node": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_intp, c_intp, ctypes.c_char_p, ctypes.c_size_t,
                                     ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]),
+    "ce_plan_describe_steps": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                              ctypes.c_size_t]),
     "ce_layer_expression": (ctypes.c_int, [ctypes.c_char_p, c_i64p, ctypes.c_int, c_i64p, ctypes.c_int,
                                            ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                            ctypes.c_int64, c_i64p, ctypes.c_int, ctypes.c_double, ctypes.c_char_p,

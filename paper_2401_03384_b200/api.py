@@ -119,6 +119,12 @@ class Plan:
         check(lib().ce_plan_tree_encoding(self._h, buf, len(buf)))
         return buf.value.decode()
 
+    def describe_steps(self, backward: bool = False, math: str = "auto") -> str:
+        """Kernel steps the device executor compiles this plan into (no GPU needed)."""
+        buf = ctypes.create_string_buffer(1 << 20)
+        check(lib().ce_plan_describe_steps(self._h, int(backward), 0 if math in ("auto", "tf32") else 1, buf, len(buf)))
+        return buf.value.decode()
+
     def nodes(self):
         out = []
         for j in range(self.n_nodes):

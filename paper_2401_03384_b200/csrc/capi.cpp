@@ -256,6 +256,15 @@ ce_status ce_layer_expression(const char* kind, const int64_t* t_factors, int n_
   });
 }
 
+ce_status ce_plan_describe_steps(const ce_plan* plan, int want_backward, int math, char* buf, size_t cap) {
+  return guard([&] {
+    ExecConfig cfg;
+    cfg.math = math;
+    Executor ex(plan->plan, want_backward != 0, cfg);
+    copy_out(ex.describe() + "workspace_bytes " + std::to_string(ex.workspace_bytes()) + "\n", buf, cap);
+  });
+}
+
 ce_status ce_ctx_create(int device, const ce_options* opts, ce_ctx** out) {
   return guard([&] {
     auto c = std::make_unique<ce_ctx>();
@@ -366,8 +375,13 @@ ce_status ce_pairwise_grad(ce_ctx* ctx, const char* expr, const int64_t* dims, c
     Executor ex(pairwise_plan(expr, dims, ranks, mode), true, cfg);
     const float* ins[2] = {a, b};
     float* dins[2] = {da, db};
-    // the backward of a single node reads only the operands, not the forward result
+    // backward reuses the forward's workspace (self-contraction sums), so run it first
+    float* scratch = nullptr;
+    cuda_ok(cudaMallocAsync(&scratch, static_cast<size_t>(element_count(ex.output_dims())) * 4, ctx->stream),
+            "cudaMallocAsync");
+    ex.forward(ins, scratch, ctx->stream);
     ex.backward(ins, dout, dins, ctx->stream);
+    cuda_ok(cudaFreeAsync(scratch, ctx->stream), "cudaFreeAsync");
     cuda_ok(cudaStreamSynchronize(ctx->stream), "pairwise_grad");
   });
 }

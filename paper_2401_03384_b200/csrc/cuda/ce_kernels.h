@@ -6,6 +6,9 @@
 #include "ce_device.h"
 
 cudaError_t ce_launch_direct(const CeSimtDesc& d, const float* A, const float* B, float* C, cudaStream_t s);
+// out_span: elements of C zeroed before a split-K (atomic) reduction
+cudaError_t ce_launch_reduce(const CeSimtDesc& d, const float* A, const float* B, float* C, int64_t out_span,
+                             cudaStream_t s);
 cudaError_t ce_launch_tiled(const CeSimtDesc& d, const float* A, const float* B, float* C, int a_kfast,
                             int b_kfast, cudaStream_t s);
 cudaError_t ce_launch_fill(float* dst, int64_t n, uint64_t seed, cudaStream_t s);

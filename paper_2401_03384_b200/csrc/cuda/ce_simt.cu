@@ -11,6 +11,8 @@
 //  * ce_fill_kernel — SplitMix64 (reference tensor.cpp:107-130) in closed form.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "ce_device.h"
 #include "ce_kernels.h"
 
@@ -80,6 +82,66 @@ __global__ void __launch_bounds__(256) ce_direct_kernel(const CeSimtDesc d, cons
       C[offC] += acc;
     else
       C[offC] = acc;
+  }
+}
+
+// ----------------------------------------------------------------------------- reduce
+// Few outputs, long K (e.g. the depthwise filter gradient of CP's `bhwr,rh->bhwr`:
+// 48 outputs x 8192 terms): one CTA per (output, K split), 256 threads stride
+// the K range, warp-shuffle + smem tree reduction, one atomicAdd per CTA when split.
+__global__ void __launch_bounds__(256) ce_reduce_kernel(const CeSimtDesc d, const float* __restrict__ A,
+                                                        const float* __restrict__ B, float* __restrict__ C,
+                                                        int64_t k_per_split) {
+  const CeProblem& p = d.p;
+  __shared__ float warp_sum[8];
+  int64_t val[CE_MAX_VARS];
+  int64_t rest = blockIdx.x, offA = 0, offB = 0, offC = 0;
+  for (int i = 0; i < d.nout; ++i) {
+    const int v = d.ov[i];
+    const int64_t e = p.ext[v];
+    val[v] = rest % e;
+    rest /= e;
+    offA += val[v] * p.sa[v];
+    offB += val[v] * p.sb[v];
+    offC += val[v] * p.sc[v];
+  }
+  const int64_t k_begin = blockIdx.y * k_per_split;
+  const int64_t k_end = min(d.K, k_begin + k_per_split);
+  float acc = 0.f;
+  for (int64_t k = k_begin + threadIdx.x; k < k_end; k += blockDim.x) {
+    int64_t r = k, a_off = offA, b_off = offB;
+    for (int i = 0; i < d.nk; ++i) {
+      const int v = d.kv[i];
+      val[v] = r % p.ext[v];
+      r /= p.ext[v];
+      a_off += val[v] * p.sa[v];
+      b_off += val[v] * p.sb[v];
+    }
+    bool ok = true;
+    for (int g = 0; g < p.ng_a && ok; ++g) {
+      int64_t o;
+      ok = gather_index(p.ga[g], val[p.ga[g].pv], val[p.ga[g].qv], &o);
+      a_off += o;
+    }
+    for (int g = 0; g < p.ng_b && ok; ++g) {
+      int64_t o;
+      ok = gather_index(p.gb[g], val[p.gb[g].pv], val[p.gb[g].qv], &o);
+      b_off += o;
+    }
+    if (ok) acc += p.unary ? __ldg(A + a_off) : __ldg(A + a_off) * __ldg(B + b_off);
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? warp_sum[threadIdx.x] : 0.f;
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) {
+      if (gridDim.y > 1 || p.accumulate)
+        atomicAdd(C + offC, acc);
+      else
+        C[offC] = acc;
+    }
   }
 }
 
@@ -275,6 +337,24 @@ cudaError_t ce_launch_direct(const CeSimtDesc& d, const float* A, const float* B
   const int64_t total = d.Z * d.M * d.N;
   if (total == 0) return cudaSuccess;
   ce_direct_kernel<<<grid_for(total, 256), 256, 0, s>>>(d, A, B, C);
+  return cudaGetLastError();
+}
+
+cudaError_t ce_launch_reduce(const CeSimtDesc& d, const float* A, const float* B, float* C, int64_t out_span,
+                             cudaStream_t s) {
+  const int64_t outs = d.Z * d.M * d.N;
+  if (outs == 0) return cudaSuccess;
+  // enough CTAs for ~4 waves, each thread doing >= 8 terms
+  int64_t split = (148 * 4 + outs - 1) / outs;
+  split = std::max<int64_t>(1, std::min<int64_t>(split, d.K / (256 * 8)));
+  if (split > 65535) split = 65535;
+  const int64_t per = (d.K + split - 1) / split;
+  if (split > 1 && !d.p.accumulate) {
+    cudaError_t e = cudaMemsetAsync(C, 0, static_cast<size_t>(out_span) * 4, s);
+    if (e != cudaSuccess) return e;
+  }
+  if (outs > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  ce_reduce_kernel<<<dim3(static_cast<unsigned>(outs), static_cast<unsigned>(split)), 256, 0, s>>>(d, A, B, C, per);
   return cudaGetLastError();
 }
 

@@ -1,15 +1,90 @@
-// Tensor-core (tcgen05, kind::tf32) implicit-GEMM path: plan + launcher.
+// Tensor-core path (families a + b1): tcgen05 kind::tf32 implicit GEMM fed by
+// TMA, accumulating in TMEM.
+//
+// A lowered problem (ce_device.h) is mapped onto "units": index variables
+// merged where they are memory-contiguous in every TMA operand.  Each operand
+// becomes a <=5-D TMA tensor map; per tile and per K-iteration the producer
+// computes every TMA coordinate as an affine function of unit values
+// (coordinate = cst + c0*val[u0] + c1*val[u1]), which is how the convolution's
+// shifted taps (x = sp*p + sq*q + c) and Same/Full zero padding (TMA OOB fill)
+// are expressed without any im2col buffer.
+//
+//   A (M side) tile: 128 rows x 32 K  (K-major: one box; MN-major: 4 boxes of 32)
+//   B (N side) tile: BN rows x 32 K
+//   D: 128 x BN fp32 in TMEM -> registers -> (smem transpose) -> global scatter
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "ce_device.h"
 
+#define TC_MAX_UNITS 14
+#define TC_BM 128
+#define TC_BK 32
+
+enum TcSrc { TC_SRC_MTILE = 0, TC_SRC_NTILE = 1, TC_SRC_GRID = 2, TC_SRC_K = 3 };
+
+struct TcUnit {
+  int32_t ext;    // extent (product of member var extents)
+  int32_t box;    // tile/block extent along this unit (1 for grid / loop units)
+  int32_t src;    // TcSrc
+  int32_t nv;     // member vars, innermost first
+  int32_t vext[4];
+  int64_t sc[4];  // out stride of each member var (0 for K units)
+};
+
+struct TcDim {    // one TMA coordinate
+  int32_t u0, u1; // unit ids (-1 = none)
+  int32_t c0, c1; // coefficients
+  int32_t cst;
+};
+
+struct TcOperand {
+  TcDim dim[5];
+  int32_t mn_major;   // 0: K-major (box = 32 K x rows), 1: MN-major (nsub boxes of 32 MN x 32 K)
+  int32_t nsub;       // TMA issues per stage
+  int32_t stage_bytes;
+};
+
+struct TcParams {
+  CUtensorMap ta;     // 64-byte aligned, first members
+  CUtensorMap tb;
+  TcOperand oa, ob;
+  TcUnit u[TC_MAX_UNITS];
+  int32_t nunits;
+  int32_t nm, mt[3];      // M-tile units, row order fastest first
+  int32_t nn, nt[3];      // N-tile units, column order fastest first
+  int32_t ng, gu[8];      // grid units
+  int32_t nk, ku[6];      // K-loop units, fastest first
+  int32_t m_rows;         // rows filled by A per tile (<= 128)
+  int32_t n_cols;         // columns filled by B per tile (<= BN)
+  int32_t n_mma;          // MMA N (multiple of 16)
+  int32_t k_iters;        // K iterations in total
+  int32_t k_split;        // CTAs along K (atomic epilogue when > 1)
+  int32_t transpose_store;// stage through smem so lanes write consecutive columns
+  uint32_t idesc;         // tcgen05 instruction descriptor
+  int32_t tiles_m, tiles_n, grid_z;
+  int32_t mn_lbo, mn_sbo;  // MN-major descriptor strides (bytes)
+};
+
+// Host-side plan: everything except the pointer-dependent tensor maps.
 struct TcPlan {
   int valid = 0;
+  int bn = 0;                 // template tile N (64 / 128 / 256)
+  TcParams params{};          // maps filled at launch
+  // tensor-map geometry per operand (innermost first)
+  int rank_a = 0, rank_b = 0;
+  uint64_t gdim_a[5]{}, gdim_b[5]{};
+  uint64_t gstride_a[5]{}, gstride_b[5]{};  // bytes, [0] unused
+  uint32_t box_a[5]{}, box_b[5]{};
+  int64_t out_span = 0;       // elements of C to zero before a split-K launch
+  const void* cached_a = nullptr;
+  const void* cached_b = nullptr;
+  const char* why = "";       // reason when not valid (diagnostics)
 };
 
 // Decides whether a lowered problem maps onto the tcgen05 kernel and fills the plan.
 bool ce_tc_plan(const CeProblem& p, TcPlan* out);
-cudaError_t ce_launch_tc(const TcPlan& plan, const float* A, const float* B, float* C, cudaStream_t s);
+cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C, cudaStream_t s);

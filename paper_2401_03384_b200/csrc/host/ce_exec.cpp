@@ -9,6 +9,8 @@
 #include "ce_exec.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "../cuda/ce_kernels.h"
@@ -43,7 +45,7 @@ Executor::Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cf
   }
   build_forward();
   if (want_backward_) build_backward();
-  if (ws_bytes_ > 0) cuda_check(cudaMalloc(&ws_, static_cast<size_t>(ws_bytes_)), "cudaMalloc(workspace)");
+  if (const char* dbg = std::getenv("CE_DEBUG"); dbg && *dbg == '1') std::fputs(describe().c_str(), stderr);
 }
 
 Executor::~Executor() {
@@ -68,18 +70,144 @@ std::vector<int64_t> Executor::output_dims() const {
   return d;
 }
 
-void Executor::add_problem(std::vector<Step>& list, const CeProblem& p, BufRef a, BufRef b, BufRef c, int node,
+namespace {
+// A unary permute that rewrites one operand of `p` so that the vars in
+// `inner_order` become its innermost axes (inner_order[0] unit-stride, innermost
+// pitch padded to 16 B) and every other axis keeps its relative order.  Returns
+// the pack problem and patches p's strides for that operand in place.
+CeProblem repack(CeProblem& p, bool side_b, const std::vector<int>& inner_order, int64_t* span) {
+  int64_t* s = side_b ? p.sb : p.sa;
+  CeGather* g = side_b ? p.gb : p.ga;
+  const int ng = side_b ? p.ng_b : p.ng_a;
+  struct Ax { int64_t stride, ext; int var, gi, rank; };
+  std::vector<Ax> ax;
+  auto rank_of = [&](int v) {
+    for (std::size_t i = 0; i < inner_order.size(); ++i)
+      if (inner_order[i] == v) return static_cast<int>(i);
+    return 1 << 20;
+  };
+  for (int v = 0; v < p.nv; ++v)
+    if (s[v]) ax.push_back({s[v], p.ext[v], v, -1, rank_of(v)});
+  for (int i = 0; i < ng; ++i) ax.push_back({g[i].stride, g[i].extent, -1, i, 1 << 20});
+  // innermost first: listed vars in order, then the rest by ascending original stride
+  std::stable_sort(ax.begin(), ax.end(), [](const Ax& x, const Ax& y) {
+    if (x.rank != y.rank) return x.rank < y.rank;
+    return x.stride < y.stride;
+  });
+  CeProblem pk{};
+  pk.unary = 1;
+  int64_t acc = 1;
+  for (std::size_t i = 0; i < ax.size(); ++i) {
+    // the listed vars stay contiguous (so they can merge into one K unit); the first
+    // axis after them starts on a 16-byte boundary (TMA stride legality)
+    if (i > 0 && ax[i].rank >= (1 << 20) && ax[i - 1].rank < (1 << 20)) acc = (acc + 3) / 4 * 4;
+    const int v = pk.nv++;
+    pk.ext[v] = ax[i].ext;
+    pk.cls[v] = CE_M;
+    pk.sa[v] = ax[i].stride;
+    pk.sc[v] = acc;
+    if (ax[i].var >= 0) s[ax[i].var] = acc; else g[ax[i].gi].stride = acc;
+    acc *= ax[i].ext;
+  }
+  *span = acc;
+  return pk;
+}
+
+int inner_var(const CeProblem& p, bool side_b) {
+  const int64_t* s = side_b ? p.sb : p.sa;
+  for (int v = 0; v < p.nv; ++v)
+    if (s[v] == 1 && p.ext[v] > 1) return v;
+  return -1;
+}
+
+// Plain K vars shared by A and B, ordered by their stride in `side` (ascending).
+std::vector<int> shared_k_order(const CeProblem& p, bool by_b) {
+  std::vector<int> v;
+  for (int i = 0; i < p.nv; ++i)
+    if (p.cls[i] == CE_K && p.sa[i] && p.sb[i]) v.push_back(i);
+  const int64_t* s = by_b ? p.sb : p.sa;
+  std::stable_sort(v.begin(), v.end(), [&](int x, int y) { return s[x] < s[y]; });
+  return v;
+}
+}  // namespace
+
+void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef a, BufRef b, BufRef c, int node,
                            const std::string& label) {
+  CeProblem p = p0;
   Step st;
+  st.node = node;
+  st.label = label;
+  if (cfg_.math == 0 && !p.unary) {
+    bool ok = ce_tc_plan(p, &st.tc);
+    if (!ok) {
+      // tf32 tensor cores need both operands K-major over the same K unit: repack
+      // the operand(s) whose unit-stride axis is not a shared K var, mirroring the
+      // partner's K order so contiguous K vars still merge into one unit.
+      const int ia = inner_var(p, false), ib = inner_var(p, true);
+      const bool a_ok = ia >= 0 && p.cls[ia] == CE_K && p.sb[ia];
+      const bool b_ok = ib >= 0 && p.cls[ib] == CE_K && p.sa[ib];
+      std::vector<int> order;
+      bool pack_a = false, pack_b = false;
+      if (a_ok && !(b_ok && ib == ia)) {
+        order = shared_k_order(p, false);
+        pack_b = true;
+      } else if (b_ok && !a_ok) {
+        order = shared_k_order(p, true);
+        pack_a = true;
+      } else if (!a_ok && !b_ok) {
+        order = shared_k_order(p, false);
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p.ext[x] > p.ext[y]; });
+        if (!order.empty()) order.resize(1);
+        pack_a = pack_b = true;
+      }
+      if (!order.empty() && (pack_a || pack_b)) {
+        CeProblem q = p;
+        CeProblem pks[2];
+        int64_t spans[2] = {0, 0};
+        if (pack_a) pks[0] = repack(q, false, order, &spans[0]);
+        if (pack_b) pks[1] = repack(q, true, order, &spans[1]);
+        TcPlan t;
+        if (ce_tc_plan(q, &t)) {
+          for (int side = 0; side < 2; ++side) {
+            if (!(side ? pack_b : pack_a)) continue;
+            Step ps;
+            ps.kind = Step::kDirect;
+            ps.desc = simt_desc(pks[side]);
+            ps.a = side ? b : a;
+            ps.c = {BufRef::kWork, alloc(spans[side])};
+            ps.node = node;
+            ps.label = label + (side ? ":packB" : ":packA");
+            (side ? b : a) = ps.c;
+            list.push_back(ps);
+          }
+          p = q;
+          st.tc = t;
+          ok = true;
+        }
+      }
+    }
+    if (ok) {
+      st.kind = Step::kTc;
+      st.a = a;
+      st.b = b;
+      st.c = c;
+      st.desc = simt_desc(p);
+      list.push_back(st);
+      return;
+    }
+  }
   st.a = a;
   st.b = b;
   st.c = c;
-  st.node = node;
-  st.label = label;
   st.desc = simt_desc(p);
   const CeSimtDesc& d = st.desc;
-  if (cfg_.math == 0 && !p.unary && ce_tc_plan(p, &st.tc)) {
-    st.kind = Step::kTc;
+  const int64_t outs = d.Z * d.M * d.N;
+  if (d.K >= 1024 && outs < 148 * 256 && (p.unary || d.K <= 32 || d.M < 16 || d.N < 16 || outs < 4096)) {
+    st.kind = Step::kReduce;
+    int64_t span = 0;
+    for (int v = 0; v < p.nv; ++v)
+      if (p.cls[v] != CE_K) span += (p.ext[v] - 1) * p.sc[v];
+    st.zero_elems = span + 1;
   } else if (p.unary || d.K <= 32 || d.M < 16 || d.N < 16) {
     st.kind = Step::kDirect;
   } else {
@@ -199,14 +327,41 @@ float* Executor::resolve(const BufRef& r) const {
   }
 }
 
+std::string Executor::describe() const {
+  static const char* kinds[] = {"direct", "tiled", "tc", "zero", "reduce"};
+  std::string out;
+  char line[512];
+  for (const auto* list : {&fwd_, &bwd_})
+    for (const Step& st : *list) {
+      int n = std::snprintf(line, sizeof line, "%s %s %s", list == &fwd_ ? "fwd" : "bwd", st.label.c_str(), kinds[st.kind]);
+      if (st.kind == Step::kTc) {
+        const TcParams& P = st.tc.params;
+        std::snprintf(line + n, sizeof line - n,
+                      " bn=%d rows=%d cols=%d mma_n=%d tiles=%dx%dx%d split=%d kit=%d amn=%d bmn=%d tr=%d\n", st.tc.bn,
+                      P.m_rows, P.n_cols, P.n_mma, P.tiles_m, P.tiles_n, P.grid_z, P.k_split, P.k_iters, P.oa.mn_major,
+                      P.ob.mn_major, P.transpose_store);
+      } else {
+        std::snprintf(line + n, sizeof line - n, " Z=%lld M=%lld N=%lld K=%lld\n", (long long)st.desc.Z,
+                      (long long)st.desc.M, (long long)st.desc.N, (long long)st.desc.K);
+      }
+      out += line;
+    }
+  return out;
+}
+
+void Executor::ensure_workspace() {
+  if (!ws_ && ws_bytes_ > 0) cuda_check(cudaMalloc(&ws_, static_cast<size_t>(ws_bytes_)), "cudaMalloc(workspace)");
+}
+
 int Executor::tc_steps(bool bwd) const {
   int n = 0;
   for (const auto& s : bwd ? bwd_ : fwd_) n += s.kind == Step::kTc;
   return n;
 }
 
-void Executor::run(const std::vector<Step>& steps, cudaStream_t s) {
-  for (const Step& st : steps) {
+void Executor::run(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s) {
+  for (Step& st : steps) {
+    if (need && st.node >= 0 && !(*need)[static_cast<std::size_t>(st.node)]) continue;
     const float* A = resolve(st.a);
     const float* B = resolve(st.b);
     float* C = resolve(st.c);
@@ -217,6 +372,7 @@ void Executor::run(const std::vector<Step>& steps, cudaStream_t s) {
       case Step::kTiled: e = ce_launch_tiled(st.desc, A, B, C, st.a_kfast, st.b_kfast, s); break;
       case Step::kTc: e = ce_launch_tc(st.tc, A, B, C, s); break;
       case Step::kZero: e = cudaMemsetAsync(C, 0, static_cast<size_t>(st.zero_elems) * 4, s); break;
+      case Step::kReduce: e = ce_launch_reduce(st.desc, A, B, C, st.zero_elems, s); break;
     }
     cuda_check(e, st.label.c_str());
     ++last_launches_;
@@ -224,14 +380,16 @@ void Executor::run(const std::vector<Step>& steps, cudaStream_t s) {
 }
 
 void Executor::forward(const float* const* inputs, float* out, cudaStream_t s) {
+  ensure_workspace();
   inputs_.assign(inputs, inputs + n_);
   out_ = out;
   last_launches_ = 0;
-  run(fwd_, s);
+  run(fwd_, nullptr, s);
 }
 
 void Executor::backward(const float* const* inputs, const float* dout, float* const* dinputs, cudaStream_t s) {
   if (!want_backward_) throw std::runtime_error("executor was created without backward support");
+  ensure_workspace();
   dout_ = dout;
   // intermediate gradients are only needed above requested inputs
   std::vector<char> need(id_view_.size(), 0);
@@ -239,14 +397,11 @@ void Executor::backward(const float* const* inputs, const float* dout, float* co
   for (std::size_t j = 0; j < plan_.nodes.size(); ++j)
     need[static_cast<std::size_t>(n_) + j] =
         need[static_cast<std::size_t>(plan_.nodes[j].left)] || need[static_cast<std::size_t>(plan_.nodes[j].right)];
-  std::vector<Step> todo;
-  for (const Step& st : bwd_)
-    if (plan_.nodes.empty() || need[static_cast<std::size_t>(st.node)]) todo.push_back(st);
   inputs_.assign(inputs, inputs + n_);
   dinputs_.assign(n_, nullptr);
   for (int i = 0; i < n_ && dinputs; ++i) dinputs_[static_cast<std::size_t>(i)] = dinputs[i];
   last_launches_ = 0;
-  run(todo, s);
+  run(bwd_, plan_.nodes.empty() ? nullptr : &need, s);
 }
 
 }  // namespace ce

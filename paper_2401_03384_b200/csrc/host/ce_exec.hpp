@@ -24,7 +24,7 @@ struct BufRef {
 };
 
 struct Step {
-  enum Kind { kDirect, kTiled, kTc, kZero } kind = kDirect;
+  enum Kind { kDirect, kTiled, kTc, kZero, kReduce } kind = kDirect;
   CeSimtDesc desc{};
   int a_kfast = 0, b_kfast = 0;
   TcPlan tc{};
@@ -55,14 +55,16 @@ class Executor {
   const std::vector<Step>& forward_steps() const { return fwd_; }
   const std::vector<Step>& backward_steps() const { return bwd_; }
   std::vector<int64_t> output_dims() const;
+  std::string describe() const;  // one line per kernel step (no CUDA calls)
 
  private:
   int64_t alloc(int64_t elems);
+  void ensure_workspace();
   void add_problem(std::vector<Step>& list, const CeProblem& p, BufRef a, BufRef b, BufRef c, int node,
                    const std::string& label);
   void build_forward();
   void build_backward();
-  void run(const std::vector<Step>& steps, cudaStream_t s);
+  void run(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s);
   float* resolve(const BufRef& r) const;
 
   EvaluationPlan plan_;

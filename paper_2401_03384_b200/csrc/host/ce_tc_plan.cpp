@@ -1,0 +1,422 @@
+// Host planner for the tcgen05 implicit-GEMM path (see cuda/ce_tc.h).
+//
+// Given a lowered pairwise step, decide:
+//   * units: vars merged where contiguous in every TMA operand;
+//   * per operand: K-major (K unit innermost) or MN-major (tile unit innermost);
+//   * the K block (32 K indices per stage) both operands enumerate identically;
+//   * M tile (<=128 rows) and N tile (<=256 columns) boxes, grid and K-loop units;
+//   * split-K for steps with few output tiles and long K (factor gradients).
+// Anything that does not fit (wrap-around Circular taps, >5 TMA dims, strides
+// not multiple of 16 B, no unit-stride axis) returns false and the executor uses
+// the SIMT kernels (ce_simt.cu).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "../cuda/ce_tc.h"
+
+namespace {
+
+struct Axis {          // one TMA dim of an operand, before unit assignment
+  bool gather = false;
+  int v0 = -1, v1 = -1;  // plain: v0; gather: p = v0, q = v1
+  int c0 = 1, c1 = 0;
+  int64_t cst = 0;
+  int64_t ext = 0;
+  int64_t stride = 0;    // elements
+};
+
+std::vector<Axis> axes_of(const CeProblem& p, bool is_a) {
+  std::vector<Axis> ax;
+  const int64_t* s = is_a ? p.sa : p.sb;
+  for (int v = 0; v < p.nv; ++v)
+    if (s[v]) {
+      Axis a;
+      a.v0 = v;
+      a.ext = p.ext[v];
+      a.stride = s[v];
+      ax.push_back(a);
+    }
+  const int ng = is_a ? p.ng_a : p.ng_b;
+  const CeGather* g = is_a ? p.ga : p.gb;
+  for (int i = 0; i < ng; ++i) {
+    Axis a;
+    a.gather = true;
+    a.v0 = g[i].pv;
+    a.v1 = g[i].qv;
+    a.c0 = g[i].sp;
+    a.c1 = g[i].sq;
+    a.cst = g[i].c;
+    a.ext = g[i].extent;
+    a.stride = g[i].stride;
+    ax.push_back(a);
+  }
+  // extent-1 plain axes carry nothing
+  ax.erase(std::remove_if(ax.begin(), ax.end(), [](const Axis& a) { return !a.gather && a.ext == 1; }), ax.end());
+  std::sort(ax.begin(), ax.end(), [](const Axis& x, const Axis& y) { return x.stride < y.stride; });
+  return ax;
+}
+
+bool in_gather(const CeProblem& p, int v) {
+  for (int i = 0; i < p.ng_a; ++i)
+    if (p.ga[i].pv == v || p.ga[i].qv == v) return true;
+  for (int i = 0; i < p.ng_b; ++i)
+    if (p.gb[i].pv == v || p.gb[i].qv == v) return true;
+  return false;
+}
+
+// Group of vars forming one unit (innermost first).
+struct Group {
+  std::vector<int> vars;
+  int64_t ext = 1;
+  int cls = 0;
+};
+
+// Merge var `outer` onto group g if it continues g's innermost-first stride chain
+// in every TMA operand (A, B).  Out strides are not required to chain: the
+// epilogue decomposes units back into vars.
+bool chains(const CeProblem& p, const Group& g, int outer) {
+  const int inner = g.vars.back();
+  for (const int64_t* s : {p.sa, p.sb}) {
+    const bool hi = s[inner] != 0, ho = s[outer] != 0;
+    if (hi != ho) return false;
+    if (hi && s[outer] != s[inner] * p.ext[inner]) return false;
+  }
+  return true;
+}
+
+int64_t pow2ceil(int64_t x) {
+  int64_t r = 1;
+  while (r < x) r <<= 1;
+  return r;
+}
+
+}  // namespace
+
+bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
+  *plan = TcPlan{};
+  auto fail = [&](const char* why) {
+    plan->valid = 0;
+    plan->why = why;
+    return false;
+  };
+  if (p.unary) return fail("unary");
+  for (int i = 0; i < p.ng_a; ++i)
+    if (p.ga[i].wrap) return fail("circular wrap");
+  for (int i = 0; i < p.ng_b; ++i)
+    if (p.gb[i].wrap) return fail("circular wrap");
+
+  // ---------------------------------------------------------------- units
+  // Seed groups from single vars, then greedily chain contiguous same-class plain vars.
+  std::vector<Group> groups;
+  std::vector<int> order(static_cast<std::size_t>(p.nv));
+  for (int v = 0; v < p.nv; ++v) order[static_cast<std::size_t>(v)] = v;
+  // chain candidates by the stride they have in A (else B)
+  auto key = [&](int v) { return p.sa[v] ? p.sa[v] : p.sb[v]; };
+  std::sort(order.begin(), order.end(), [&](int x, int y) { return key(x) < key(y); });
+  std::vector<int> unit_of(static_cast<std::size_t>(p.nv), -1);
+  for (int v : order) {
+    if (p.ext[v] == 1 && !in_gather(p, v)) {
+      // size-1 vars vanish: attach to nothing (value always 0)
+      continue;
+    }
+    bool merged = false;
+    if (!in_gather(p, v)) {
+      for (std::size_t gi = 0; gi < groups.size() && !merged; ++gi) {
+        Group& g = groups[gi];
+        if (g.cls != p.cls[v] || in_gather(p, g.vars.back()) || g.vars.size() >= 4) continue;
+        if (chains(p, g, v)) {
+          g.vars.push_back(v);
+          g.ext *= p.ext[v];
+          unit_of[static_cast<std::size_t>(v)] = static_cast<int>(gi);
+          merged = true;
+        }
+      }
+    }
+    if (!merged) {
+      Group g;
+      g.vars = {v};
+      g.ext = p.ext[v];
+      g.cls = p.cls[v];
+      unit_of[static_cast<std::size_t>(v)] = static_cast<int>(groups.size());
+      groups.push_back(g);
+    }
+  }
+  if (static_cast<int>(groups.size()) > TC_MAX_UNITS) return fail("too many units");
+
+  // operand dims in units
+  auto build = [&](bool is_a, std::vector<Axis>& out) -> bool {
+    std::vector<Axis> ax = axes_of(p, is_a);
+    for (Axis& a : ax) {
+      if (a.gather) continue;
+      const int u = unit_of[static_cast<std::size_t>(a.v0)];
+      if (groups[static_cast<std::size_t>(u)].vars.front() != a.v0) { a.ext = -1; continue; }  // merged into inner
+      a.ext = groups[static_cast<std::size_t>(u)].ext;
+    }
+    ax.erase(std::remove_if(ax.begin(), ax.end(), [](const Axis& a) { return a.ext < 0; }), ax.end());
+    out = ax;
+    return true;
+  };
+  std::vector<Axis> A, B;
+  build(true, A);
+  build(false, B);
+  if (A.empty() || B.empty()) return fail("empty operand");
+  if (A.size() > 5 || B.size() > 5) return fail("more than 5 TMA dims");
+  if (A.front().stride != 1 || A.front().gather) return fail("A has no unit-stride plain axis");
+  if (B.front().stride != 1 || B.front().gather) return fail("B has no unit-stride plain axis");
+  for (const auto* ops : {&A, &B})
+    for (std::size_t i = 1; i < ops->size(); ++i)
+      if (((*ops)[i].stride * 4) % 16 != 0) return fail("stride not a multiple of 16 bytes");
+
+  auto ucls = [&](int v) { return p.cls[v]; };
+  auto uid = [&](int v) { return unit_of[static_cast<std::size_t>(v)]; };
+  const int innerA = A.front().v0, innerB = B.front().v0;
+  const int ia_cls = ucls(innerA), ib_cls = ucls(innerB);
+  // tcgen05 kind::tf32 with the MN-major (transpose) descriptor bits set returns zeros on
+  // sm_100a (measured: tests/tc_probe2.py); only K-major operands are planned.  The
+  // executor repacks operands whose unit-stride axis is not the shared K unit.
+  if (ia_cls != CE_K || ib_cls != CE_K) return fail("operand not K-major (tf32 requires K-major)");
+  int a_mn = -1, b_mn = -1;
+  std::vector<std::pair<int, int>> kblock;  // (unit, box)
+  auto has_plain = [&](const std::vector<Axis>& ops, int u) {
+    for (const Axis& a : ops)
+      if (!a.gather && uid(a.v0) == u) return true;
+    return false;
+  };
+  if (ia_cls == CE_K) {
+    a_mn = 0;
+    kblock = {{uid(innerA), TC_BK}};
+    if (ib_cls == CE_K && uid(innerB) == uid(innerA)) {
+      b_mn = 0;
+    } else if (ib_cls == CE_N && has_plain(B, uid(innerA))) {
+      b_mn = 1;
+    } else {
+      return fail("K blocks of A and B disagree");
+    }
+  } else if (ia_cls == CE_M) {
+    a_mn = 1;
+    if (ib_cls == CE_K) {
+      b_mn = 0;
+      if (!has_plain(A, uid(innerB))) return fail("K block of B not addressable in A");
+      kblock = {{uid(innerB), TC_BK}};
+    } else if (ib_cls == CE_N) {
+      b_mn = 1;
+      // K rows from K units addressable in both operands (plain, or gathered with q-coef +1),
+      // ordered by A's stride
+      int64_t remaining = TC_BK;
+      for (const Axis& a : A) {
+        if (remaining == 1) break;
+        int u = -1;
+        if (!a.gather && ucls(a.v0) == CE_K) u = uid(a.v0);
+        if (a.gather && ucls(a.v1) == CE_K && a.c1 == 1) u = uid(a.v1);
+        if (u < 0) continue;
+        bool in_b = false;
+        for (const Axis& b : B) {
+          if (!b.gather && uid(b.v0) == u) in_b = true;
+          if (b.gather && uid(b.v1) == u && b.c1 == 1) in_b = true;
+        }
+        if (!in_b) continue;
+        const int64_t e = groups[static_cast<std::size_t>(u)].ext;
+        int64_t box = std::min(remaining, pow2ceil(e));
+        kblock.push_back({u, static_cast<int>(box)});
+        remaining /= box;
+      }
+      if (kblock.empty()) return fail("no shared K unit for MN-major operands");
+      if (remaining > 1) kblock.back().second *= static_cast<int>(remaining);
+    } else {
+      return fail("B inner axis class");
+    }
+  } else {
+    return fail("A inner axis class");
+  }
+
+  // ---------------------------------------------------------------- tiles
+  std::vector<TcUnit> U(groups.size());
+  for (std::size_t i = 0; i < groups.size(); ++i) {
+    TcUnit& t = U[i];
+    t = TcUnit{};
+    t.ext = static_cast<int32_t>(groups[i].ext);
+    t.box = 1;
+    t.nv = static_cast<int32_t>(groups[i].vars.size());
+    for (int k = 0; k < t.nv; ++k) {
+      const int v = groups[i].vars[static_cast<std::size_t>(k)];
+      t.vext[k] = static_cast<int32_t>(p.ext[v]);
+      t.sc[k] = p.sc[v];
+    }
+    const int c = groups[i].cls;
+    t.src = c == CE_K ? TC_SRC_K : TC_SRC_GRID;
+    if (groups[i].ext >= (1ll << 31)) return fail("extent above 2^31");
+  }
+  for (auto& kb : kblock) U[static_cast<std::size_t>(kb.first)].box = kb.second;
+
+  TcParams& P = plan->params;
+  std::memset(&P, 0, sizeof(P));
+  // M tile from A, N tile from B
+  auto tile = [&](const std::vector<Axis>& ops, bool mn_major, int cls, int cap, int32_t* list, int32_t* n,
+                  int src) -> int {
+    int rows = 1;
+    if (mn_major) {
+      const int u = uid(ops.front().v0);
+      const int box = std::min<int>(cap, static_cast<int>((U[static_cast<std::size_t>(u)].ext + 31) / 32 * 32));
+      U[static_cast<std::size_t>(u)].box = box;
+      U[static_cast<std::size_t>(u)].src = src;
+      list[(*n)++] = u;
+      return box;
+    }
+    int remaining = cap;
+    for (const Axis& a : ops) {
+      if (remaining <= 1 || *n >= 3) break;
+      int u = -1;
+      if (!a.gather && ucls(a.v0) == cls) u = uid(a.v0);
+      if (a.gather && ucls(a.v0) == cls && a.c0 == 1) u = uid(a.v0);
+      if (u < 0 || U[static_cast<std::size_t>(u)].src != TC_SRC_GRID) continue;
+      const int e = U[static_cast<std::size_t>(u)].ext;
+      const int box = std::min(e, remaining);
+      U[static_cast<std::size_t>(u)].box = box;
+      U[static_cast<std::size_t>(u)].src = src;
+      list[(*n)++] = u;
+      rows *= box;
+      remaining /= box;
+    }
+    return rows;
+  };
+  P.m_rows = tile(A, a_mn == 1, CE_M, TC_BM, P.mt, &P.nm, TC_SRC_MTILE);
+  // N tile: up to 256 columns
+  int ncap = 256;
+  P.n_cols = tile(B, b_mn == 1, CE_N, ncap, P.nt, &P.nn, TC_SRC_NTILE);
+  if (P.nm == 0 || P.nn == 0) return fail("no M or N tile unit");
+  P.n_mma = static_cast<int32_t>((P.n_cols + 15) / 16 * 16);
+  plan->bn = P.n_mma <= 64 ? 64 : P.n_mma <= 128 ? 128 : 256;
+  if (b_mn == 1 && P.n_cols % 32) return fail("MN-major B tile must be a multiple of 32");
+
+  // grid / K-loop units
+  for (std::size_t i = 0; i < U.size(); ++i) {
+    if (U[i].src == TC_SRC_GRID) P.gu[P.ng++] = static_cast<int32_t>(i);
+    if (P.ng > 8) return fail("too many grid units");
+  }
+  for (auto& kb : kblock) P.ku[P.nk++] = kb.first;
+  for (std::size_t i = 0; i < U.size(); ++i) {
+    if (U[i].src != TC_SRC_K) continue;
+    bool in_block = false;
+    for (auto& kb : kblock) in_block |= kb.first == static_cast<int>(i);
+    if (!in_block) {
+      if (P.nk >= 6) return fail("too many K units");
+      P.ku[P.nk++] = static_cast<int32_t>(i);
+    }
+  }
+
+  // ---------------------------------------------------------------- TMA dims
+  auto dims_for = [&](const std::vector<Axis>& ops, bool mn_major, TcOperand& o, uint64_t* gdim, uint64_t* gstride,
+                      uint32_t* box, int* rank) -> bool {
+    // order: inner, then box>1 dims in K-block order (MN-major) or tile order (K-major), then the rest
+    std::vector<const Axis*> ord{&ops.front()};
+    auto boxed_unit = [&](const Axis& a) -> int {
+      if (!a.gather) return uid(a.v0);
+      const int up = uid(a.v0), uq = uid(a.v1);
+      if (U[static_cast<std::size_t>(up)].box > 1) return up;
+      if (U[static_cast<std::size_t>(uq)].box > 1) return uq;
+      return up;
+    };
+    std::vector<int> pref;
+    if (mn_major)
+      for (auto& kb : kblock) pref.push_back(kb.first);
+    else
+      for (int i = 0; i < (&o == &P.oa ? P.nm : P.nn); ++i) pref.push_back((&o == &P.oa ? P.mt : P.nt)[i]);
+    for (int u : pref)
+      for (const Axis& a : ops)
+        if (&a != &ops.front() && boxed_unit(a) == u && U[static_cast<std::size_t>(u)].box > 1) ord.push_back(&a);
+    for (const Axis& a : ops)
+      if (std::find(ord.begin(), ord.end(), &a) == ord.end()) ord.push_back(&a);
+    *rank = static_cast<int>(ord.size());
+    int64_t rows = 1;
+    for (int d = 0; d < 5; ++d) {
+      TcDim& td = o.dim[d];
+      td = TcDim{-1, -1, 0, 0, 0};
+      if (d >= *rank) {
+        gdim[d] = 1;
+        box[d] = 1;
+        gstride[d] = gstride[d - 1] * gdim[d - 1];
+        continue;
+      }
+      const Axis& a = *ord[static_cast<std::size_t>(d)];
+      gdim[d] = static_cast<uint64_t>(a.ext);
+      gstride[d] = static_cast<uint64_t>(a.stride) * 4;
+      if (!a.gather) {
+        td.u0 = uid(a.v0);
+        td.c0 = 1;
+        box[d] = static_cast<uint32_t>(U[static_cast<std::size_t>(td.u0)].box);
+      } else {
+        td.u0 = uid(a.v0);
+        td.c0 = a.c0;
+        td.u1 = uid(a.v1);
+        td.c1 = a.c1;
+        td.cst = static_cast<int32_t>(a.cst);
+        const int b0 = U[static_cast<std::size_t>(td.u0)].box, b1 = U[static_cast<std::size_t>(td.u1)].box;
+        if (b0 > 1 && b1 > 1) return false;
+        if ((b0 > 1 && a.c0 != 1) || (b1 > 1 && a.c1 != 1)) return false;
+        box[d] = static_cast<uint32_t>(std::max(b0, b1));
+      }
+      if (d == 0) {
+        box[0] = 32;  // 128-byte rows (SWIZZLE_128B)
+      } else {
+        rows *= box[d];
+      }
+      if (box[d] > 256) return false;
+    }
+    if (gstride[0] != 4) return false;
+    o.mn_major = mn_major ? 1 : 0;
+    if (mn_major) {
+      if (rows != TC_BK) return false;
+      o.nsub = U[static_cast<std::size_t>(uid(ops.front().v0))].box / 32;
+      o.stage_bytes = o.nsub * 32 * 128;
+    } else {
+      o.nsub = 1;
+      o.stage_bytes = static_cast<int32_t>(rows * 128);
+    }
+    return true;
+  };
+  if (!dims_for(A, a_mn == 1, P.oa, plan->gdim_a, plan->gstride_a, plan->box_a, &plan->rank_a))
+    return fail("A TMA dims");
+  if (!dims_for(B, b_mn == 1, P.ob, plan->gdim_b, plan->gstride_b, plan->box_b, &plan->rank_b))
+    return fail("B TMA dims");
+  if (a_mn == 0 && P.oa.stage_bytes != P.m_rows * 128) return fail("A rows");
+  if (b_mn == 0 && P.ob.stage_bytes != P.n_cols * 128) return fail("B rows");
+  if (P.ob.stage_bytes > plan->bn * 128) return fail("B tile too large");
+
+  // ---------------------------------------------------------------- grid
+  P.nunits = static_cast<int32_t>(U.size());
+  for (std::size_t i = 0; i < U.size(); ++i) P.u[i] = U[i];
+  int64_t tm = 1, tn = 1, gz = 1, ki = 1;
+  for (int i = 0; i < P.nm; ++i) tm *= (U[P.mt[i]].ext + U[P.mt[i]].box - 1) / U[P.mt[i]].box;
+  for (int i = 0; i < P.nn; ++i) tn *= (U[P.nt[i]].ext + U[P.nt[i]].box - 1) / U[P.nt[i]].box;
+  for (int i = 0; i < P.ng; ++i) gz *= U[P.gu[i]].ext;
+  for (int i = 0; i < P.nk; ++i) ki *= (U[P.ku[i]].ext + U[P.ku[i]].box - 1) / U[P.ku[i]].box;
+  if (tm > 0x7fffffff || tn > 65535 || ki > 0x7fffffff) return fail("grid too large");
+  P.tiles_m = static_cast<int32_t>(tm);
+  P.tiles_n = static_cast<int32_t>(tn);
+  P.grid_z = static_cast<int32_t>(gz);
+  P.k_iters = static_cast<int32_t>(ki);
+  // split-K when the output grid cannot fill the 148 SMs and K is long
+  const int64_t ctas = tm * tn * gz;
+  int split = 1;
+  if (ctas < 148 && ki >= 16) {
+    split = static_cast<int>(std::min<int64_t>((2 * 148 + ctas - 1) / ctas, ki / 8));
+    split = std::max(split, 1);
+  }
+  if (gz * split > 65535) return fail("grid z too large");
+  P.k_split = split;
+  // output span (for zeroing before split-K accumulation)
+  int64_t span = 0;
+  for (int v = 0; v < p.nv; ++v)
+    if (p.cls[v] != CE_K) span += (p.ext[v] - 1) * p.sc[v];
+  plan->out_span = span + 1;
+  // transposed store when the fastest N var is unit-stride in the output
+  const TcUnit& n0 = U[static_cast<std::size_t>(P.nt[0])];
+  P.transpose_store = n0.sc[0] == 1 ? 1 : 0;
+  P.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+            (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(P.n_mma >> 3) << 17) |
+            (static_cast<uint32_t>(TC_BM >> 4) << 24);
+  plan->valid = 1;
+  plan->why = "ok";
+  return true;
+}
