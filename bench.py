@@ -1,0 +1,372 @@
+"""Benchmark: tensorized 3x3 conv layers (Tucker + TT, cfg2 of BASELINE.json),
+batch 128 per GPU, 256->256 channels, 14x14, forward + backward on B200.
+
+One step = forward + backward (input AND factor gradients) of four layers
+  TK cr=0.1 (R=57), TK cr=1.0 (R=229), TT cr=0.1 (R=65), TT cr=1.0 (R=273)
+through libce's C-ABI (plans from the reference-identical planner, training
+cost mode).  `value` = algorithmic TFLOP/s over all GPUs = sum over nodes of
+2*flops_actual (forward) + 2*flops_actual per adjoint (dA, dB), divided by the
+device time of the step (CUDA events on the executor stream, max over ranks).
+L2 is flushed (256 MiB write) between timed steps, outside the events.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU: one process per GPU (torchrun), batch sharded (128 per GPU, weak
+scaling), factors replicated, factor gradients all-reduced with NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LAYERS = [("tk", 0.1), ("tk", 1.0), ("tt", 0.1), ("tt", 1.0)]
+METRIC = "TFLOP/s & layer fwd+bwd latency, tensorized ResNet-34 convs, 1/2/4/8 B200 vs CPU"
+PER_GPU_BATCH = 128
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), float(j["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+def layer_expr(kind, cr, batch):
+    import paper_2401_03384_b200 as ce
+    slots = {"tk": 2, "tt": 3}[kind]
+    return ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, batch, [1] * slots), cr)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
+                          and "Not" not in r[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- CPU / reference
+def cpu_reference_time(batch_cpu=2, reps=2):
+    """Reference execute() (FP64, OpenMP, all host cores) on a batch subset of each layer.
+
+    Returns (seconds for the subset forward of all layers, FLOPs of that subset, kind, cores)."""
+    import numpy as np
+    from oracle import ref
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    total_s, total_flops = 0.0, 0.0
+    kind = "reference"
+    for k, cr in LAYERS:
+        le = layer_expr(k, cr, batch_cpu)
+        import paper_2401_03384_b200 as ce
+        p = ce.optimal(le.expr, le.dims, "same", "training")
+        ins = [np.asarray(np.float32(ref.fill_random(d, 1000 + i) if ref.available() else 0), dtype=np.float64)
+               for i, d in enumerate(le.dims)]
+        if ref.available():
+            s = ref.time_execute(le.expr, le.dims, ins, "same", "training", reps=reps)
+        else:  # numpy port of the reference (oracle/np_oracle.py)
+            from oracle import np_oracle as npo
+            kind = "port"
+            nodes = [(n["left"], n["right"], n["result"]) for n in json.loads(p.to_json())["nodes"]]
+            ins = [npo.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
+            t0 = time.perf_counter()
+            npo.execute(le.expr, le.dims, nodes, ins)
+            s = time.perf_counter() - t0
+            cores = 1
+        total_s += s
+        total_flops += 2.0 * p.flops_actual
+    return total_s, total_flops, kind, cores
+
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the reference's own CPU executor (forward only: it has no backward)."""
+    if rank != 0:
+        return
+    batch_cpu = 2
+    secs = []
+    flops = None
+    for _ in range(args.warmup):
+        cpu_reference_time(batch_cpu, reps=1)
+    for _ in range(args.steps):
+        s, flops, kind, cores = cpu_reference_time(batch_cpu, reps=1)
+        secs.append(s)
+    t = statistics.median(secs)
+    # scale the bounded sample to the GPU arm's workload: forward FLOPs are exactly linear in B
+    value = flops / t / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3 * (PER_GPU_BATCH * world / batch_cpu),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2 TK+TT 3x3 conv layers cr{0.1,1.0}, 256->256, 14x14",
+                   "global_batch": PER_GPU_BATCH * world, "sample_batch": batch_cpu,
+                   "note": "reference has no backward: forward only, FLOPs-normalised"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+                         "sample": f"reference execute() forward of the 4 layers at batch {batch_cpu} (of 128), "
+                                   f"OMP_NUM_THREADS={cores}"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-json", default=None, help="write per-kernel times here")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import Context, Executor
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    ctx = Context(local, "auto")
+    stream = ctx.torch_stream
+    dev = torch.device(f"cuda:{local}")
+
+    layers = []
+    for kind, cr in LAYERS:
+        le = layer_expr(kind, cr, PER_GPU_BATCH)
+        plan = ce.optimal(le.expr, le.dims, "same", "training")
+        ex = Executor(ctx, plan, backward=True)
+        # inputs: X sharded by rank (different seeds per rank), factors identical everywhere
+        xs = [ctx.fill_random(d, 1000 + i + (7919 * rank if i == 0 else 0)) for i, d in enumerate(le.dims)]
+        dout = ctx.fill_random(plan.out_dims, 2000 + rank)
+        fwd_flops = 2.0 * plan.flops_actual
+        layers.append(dict(kind=kind, cr=cr, le=le, plan=plan, ex=ex, xs=xs, dout=dout,
+                           flops=3.0 * fwd_flops, out=torch.empty(plan.out_dims, device=dev)))
+    step_flops = sum(l["flops"] for l in layers)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+
+    def one_step(collect=None):
+        launches = 0
+        for l in layers:
+            l["ex"].execute(l["xs"], l["out"])
+            launches += l["ex"].stats.kernels_launched
+            grads = l["ex"].backward(l["xs"], l["dout"])
+            launches += l["ex"].stats.kernels_launched
+            if world > 1:
+                for g in grads[1:]:  # factor gradients only; X gradients stay sharded
+                    dist.all_reduce(g)
+                    launches += 1
+            l["grads"] = grads
+        return launches
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+
+    times = []
+    launches = 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            launches = one_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    ms = statistics.mean(times)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * step_flops / (ms * 1e-3) / 1e12
+
+    # per-layer fwd+bwd latency (device, one more pass, events per layer)
+    lat = {}
+    for l in layers:
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        l["ex"].execute(l["xs"], l["out"])
+        l["ex"].backward(l["xs"], l["dout"])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        lat[f"{l['kind']}_cr{l['cr']}_R{l['le'].ranks[0]}"] = round(e0.elapsed_time(e1), 4)
+
+    # ---------------------------------------------------------------- e2e through the public API, host buffers
+    pinned = []
+    for l in layers:
+        hin = [x.cpu().pin_memory() for x in l["xs"]]
+        hd = l["dout"].cpu().pin_memory()
+        hout = torch.empty(l["plan"].out_dims, pin_memory=True)
+        hg = [torch.empty(x.shape, pin_memory=True) for x in l["xs"]]
+        din = [torch.empty_like(x) for x in l["xs"]]
+        pinned.append((hin, hd, hout, hg, din, torch.empty_like(l["dout"])))
+    h2d = sum(sum(x.numel() * 4 for x in p[0]) + p[1].numel() * 4 for p in pinned)
+    d2h = sum(p[2].numel() * 4 + sum(g.numel() * 4 for g in p[3]) for p in pinned)
+
+    def e2e_step():
+        with torch.cuda.stream(stream):
+            for l, (hin, hd, hout, hg, din, ddout) in zip(layers, pinned):
+                for d, h in zip(din, hin):
+                    d.copy_(h, non_blocking=True)
+                ddout.copy_(hd, non_blocking=True)
+                out = l["ex"].execute(din, l["out"])
+                grads = l["ex"].backward(din, ddout)
+                if world > 1:
+                    for g in grads[1:]:
+                        dist.all_reduce(g)
+                hout.copy_(out, non_blocking=True)
+                for h, g in zip(hg, grads):
+                    h.copy_(g, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_times = []
+    for _ in range(max(3, args.steps // 2)):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_times.append(e0.elapsed_time(e1))
+    e2e_ms = statistics.mean(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * step_flops / (e2e_ms * 1e-3) / 1e12
+
+    # ---------------------------------------------------------------- live per-kernel roofline
+    hbm, bf16, peak_kind = load_peaks()
+    tf32_peak = bf16 / 2.0
+    kern = []
+    for l in layers:
+        l["ex"].set_profiling(True)
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        l["ex"].execute(l["xs"], l["out"])
+        f = l["ex"].profile(False)
+        l["ex"].backward(l["xs"], l["dout"])
+        b = l["ex"].profile(True)
+        torch.cuda.synchronize()
+        l["ex"].set_profiling(False)
+        tag = f"{l['kind']}{l['cr']}"
+        kern += [(tag + ":" + n, k, t, fl, by) for (n, k, t, fl, by) in f + b]
+    total_k = sum(k[2] for k in kern)
+    top = max(kern, key=lambda k: k[2])
+    name, kind, t_ms, fl, by = top
+    if kind == "tc":
+        ach = fl / (t_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": tf32_peak, "unit": "TFLOP/s",
+                "frac": round(ach / tf32_peak, 4), "traffic": None,
+                "kernel": name, "share_of_step": round(t_ms / total_k, 3),
+                "peak_note": f"TF32 dense = bf16_tflops/2 of {peak_kind} ({bf16} TF)",
+                "hbm_frac": round(by / (t_ms * 1e-3) / 1e9 / hbm, 4)}
+    else:
+        ach = by / (t_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(ach / hbm, 4), "traffic": None, "kernel": name,
+                "share_of_step": round(t_ms / total_k, 3), "peak_note": f"{peak_kind} copy bandwidth"}
+    if args.profile_json and rank == 0:
+        with open(args.profile_json, "w") as f:
+            json.dump([dict(name=n, kind=k, ms=t, flops=fl, bytes=by,
+                            tflops=fl / (t * 1e-3) / 1e12 if t > 0 else 0, gbs=by / (t * 1e-3) / 1e9 if t > 0 else 0)
+                       for (n, k, t, fl, by) in kern], f, indent=1)
+
+    # ---------------------------------------------------------------- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s, fl_cpu, kindc, cores = cpu_reference_time(2, reps=2)
+        cpu = {"value": fl_cpu / s / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kindc,
+               "sample": "reference execute() FORWARD (no backward exists) of the 4 layers at batch 2 of 128, "
+                         "FP64, best of 2; FLOPs-normalised"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "tf32", "data": "synthetic (SplitMix64 fill_random, reference seeds)",
+            "config": {"workload": "cfg2: Tucker + TT 3x3 conv layers, 256->256 ch, 14x14, fwd+bwd (all grads)",
+                       "layers": [f"{l['kind']} cr={l['cr']} R={l['le'].ranks[0]} tree={l['plan'].tree_encoding()}"
+                                  for l in layers],
+                       "global_batch": PER_GPU_BATCH * world, "per_gpu_batch": PER_GPU_BATCH,
+                       "parallelism": f"batch-sharded x{world}, factor-grad NCCL all-reduce" if world > 1 else "1 GPU",
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "flops_per_step_per_gpu": step_flops},
+            "layer_fwd_bwd_ms": lat,
+            "e2e": {"value": round(e2e_value, 3), "unit": "TFLOP/s", "ms_per_step": round(e2e_ms, 4),
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "pinned host -> H2D -> ce_execute + ce_backward (C-ABI) -> D2H of output + all grads"},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

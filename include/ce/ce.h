@@ -146,6 +146,13 @@ ce_status ce_execute(ce_executor* ex, const float* const* inputs, float* out, ce
  * intermediates it left in the workspace are reused (no recompute). */
 ce_status ce_backward(ce_executor* ex, const float* const* inputs, const float* dout, float* const* dinputs,
                       ce_exec_stats* stats);
+/* Per-kernel device timing: when enabled, every launched step is bracketed by
+ * CUDA events on the ctx stream.  ce_executor_profile reports the last forward
+ * (backward = 0) or backward call: newline-separated labels, kind (0 direct,
+ * 1 tiled, 2 tensor-core, 3 memset, 4 reduce), ms, algorithmic FLOPs and bytes. */
+ce_status ce_executor_set_profiling(ce_executor* ex, int enable);
+ce_status ce_executor_profile(ce_executor* ex, int backward, int max_steps, int* n_steps, char* labels,
+                              size_t labels_cap, int* kinds, float* ms, double* flops, double* bytes);
 /* Host-buffer convenience (e2e path): H2D copy, execute, D2H copy, synchronize. */
 ce_status ce_execute_host(ce_executor* ex, const float* const* host_inputs, float* host_out);
 

@@ -73,6 +73,10 @@ SIGNATURES = {
     "ce_execute": (ctypes.c_int, [ctypes.c_void_p, c_fpp, ctypes.c_void_p, ctypes.POINTER(ExecStats)]),
     "ce_backward": (ctypes.c_int, [ctypes.c_void_p, c_fpp, ctypes.c_void_p, c_fpp, ctypes.POINTER(ExecStats)]),
     "ce_execute_host": (ctypes.c_int, [ctypes.c_void_p, c_fpp, ctypes.c_void_p]),
+    "ce_executor_set_profiling": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "ce_executor_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, c_intp, ctypes.c_char_p,
+                                           ctypes.c_size_t, c_intp, ctypes.POINTER(ctypes.c_float),
+                                           ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "ce_pairwise_eval": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, c_i64p, c_intp, ctypes.c_char_p,
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ce_pairwise_grad": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, c_i64p, c_intp, ctypes.c_char_p,

@@ -331,6 +331,28 @@ ce_status ce_backward(ce_executor* ex, const float* const* inputs, const float* 
   });
 }
 
+ce_status ce_executor_set_profiling(ce_executor* ex, int enable) {
+  return guard([&] { ex->ex->set_profiling(enable != 0); });
+}
+
+ce_status ce_executor_profile(ce_executor* ex, int backward, int max_steps, int* n_steps, char* labels,
+                              size_t labels_cap, int* kinds, float* ms, double* flops, double* bytes) {
+  return guard([&] {
+    auto t = ex->ex->step_times(backward != 0);
+    std::string names;
+    const int n = std::min<int>(max_steps, static_cast<int>(t.size()));
+    for (int i = 0; i < n; ++i) {
+      names += t[static_cast<std::size_t>(i)].label + "\n";
+      kinds[i] = t[static_cast<std::size_t>(i)].kind;
+      ms[i] = t[static_cast<std::size_t>(i)].ms;
+      flops[i] = t[static_cast<std::size_t>(i)].flops;
+      bytes[i] = t[static_cast<std::size_t>(i)].bytes;
+    }
+    *n_steps = n;
+    copy_out(names, labels, labels_cap);
+  });
+}
+
 ce_status ce_execute_host(ce_executor* ex, const float* const* host_inputs, float* host_out) {
   return guard([&] {
     cuda_ok(cudaSetDevice(ex->ctx->device), "cudaSetDevice");

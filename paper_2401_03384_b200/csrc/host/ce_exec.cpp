@@ -50,7 +50,35 @@ Executor::Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cf
 
 Executor::~Executor() {
   if (ws_) cudaFree(ws_);
+  for (auto* list : {&fwd_, &bwd_})
+    for (Step& st : *list) {
+      if (st.ev0) cudaEventDestroy(st.ev0);
+      if (st.ev1) cudaEventDestroy(st.ev1);
+    }
 }
+
+namespace {
+// Logical (compulsory) element counts of A, B and C of a lowered problem.
+double operand_elems(const CeProblem& p, int which) {
+  double n = 1;
+  if (which == 2) {
+    for (int v = 0; v < p.nv; ++v)
+      if (p.cls[v] != CE_K) n *= static_cast<double>(p.ext[v]);
+    return n;
+  }
+  const int64_t* s = which == 0 ? p.sa : p.sb;
+  const CeGather* g = which == 0 ? p.ga : p.gb;
+  const int ng = which == 0 ? p.ng_a : p.ng_b;
+  if (which == 1 && p.unary) return 0;
+  for (int v = 0; v < p.nv; ++v)
+    if (s[v]) n *= static_cast<double>(p.ext[v]);
+  for (int i = 0; i < ng; ++i) n *= static_cast<double>(g[i].extent);
+  return n;
+}
+double problem_bytes(const CeProblem& p) {
+  return 4.0 * (operand_elems(p, 0) + operand_elems(p, 1) + operand_elems(p, 2));
+}
+}  // namespace
 
 int64_t Executor::alloc(int64_t elems) {
   const int64_t off = ws_bytes_;
@@ -177,6 +205,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
             ps.c = {BufRef::kWork, alloc(spans[side])};
             ps.node = node;
             ps.label = label + (side ? ":packB" : ":packA");
+            ps.bytes = 8.0 * operand_elems(pks[side], 0);
             (side ? b : a) = ps.c;
             list.push_back(ps);
           }
@@ -192,6 +221,8 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       st.b = b;
       st.c = c;
       st.desc = simt_desc(p);
+      st.flops = pending_flops_;
+      st.bytes = problem_bytes(p);
       list.push_back(st);
       return;
     }
@@ -200,6 +231,8 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
   st.b = b;
   st.c = c;
   st.desc = simt_desc(p);
+  st.flops = pending_flops_;
+  st.bytes = problem_bytes(p);
   const CeSimtDesc& d = st.desc;
   const int64_t outs = d.Z * d.M * d.N;
   if (d.K >= 1024 && outs < 148 * 256 && (p.unary || d.K <= 32 || d.M < 16 || d.N < 16 || outs < 4096)) {
@@ -259,6 +292,7 @@ void Executor::build_forward() {
     const bool last = j + 1 == plan_.nodes.size();
     View res = last ? out_view : padded_view(op.result, op.result_dims, 4);
     BufRef res_ref = last ? BufRef{BufRef::kOutput, 0} : BufRef{BufRef::kWork, alloc(view_span(res))};
+    pending_flops_ = 2.0 * static_cast<double>(flops_actual(op));
     add_problem(fwd_, lower_pairwise(op, red_view_[0][j], red_view_[1][j], res, res, Adjoint::Forward),
                 red_ref_[0][j], red_ref_[1][j], res_ref, static_cast<int>(j), "node" + std::to_string(j));
     id_view_.push_back(res);
@@ -296,6 +330,7 @@ void Executor::build_backward() {
     const int ids[2] = {node.left, node.right};
     const Subscripts* selfs[2] = {&op.left_self, &op.right_self};
     for (int s = 0; s < 2; ++s) {
+      pending_flops_ = 2.0 * static_cast<double>(flops_actual(op));
       const auto id = static_cast<std::size_t>(ids[s]);
       const Adjoint which = s == 0 ? Adjoint::GradLeft : Adjoint::GradRight;
       const std::string label = "grad:" + std::to_string(id);
@@ -310,6 +345,7 @@ void Executor::build_backward() {
         BufRef tref{BufRef::kWork, alloc(view_span(tmp))};
         add_problem(bwd_, lower_pairwise(op, red_view_[0][jj], red_view_[1][jj], gview[cid], tmp, which), a, b, tref,
                     static_cast<int>(id), label);
+        pending_flops_ = 0;
         add_problem(bwd_, lower_unary(tmp, gview[id]), tref, {}, gref[id], static_cast<int>(id), label + ":bcast");
       }
     }
@@ -361,11 +397,20 @@ int Executor::tc_steps(bool bwd) const {
 
 void Executor::run(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s) {
   for (Step& st : steps) {
+    st.ran = false;
     if (need && st.node >= 0 && !(*need)[static_cast<std::size_t>(st.node)]) continue;
     const float* A = resolve(st.a);
     const float* B = resolve(st.b);
     float* C = resolve(st.c);
     if (!C) continue;  // gradient not requested
+    st.ran = true;
+    if (profiling_) {
+      if (!st.ev0) {
+        cuda_check(cudaEventCreate(&st.ev0), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&st.ev1), "cudaEventCreate");
+      }
+      cuda_check(cudaEventRecord(st.ev0, s), "cudaEventRecord");
+    }
     cudaError_t e = cudaSuccess;
     switch (st.kind) {
       case Step::kDirect: e = ce_launch_direct(st.desc, A, B, C, s); break;
@@ -375,8 +420,21 @@ void Executor::run(std::vector<Step>& steps, const std::vector<char>* need, cuda
       case Step::kReduce: e = ce_launch_reduce(st.desc, A, B, C, st.zero_elems, s); break;
     }
     cuda_check(e, st.label.c_str());
+    if (profiling_) cuda_check(cudaEventRecord(st.ev1, s), "cudaEventRecord");
     ++last_launches_;
   }
+}
+
+std::vector<Executor::StepTime> Executor::step_times(bool bwd) {
+  std::vector<StepTime> out;
+  for (Step& st : bwd ? bwd_ : fwd_) {
+    if (!st.ran || !st.ev0) continue;
+    cuda_check(cudaEventSynchronize(st.ev1), "cudaEventSynchronize");
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, st.ev0, st.ev1), "cudaEventElapsedTime");
+    out.push_back({st.label, static_cast<int>(st.kind), ms, st.flops, st.bytes});
+  }
+  return out;
 }
 
 void Executor::forward(const float* const* inputs, float* out, cudaStream_t s) {

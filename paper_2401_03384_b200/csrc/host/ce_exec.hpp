@@ -30,6 +30,10 @@ struct Step {
   TcPlan tc{};
   BufRef a, b, c;
   int64_t zero_elems = 0;
+  double flops = 0;   // algorithmic FLOPs (2 x flops_actual of the node / adjoint)
+  double bytes = 0;   // compulsory bytes (|A| + |B| + |C|) x 4
+  bool ran = false;   // launched by the last call
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int node = -1;
   std::string label;
 };
@@ -56,6 +60,16 @@ class Executor {
   const std::vector<Step>& backward_steps() const { return bwd_; }
   std::vector<int64_t> output_dims() const;
   std::string describe() const;  // one line per kernel step (no CUDA calls)
+  void set_profiling(bool on) { profiling_ = on; }
+  // per launched step of the last forward (bwd=false) or backward call:
+  // label, kind, device ms (CUDA events on the launch stream), flops, bytes
+  struct StepTime {
+    std::string label;
+    int kind;
+    float ms;
+    double flops, bytes;
+  };
+  std::vector<StepTime> step_times(bool bwd);
 
  private:
   int64_t alloc(int64_t elems);
@@ -85,6 +99,8 @@ class Executor {
   const float* dout_ = nullptr;
   std::vector<float*> dinputs_;
   int last_launches_ = 0;
+  bool profiling_ = false;
+  double pending_flops_ = 0;  // FLOPs credited to the next add_problem (build time)
 };
 
 }  // namespace ce

@@ -96,6 +96,24 @@ class Executor:
         del k1, k2
         return grads
 
+    def set_profiling(self, on: bool = True):
+        check(lib().ce_executor_set_profiling(self._h, int(on)))
+
+    def profile(self, backward: bool = False):
+        """[(label, kind, ms, flops, bytes)] of the last forward/backward call (CUDA events per kernel)."""
+        n_max = 256
+        n = ctypes.c_int()
+        labels = ctypes.create_string_buffer(1 << 16)
+        kinds = (ctypes.c_int * n_max)()
+        ms = (ctypes.c_float * n_max)()
+        fl = (ctypes.c_double * n_max)()
+        by = (ctypes.c_double * n_max)()
+        check(lib().ce_executor_profile(self._h, int(backward), n_max, ctypes.byref(n), labels, len(labels), kinds,
+                                        ms, fl, by))
+        names = labels.value.decode().split("\n")
+        kind_names = ["direct", "tiled", "tc", "memset", "reduce"]
+        return [(names[i], kind_names[kinds[i]], float(ms[i]), float(fl[i]), float(by[i])) for i in range(n.value)]
+
     def execute_host(self, host_inputs: Sequence["numpy.ndarray"], host_out: "numpy.ndarray"):  # noqa: F821
         """H2D + execute + D2H + sync through the C-ABI (the end-to-end call)."""
         arrs = [a for a in host_inputs]
