@@ -184,6 +184,7 @@ def main():
     ctx = Context(local, "auto")
     stream = ctx.torch_stream
     dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_stream(stream)  # every torch op of the bench is ordered with libce's kernels
 
     layers = []
     for kind, cr in LAYERS:

@@ -312,6 +312,50 @@ __global__ void __launch_bounds__(256) ce_tiled_kernel(const CeSimtDesc d, const
   }
 }
 
+// ----------------------------------------------------------------------------- permute
+// Family (c): axis permutation (operand repacking, reference permute tensor.cpp:50-94).
+// 32x32 shared-memory tile over (input unit-stride axis, output unit-stride axis) so
+// both the load and the store are coalesced; all other axes are a flattened batch.
+struct CePermDesc {
+  int32_t nrest;
+  int32_t vin, vout;       // indices into ext/sa/sc
+  int64_t ext[CE_MAX_VARS], sa[CE_MAX_VARS], sc[CE_MAX_VARS];
+  int32_t rest[CE_MAX_VARS];
+  int64_t nbatch;
+};
+
+__global__ void __launch_bounds__(256) ce_transpose_kernel(const CePermDesc d, const float* __restrict__ A,
+                                                           float* __restrict__ C) {
+  __shared__ float tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int64_t x0 = static_cast<int64_t>(blockIdx.x) * 32;  // along vin
+  const int64_t y0 = static_cast<int64_t>(blockIdx.y) * 32;  // along vout
+  const int64_t ein = d.ext[d.vin], eout = d.ext[d.vout];
+  const int64_t sa_out = d.sa[d.vout], sc_in = d.sc[d.vin];
+  for (int64_t bt = blockIdx.z; bt < d.nbatch; bt += gridDim.z) {
+    int64_t r = bt, bin = 0, bout = 0;
+    for (int i = 0; i < d.nrest; ++i) {
+      const int v = d.rest[i];
+      const int64_t x = r % d.ext[v];
+      r /= d.ext[v];
+      bin += x * d.sa[v];
+      bout += x * d.sc[v];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t y = y0 + ty + 8 * j, x = x0 + tx;
+      tile[ty + 8 * j][tx] = (x < ein && y < eout) ? __ldg(A + bin + x + y * sa_out) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t x = x0 + ty + 8 * j, y = y0 + tx;
+      if (x < ein && y < eout) C[bout + y + x * sc_in] = tile[tx][ty + 8 * j];
+    }
+    __syncthreads();
+  }
+}
+
 // ----------------------------------------------------------------------------- fill
 __global__ void ce_fill_kernel(float* __restrict__ dst, int64_t n, uint64_t seed) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -365,6 +409,42 @@ cudaError_t ce_launch_tiled(const CeSimtDesc& d, const float* A, const float* B,
             (unsigned)(d.Z < 65535 ? d.Z : 65535));
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
   ce_tiled_kernel<<<grid, 256, 0, s>>>(d, A, B, C, a_kfast, b_kfast);
+  return cudaGetLastError();
+}
+
+bool ce_permute_supported(const CeProblem& p) {
+  if (!p.unary || p.ng_a) return false;
+  int vin = -1, vout = -1;
+  for (int v = 0; v < p.nv; ++v) {
+    if (p.cls[v] == CE_K || p.sa[v] == 0 || p.sc[v] == 0) return false;  // pure permutation only
+    if (p.sa[v] == 1) vin = v;
+    if (p.sc[v] == 1) vout = v;
+  }
+  return vin >= 0 && vout >= 0 && vin != vout;
+}
+
+cudaError_t ce_launch_permute(const CeProblem& p, const float* A, float* C, cudaStream_t s) {
+  CePermDesc d{};
+  d.vin = d.vout = -1;
+  for (int v = 0; v < p.nv; ++v) {
+    d.ext[v] = p.ext[v];
+    d.sa[v] = p.sa[v];
+    d.sc[v] = p.sc[v];
+    if (p.sa[v] == 1 && d.vin < 0) d.vin = v;
+    if (p.sc[v] == 1 && d.vout < 0) d.vout = v;
+  }
+  if (d.vin < 0 || d.vout < 0 || d.vin == d.vout) return cudaErrorInvalidValue;
+  d.nbatch = 1;
+  for (int v = 0; v < p.nv; ++v)
+    if (v != d.vin && v != d.vout) {
+      d.rest[d.nrest++] = v;
+      d.nbatch *= p.ext[v];
+    }
+  const int64_t gx = (p.ext[d.vin] + 31) / 32, gy = (p.ext[d.vout] + 31) / 32;
+  if (gx > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
+  const int64_t gz = std::min<int64_t>(d.nbatch, 65535);
+  ce_transpose_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(gz)), 256, 0,
+                        s>>>(d, A, C);
   return cudaGetLastError();
 }
 

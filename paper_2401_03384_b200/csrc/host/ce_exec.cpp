@@ -103,7 +103,8 @@ namespace {
 // `inner_order` become its innermost axes (inner_order[0] unit-stride, innermost
 // pitch padded to 16 B) and every other axis keeps its relative order.  Returns
 // the pack problem and patches p's strides for that operand in place.
-CeProblem repack(CeProblem& p, bool side_b, const std::vector<int>& inner_order, int64_t* span) {
+CeProblem repack(CeProblem& p, bool side_b, const std::vector<int>& inner_order, int64_t* span,
+                 const int64_t* partner = nullptr) {
   int64_t* s = side_b ? p.sb : p.sa;
   CeGather* g = side_b ? p.gb : p.ga;
   const int ng = side_b ? p.ng_b : p.ng_a;
@@ -129,6 +130,10 @@ CeProblem repack(CeProblem& p, bool side_b, const std::vector<int>& inner_order,
     // the listed vars stay contiguous (so they can merge into one K unit); the first
     // axis after them starts on a 16-byte boundary (TMA stride legality)
     if (i > 0 && ax[i].rank >= (1 << 20) && ax[i - 1].rank < (1 << 20)) acc = (acc + 3) / 4 * 4;
+    // listed vars that do not chain in the partner operand cannot merge: keep 16-byte strides
+    if (partner && i > 0 && ax[i].rank < (1 << 20) && ax[i].var >= 0 && ax[i - 1].var >= 0 &&
+        partner[ax[i].var] != partner[ax[i - 1].var] * p.ext[ax[i - 1].var])
+      acc = (acc + 3) / 4 * 4;
     const int v = pk.nv++;
     pk.ext[v] = ax[i].ext;
     pk.cls[v] = CE_M;
@@ -174,32 +179,36 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       const int ia = inner_var(p, false), ib = inner_var(p, true);
       const bool a_ok = ia >= 0 && p.cls[ia] == CE_K && p.sb[ia];
       const bool b_ok = ib >= 0 && p.cls[ib] == CE_K && p.sa[ib];
-      std::vector<int> order;
-      bool pack_a = false, pack_b = false;
-      if (a_ok && !(b_ok && ib == ia)) {
-        order = shared_k_order(p, false);
-        pack_b = true;
-      } else if (b_ok && !a_ok) {
-        order = shared_k_order(p, true);
-        pack_a = true;
-      } else if (!a_ok && !b_ok) {
-        order = shared_k_order(p, false);
-        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p.ext[x] > p.ext[y]; });
-        if (!order.empty()) order.resize(1);
-        pack_a = pack_b = true;
+      struct Attempt {
+        bool pack_a, pack_b;
+        std::vector<int> order;
+      };
+      std::vector<Attempt> attempts;
+      if (a_ok && !(b_ok && ib == ia)) attempts.push_back({false, true, shared_k_order(p, false)});
+      if (b_ok && !a_ok) attempts.push_back({true, false, shared_k_order(p, true)});
+      {
+        // both operands repacked with one K order (contiguous, so the K vars merge)
+        std::vector<int> order = shared_k_order(p, a_ok ? false : true);
+        if (!a_ok && !b_ok) {
+          std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p.ext[x] > p.ext[y]; });
+          if (!order.empty()) order.resize(1);
+        }
+        attempts.push_back({true, true, order});
       }
-      if (!order.empty() && (pack_a || pack_b)) {
+      for (const Attempt& at : attempts) {
+        if (ok || at.order.empty()) continue;
+        const bool pack_a = at.pack_a, pack_b = at.pack_b;
         CeProblem q = p;
         CeProblem pks[2];
         int64_t spans[2] = {0, 0};
-        if (pack_a) pks[0] = repack(q, false, order, &spans[0]);
-        if (pack_b) pks[1] = repack(q, true, order, &spans[1]);
+        if (pack_a) pks[0] = repack(q, false, at.order, &spans[0], pack_b ? nullptr : p.sb);
+        if (pack_b) pks[1] = repack(q, true, at.order, &spans[1], pack_a ? nullptr : p.sa);
         TcPlan t;
         if (ce_tc_plan(q, &t)) {
           for (int side = 0; side < 2; ++side) {
             if (!(side ? pack_b : pack_a)) continue;
             Step ps;
-            ps.kind = Step::kDirect;
+            ps.kind = ce_permute_supported(pks[side]) ? Step::kPermute : Step::kDirect;
             ps.desc = simt_desc(pks[side]);
             ps.a = side ? b : a;
             ps.c = {BufRef::kWork, alloc(spans[side])};
@@ -235,7 +244,9 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
   st.bytes = problem_bytes(p);
   const CeSimtDesc& d = st.desc;
   const int64_t outs = d.Z * d.M * d.N;
-  if (d.K >= 1024 && outs < 148 * 256 && (p.unary || d.K <= 32 || d.M < 16 || d.N < 16 || outs < 4096)) {
+  if (p.unary && ce_permute_supported(p)) {
+    st.kind = Step::kPermute;
+  } else if (d.K >= 1024 && outs < 148 * 256 && (p.unary || d.K <= 32 || d.M < 16 || d.N < 16 || outs < 4096)) {
     st.kind = Step::kReduce;
     int64_t span = 0;
     for (int v = 0; v < p.nv; ++v)
@@ -364,7 +375,7 @@ float* Executor::resolve(const BufRef& r) const {
 }
 
 std::string Executor::describe() const {
-  static const char* kinds[] = {"direct", "tiled", "tc", "zero", "reduce"};
+  static const char* kinds[] = {"direct", "tiled", "tc", "zero", "reduce", "permute"};
   std::string out;
   char line[512];
   for (const auto* list : {&fwd_, &bwd_})
@@ -377,8 +388,9 @@ std::string Executor::describe() const {
                       P.m_rows, P.n_cols, P.n_mma, P.tiles_m, P.tiles_n, P.grid_z, P.k_split, P.k_iters, P.oa.mn_major,
                       P.ob.mn_major, P.transpose_store);
       } else {
-        std::snprintf(line + n, sizeof line - n, " Z=%lld M=%lld N=%lld K=%lld\n", (long long)st.desc.Z,
-                      (long long)st.desc.M, (long long)st.desc.N, (long long)st.desc.K);
+        std::snprintf(line + n, sizeof line - n, " Z=%lld M=%lld N=%lld K=%lld (tc: %s)\n", (long long)st.desc.Z,
+                      (long long)st.desc.M, (long long)st.desc.N, (long long)st.desc.K,
+                      st.desc.p.unary ? "unary" : st.tc.why);
       }
       out += line;
     }
@@ -418,6 +430,7 @@ void Executor::run(std::vector<Step>& steps, const std::vector<char>* need, cuda
       case Step::kTc: e = ce_launch_tc(st.tc, A, B, C, s); break;
       case Step::kZero: e = cudaMemsetAsync(C, 0, static_cast<size_t>(st.zero_elems) * 4, s); break;
       case Step::kReduce: e = ce_launch_reduce(st.desc, A, B, C, st.zero_elems, s); break;
+      case Step::kPermute: e = ce_launch_permute(st.desc.p, A, C, s); break;
     }
     cuda_check(e, st.label.c_str());
     if (profiling_) cuda_check(cudaEventRecord(st.ev1, s), "cudaEventRecord");

@@ -24,7 +24,7 @@ struct BufRef {
 };
 
 struct Step {
-  enum Kind { kDirect, kTiled, kTc, kZero, kReduce } kind = kDirect;
+  enum Kind { kDirect, kTiled, kTc, kZero, kReduce, kPermute } kind = kDirect;
   CeSimtDesc desc{};
   int a_kfast = 0, b_kfast = 0;
   TcPlan tc{};

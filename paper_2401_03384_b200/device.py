@@ -25,6 +25,10 @@ class Context:
         self.math = math
         torch.cuda.set_device(device)
         st = stream if stream is not None else torch.cuda.current_stream(device)
+        if st.cuda_stream == 0:
+            # the legacy default stream has handle 0, which ce_ctx_create reads as "make your own";
+            # use an explicit side stream instead so callers can order work on ctx.torch_stream
+            st = torch.cuda.Stream(device)
         self.torch_stream = st
         opts = _lib.Options(MATH[math], 0, ctypes.c_void_p(st.cuda_stream))
         h = ctypes.c_void_p()
@@ -40,8 +44,13 @@ class Context:
 
     def fill_random(self, shape: Sequence[int], seed: int) -> torch.Tensor:
         """fill_random (tensor.cpp:125-130) evaluated on the device, rounded to FP32."""
-        t = torch.empty(list(shape), dtype=torch.float32, device=f"cuda:{self.device}")
-        check(lib().ce_fill_random(self._h, ctypes.c_void_p(t.data_ptr()), t.numel(), ctypes.c_uint64(seed)))
+        cur = torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(self.torch_stream):
+            t = torch.empty(list(shape), dtype=torch.float32, device=f"cuda:{self.device}")
+            check(lib().ce_fill_random(self._h, ctypes.c_void_p(t.data_ptr()), t.numel(), ctypes.c_uint64(seed)))
+        if cur.cuda_stream != self.torch_stream.cuda_stream:
+            cur.wait_stream(self.torch_stream)
+            t.record_stream(cur)
         return t
 
     def __del__(self):
@@ -75,25 +84,46 @@ class Executor:
         self._h = h
         self.stats = _lib.ExecStats()
 
+    def _order_in(self):
+        """Make the ctx stream wait for the caller's current stream (inputs produced there)."""
+        cur = torch.cuda.current_stream(self.ctx.device)
+        if cur.cuda_stream != self.ctx.torch_stream.cuda_stream:
+            self.ctx.torch_stream.wait_stream(cur)
+            return cur
+        return None
+
+    def _order_out(self, cur, tensors):
+        if cur is not None:
+            cur.wait_stream(self.ctx.torch_stream)
+            for t in tensors:
+                if t is not None:
+                    t.record_stream(cur)
+
     def execute(self, inputs: Sequence[torch.Tensor], out: Optional[torch.Tensor] = None) -> torch.Tensor:
         _check_inputs(self.plan, inputs)
-        if out is None:
-            out = torch.empty(self.plan.out_dims, dtype=torch.float32, device=inputs[0].device)
-        p, keep = _ptrs(list(inputs))
-        check(lib().ce_execute(self._h, p, ctypes.c_void_p(out.data_ptr()), ctypes.byref(self.stats)))
-        del keep
+        cur = self._order_in()
+        with torch.cuda.stream(self.ctx.torch_stream):
+            if out is None:
+                out = torch.empty(self.plan.out_dims, dtype=torch.float32, device=inputs[0].device)
+            p, keep = _ptrs(list(inputs))
+            check(lib().ce_execute(self._h, p, ctypes.c_void_p(out.data_ptr()), ctypes.byref(self.stats)))
+            del keep
+        self._order_out(cur, [out])
         return out
 
     def backward(self, inputs: Sequence[torch.Tensor], dout: torch.Tensor,
                  needs: Optional[Sequence[bool]] = None) -> List[Optional[torch.Tensor]]:
         _check_inputs(self.plan, inputs)
         needs = needs or [True] * len(inputs)
-        grads = [torch.empty_like(t) if n else None for t, n in zip(inputs, needs)]
-        p, k1 = _ptrs(list(inputs))
-        g, k2 = _ptrs(grads)
-        dout = dout.contiguous()
-        check(lib().ce_backward(self._h, p, ctypes.c_void_p(dout.data_ptr()), g, ctypes.byref(self.stats)))
-        del k1, k2
+        cur = self._order_in()
+        with torch.cuda.stream(self.ctx.torch_stream):
+            grads = [torch.empty_like(t) if n else None for t, n in zip(inputs, needs)]
+            p, k1 = _ptrs(list(inputs))
+            g, k2 = _ptrs(grads)
+            dout = dout.contiguous()
+            check(lib().ce_backward(self._h, p, ctypes.c_void_p(dout.data_ptr()), g, ctypes.byref(self.stats)))
+            del k1, k2
+        self._order_out(cur, grads)
         return grads
 
     def set_profiling(self, on: bool = True):
@@ -111,7 +141,7 @@ class Executor:
         check(lib().ce_executor_profile(self._h, int(backward), n_max, ctypes.byref(n), labels, len(labels), kinds,
                                         ms, fl, by))
         names = labels.value.decode().split("\n")
-        kind_names = ["direct", "tiled", "tc", "memset", "reduce"]
+        kind_names = ["direct", "tiled", "tc", "memset", "reduce", "permute"]
         return [(names[i], kind_names[kinds[i]], float(ms[i]), float(fl[i]), float(by[i])) for i in range(n.value)]
 
     def execute_host(self, host_inputs: Sequence["numpy.ndarray"], host_out: "numpy.ndarray"):  # noqa: F821
@@ -130,6 +160,7 @@ def pairwise_eval(ctx: Context, expr: str, a: torch.Tensor, b: torch.Tensor, mod
     """pairwise_eval (kernels.cpp:425-470) for expr "L,R->RES|convs" (keep = RES, order RES)."""
     from .api import Plan as _P  # result shape via a one-node plan
     shape = _P.optimal(expr, [list(a.shape), list(b.shape)], mode).out_dims
+    ctx.torch_stream.wait_stream(torch.cuda.current_stream(ctx.device))  # ce_pairwise_* syncs its own stream
     out = torch.empty(shape, dtype=torch.float32, device=a.device)
     d, r, _ = _dims_arg([list(a.shape), list(b.shape)])
     check(lib().ce_pairwise_eval(ctx.handle, expr.encode(), d, r, mode.encode(), ctypes.c_void_p(a.data_ptr()),
@@ -138,6 +169,7 @@ def pairwise_eval(ctx: Context, expr: str, a: torch.Tensor, b: torch.Tensor, mod
 
 
 def pairwise_grad(ctx: Context, expr: str, a, b, dout, mode: str = "same"):
+    ctx.torch_stream.wait_stream(torch.cuda.current_stream(ctx.device))
     da, db = torch.empty_like(a), torch.empty_like(b)
     d, r, _ = _dims_arg([list(a.shape), list(b.shape)])
     check(lib().ce_pairwise_grad(ctx.handle, expr.encode(), d, r, mode.encode(), ctypes.c_void_p(a.data_ptr()),
