@@ -308,6 +308,7 @@ ce_status ce_executor_create(ce_ctx* ctx, const ce_plan* plan, int want_backward
     ExecConfig cfg;
     cfg.math = ctx->opts.math;
     e->ex = std::make_unique<Executor>(plan->plan, want_backward != 0, cfg);
+    e->ex->set_use_graphs(ctx->opts.use_graphs != 0);
     *out = e.release();
   });
 }

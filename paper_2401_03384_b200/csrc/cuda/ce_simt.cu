@@ -412,35 +412,67 @@ cudaError_t ce_launch_tiled(const CeSimtDesc& d, const float* A, const float* B,
   return cudaGetLastError();
 }
 
-bool ce_permute_supported(const CeProblem& p) {
+namespace {
+// Merge axes that are contiguous in both input and output, drop extent-1 axes,
+// and pick the unit-stride axes of each side.  Returns false if not a 2-sided transpose.
+bool perm_desc(const CeProblem& p, CePermDesc* out) {
   if (!p.unary || p.ng_a) return false;
-  int vin = -1, vout = -1;
+  int64_t ext[CE_MAX_VARS], sa[CE_MAX_VARS], sc[CE_MAX_VARS];
+  int n = 0;
   for (int v = 0; v < p.nv; ++v) {
     if (p.cls[v] == CE_K || p.sa[v] == 0 || p.sc[v] == 0) return false;  // pure permutation only
-    if (p.sa[v] == 1) vin = v;
-    if (p.sc[v] == 1) vout = v;
+    if (p.ext[v] == 1) continue;
+    ext[n] = p.ext[v];
+    sa[n] = p.sa[v];
+    sc[n] = p.sc[v];
+    ++n;
   }
-  return vin >= 0 && vout >= 0 && vin != vout;
+  for (bool merged = true; merged;) {
+    merged = false;
+    for (int i = 0; i < n && !merged; ++i)
+      for (int j = 0; j < n && !merged; ++j)
+        if (i != j && sa[j] == sa[i] * ext[i] && sc[j] == sc[i] * ext[i]) {
+          ext[i] *= ext[j];
+          for (int k = j; k + 1 < n; ++k) {
+            ext[k] = ext[k + 1];
+            sa[k] = sa[k + 1];
+            sc[k] = sc[k + 1];
+          }
+          --n;
+          merged = true;
+        }
+  }
+  CePermDesc d{};
+  d.vin = d.vout = -1;
+  for (int v = 0; v < n; ++v) {
+    d.ext[v] = ext[v];
+    d.sa[v] = sa[v];
+    d.sc[v] = sc[v];
+    if (sa[v] == 1) d.vin = v;
+    if (sc[v] == 1) d.vout = v;
+  }
+  if (d.vin < 0 || d.vout < 0 || d.vin == d.vout) return false;
+  if ((ext[d.vout] + 31) / 32 > 65535) return false;
+  d.nbatch = 1;
+  for (int v = 0; v < n; ++v)
+    if (v != d.vin && v != d.vout) {
+      d.rest[d.nrest++] = v;
+      d.nbatch *= ext[v];
+    }
+  *out = d;
+  return true;
+}
+}  // namespace
+
+bool ce_permute_supported(const CeProblem& p) {
+  CePermDesc d;
+  return perm_desc(p, &d);
 }
 
 cudaError_t ce_launch_permute(const CeProblem& p, const float* A, float* C, cudaStream_t s) {
-  CePermDesc d{};
-  d.vin = d.vout = -1;
-  for (int v = 0; v < p.nv; ++v) {
-    d.ext[v] = p.ext[v];
-    d.sa[v] = p.sa[v];
-    d.sc[v] = p.sc[v];
-    if (p.sa[v] == 1 && d.vin < 0) d.vin = v;
-    if (p.sc[v] == 1 && d.vout < 0) d.vout = v;
-  }
-  if (d.vin < 0 || d.vout < 0 || d.vin == d.vout) return cudaErrorInvalidValue;
-  d.nbatch = 1;
-  for (int v = 0; v < p.nv; ++v)
-    if (v != d.vin && v != d.vout) {
-      d.rest[d.nrest++] = v;
-      d.nbatch *= p.ext[v];
-    }
-  const int64_t gx = (p.ext[d.vin] + 31) / 32, gy = (p.ext[d.vout] + 31) / 32;
+  CePermDesc d;
+  if (!perm_desc(p, &d)) return cudaErrorInvalidValue;
+  const int64_t gx = (d.ext[d.vin] + 31) / 32, gy = (d.ext[d.vout] + 31) / 32;
   if (gx > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
   const int64_t gz = std::min<int64_t>(d.nbatch, 65535);
   ce_transpose_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(gz)), 256, 0,

@@ -1,21 +1,29 @@
 // tcgen05 kind::tf32 implicit-GEMM kernel for sm_100a (families a + b1).
 //
-// One CTA = one 128 x BN output tile (x one K split).  128 threads:
-//   warp 0 lane 0 : TMA producer   (cp.async.bulk.tensor.5d -> smem ring, mbarrier tx)
-//   warp 1 lane 0 : MMA issuer     (tcgen05.mma.cta_group::1.kind::tf32, D in TMEM)
-//   warp 2        : TMEM allocator (tcgen05.alloc / dealloc)
-//   all 4 warps   : epilogue       (tcgen05.ld 32x32b -> registers -> scatter store)
-// Operand tiles are 128-byte rows with the hardware 128B swizzle shared by TMA and
-// the UMMA smem descriptors.  Convolution taps are K-loop iterations whose TMA
-// coordinates are shifted (ce_tc.h); Same/Full padding is TMA's OOB zero fill.
+// Persistent and warp-specialised: grid = min(#tiles, #SMs), each CTA walks the
+// tile list (m fastest, so CTAs running together share the B tile in L2).
+// 192 threads:
+//   warp 0 lane 0 : TMA producer   (cp.async.bulk.tensor.5d -> STAGES-deep smem ring)
+//   warp 1 lane 0 : MMA issuer     (tcgen05.mma.cta_group::1.kind::tf32 into one of two
+//                                    TMEM accumulators, tcgen05.commit -> mbarriers)
+//   warps 2..5    : epilogue       (tcgen05.ld 32x32b -> registers -> [smem transpose] ->
+//                                    global scatter / atomic add for split-K)
+// The two TMEM accumulators let the epilogue of tile t overlap the mainloop of
+// tile t+1.  Operand tiles are 128-byte K-major rows with the 128B swizzle shared
+// by TMA and the UMMA descriptors.  Convolution taps are K-loop iterations whose
+// TMA coordinates are shifted (ce_tc.h); Same/Full padding is TMA's OOB zero fill.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "ce_tc.h"
 
 namespace {
+
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -27,6 +35,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -49,11 +61,12 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
       : "memory");
 }
 
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  // SM100 UMMA shared-memory descriptor: start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
-  // version 1 [46,48), base offset 0, layout SWIZZLE_128B (2) [61,64).
-  return static_cast<uint64_t>((addr >> 4) & 0x3FFF) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
-         (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+// SM100 UMMA shared-memory descriptor, K-major SWIZZLE_128B: start>>4 [0,14),
+// LBO>>4 [16,30) (unused for swizzled K-major), SBO>>4 [32,46) = 1024 B between
+// 8-row groups, version 1 [46,48), layout SWIZZLE_128B (2) [61,64).
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t addr) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFF) | (1ull << 16) | (static_cast<uint64_t>(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -84,40 +97,34 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Value of every unit for this CTA (tile origins / grid digits); K units filled per iteration.
-__device__ __forceinline__ void tile_values(const TcParams& P, int32_t* val, int split_out[1]) {
-  for (int i = 0; i < P.nunits; ++i) val[i] = 0;
-  int64_t x = blockIdx.x;
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
+
+struct Tile {
+  int32_t val[TC_MAX_UNITS];  // tile origins / grid digits per unit (K units 0)
+  int split;
+};
+
+// Decode linear tile index t (m fastest, then n, then z, then K split).
+__device__ __forceinline__ void decode_tile(const TcParams& P, uint32_t t, Tile& T) {
+  for (int i = 0; i < TC_MAX_UNITS; ++i) T.val[i] = 0;
   for (int i = 0; i < P.nm; ++i) {
     const TcUnit& u = P.u[P.mt[i]];
-    const int32_t n = (u.ext + u.box - 1) / u.box;
-    val[P.mt[i]] = static_cast<int32_t>(x % n) * u.box;
-    x /= n;
+    const uint32_t n = static_cast<uint32_t>((u.ext + u.box - 1) / u.box);
+    T.val[P.mt[i]] = static_cast<int32_t>(t % n) * u.box;
+    t /= n;
   }
-  x = blockIdx.y;
   for (int i = 0; i < P.nn; ++i) {
     const TcUnit& u = P.u[P.nt[i]];
-    const int32_t n = (u.ext + u.box - 1) / u.box;
-    val[P.nt[i]] = static_cast<int32_t>(x % n) * u.box;
-    x /= n;
+    const uint32_t n = static_cast<uint32_t>((u.ext + u.box - 1) / u.box);
+    T.val[P.nt[i]] = static_cast<int32_t>(t % n) * u.box;
+    t /= n;
   }
-  x = blockIdx.z;
-  split_out[0] = static_cast<int>(x % P.k_split);
-  x /= P.k_split;
   for (int i = 0; i < P.ng; ++i) {
     const TcUnit& u = P.u[P.gu[i]];
-    val[P.gu[i]] = static_cast<int32_t>(x % u.ext);
-    x /= u.ext;
+    T.val[P.gu[i]] = static_cast<int32_t>(t % static_cast<uint32_t>(u.ext));
+    t /= static_cast<uint32_t>(u.ext);
   }
-}
-
-__device__ __forceinline__ void k_values(const TcParams& P, int it, int32_t* val) {
-  for (int i = 0; i < P.nk; ++i) {
-    const TcUnit& u = P.u[P.ku[i]];
-    const int32_t n = (u.ext + u.box - 1) / u.box;
-    val[P.ku[i]] = (it % n) * u.box;
-    it /= n;
-  }
+  T.split = static_cast<int>(t);
 }
 
 __device__ __forceinline__ void coords(const TcOperand& o, const int32_t* val, int c[5]) {
@@ -131,169 +138,242 @@ __device__ __forceinline__ void coords(const TcOperand& o, const int32_t* val, i
   }
 }
 
-// Offset in C of a tile-local index `local` along the given unit list (first fastest); -1 if outside.
+// Offset in C of tile-local index `local` along the unit list (first fastest); -1 if outside.
 __device__ __forceinline__ int64_t tile_offset(const TcParams& P, const int32_t* list, int n, const int32_t* val,
                                                int local) {
   int64_t off = 0;
+  uint32_t rest = static_cast<uint32_t>(local);
   for (int i = 0; i < n; ++i) {
     const TcUnit& u = P.u[list[i]];
-    const int d = local % u.box;
-    local /= u.box;
-    int64_t v = static_cast<int64_t>(val[list[i]]) + d;
-    if (v >= u.ext) return -1;
+    const uint32_t d = rest % static_cast<uint32_t>(u.box);
+    rest /= static_cast<uint32_t>(u.box);
+    uint32_t v = static_cast<uint32_t>(val[list[i]]) + d;
+    if (v >= static_cast<uint32_t>(u.ext)) return -1;
     for (int k = 0; k < u.nv; ++k) {
-      off += (v % u.vext[k]) * u.sc[k];
-      v /= u.vext[k];
+      off += static_cast<int64_t>(v % static_cast<uint32_t>(u.vext[k])) * u.sc[k];
+      v /= static_cast<uint32_t>(u.vext[k]);
     }
   }
-  return local == 0 ? off : -1;
+  return rest == 0 ? off : -1;
+}
+
+__device__ __forceinline__ void k_range(const TcParams& P, int split, int& k0, int& k1) {
+  const int per = (P.k_iters + P.k_split - 1) / P.k_split;
+  k0 = split * per;
+  k1 = min(P.k_iters, k0 + per);
 }
 
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(128, 1) ce_tc_kernel(const __grid_constant__ TcParams P, float* __restrict__ C) {
+__global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constant__ TcParams P, float* __restrict__ C) {
   constexpr int A_BYTES = TC_BM * 128;
   constexpr int B_BYTES = BN * 128;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  float* stage_out = reinterpret_cast<float*>(sB + STAGES * B_BYTES);      // [kEpiWarps][32][33]
+  int64_t* col_off = reinterpret_cast<int64_t*>(stage_out + kEpiWarps * 32 * 33);  // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(col_off + 2 * BN);
   uint64_t* empty = full + STAGES;
-  uint64_t* accf = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
-  int64_t* row_off = reinterpret_cast<int64_t*>(tmem_slot + 4);  // [128]
-  int64_t* col_off = row_off + TC_BM;                               // [BN]
+  uint64_t* tfull = empty + STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  int32_t val[TC_MAX_UNITS];
-  int split;
-  tile_values(P, val, &split);
+  const uint32_t n_tiles = static_cast<uint32_t>(P.tiles_m) * static_cast<uint32_t>(P.tiles_n) *
+                           static_cast<uint32_t>(P.grid_z) * static_cast<uint32_t>(P.k_split);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accf, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 32 * kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&P.ta) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&P.tb) : "memory");
   }
-  if (warp == 2) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  // epilogue address tables (independent of the mainloop)
-  for (int r = threadIdx.x; r < TC_BM; r += 128)
-    row_off[r] = r < P.m_rows ? tile_offset(P, P.mt, P.nm, val, r) : -1;
-  for (int c = threadIdx.x; c < BN; c += 128) col_off[c] = c < P.n_cols ? tile_offset(P, P.nt, P.nn, val, c) : -1;
-  int64_t base = 0;
-  for (int i = 0; i < P.ng; ++i) {
-    const TcUnit& u = P.u[P.gu[i]];
-    int64_t v = val[P.gu[i]];
-    for (int k = 0; k < u.nv; ++k) {
-      base += (v % u.vext[k]) * u.sc[k];
-      v /= u.vext[k];
-    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  const int per = (P.k_iters + P.k_split - 1) / P.k_split;
-  const int k0 = split * per;
-  const int k1 = min(P.k_iters, k0 + per);
-
-  if (warp == 0 && lane == 0) {
-    // ------------------------------------------------------------ TMA producer
-    const uint32_t bytes = static_cast<uint32_t>(P.oa.stage_bytes + P.ob.stage_bytes);
-    for (int it = k0, i = 0; it < k1; ++it, ++i) {
-      const int s = i % STAGES;
-      const uint32_t round = static_cast<uint32_t>(i / STAGES);
-      mbar_wait(&empty[s], (round & 1) ^ 1);
-      k_values(P, it, val);
-      mbar_expect_tx(&full[s], bytes);
-      int c[5];
-      coords(P.oa, val, c);
-      for (int j = 0; j < P.oa.nsub; ++j) {
-        int cj[5] = {c[0] + 32 * j, c[1], c[2], c[3], c[4]};
-        tma_load(sA + s * A_BYTES + j * 4096, &P.ta, &full[s], cj);
-      }
-      coords(P.ob, val, c);
-      for (int j = 0; j < P.ob.nsub; ++j) {
-        int cj[5] = {c[0] + 32 * j, c[1], c[2], c[3], c[4]};
-        tma_load(sB + s * B_BYTES + j * 4096, &P.tb, &full[s], cj);
-      }
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ------------------------------------------------------------ MMA issuer
-    for (int it = k0, i = 0; it < k1; ++it, ++i) {
-      const int s = i % STAGES;
-      const uint32_t round = static_cast<uint32_t>(i / STAGES);
-      mbar_wait(&full[s], round & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- TMA producer
+      const uint32_t bytes = static_cast<uint32_t>(P.oa.stage_bytes + P.ob.stage_bytes);
+      int step_a[6][5], step_b[6][5], kcount[6];
 #pragma unroll
-      for (int kk = 0; kk < TC_BK / 8; ++kk) {
-        // K-major: advance 32 B inside the swizzled 128-B row; MN-major: next 8-row K group (1 KB)
-        const uint64_t ad = P.oa.mn_major ? smem_desc(a0 + kk * 1024, P.mn_lbo, P.mn_sbo) : smem_desc(a0 + kk * 32, 16, 1024);
-        const uint64_t bd = P.ob.mn_major ? smem_desc(b0 + kk * 1024, P.mn_lbo, P.mn_sbo) : smem_desc(b0 + kk * 32, 16, 1024);
-        mma_tf32(tmem, ad, bd, P.idesc, (i > 0 || kk > 0) ? 1u : 0u);
-      }
-      mma_commit(&empty[s]);  // frees the smem slot once these MMAs retire
-    }
-    mma_commit(accf);  // accumulator complete
-  }
-  __syncwarp();
-
-  // ------------------------------------------------------------ epilogue
-  mbar_wait(accf, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int row = warp * 32 + lane;
-  const bool atomic = P.k_split > 1;
-  const bool empty_k = k1 <= k0;
-  float* stage = reinterpret_cast<float*>(sA) + warp * 32 * 33;  // mainloop smem is free now
-#pragma unroll 1
-  for (int ch = 0; ch < BN / 32; ++ch) {
-    if (ch * 32 >= P.n_cols) break;
-    uint32_t r[32];
-    tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + ch * 32, r);
-    if (empty_k)
-      for (int i = 0; i < 32; ++i) r[i] = 0;
-    if (P.transpose_store) {
-      for (int i = 0; i < 32; ++i) stage[lane * 33 + i] = __uint_as_float(r[i]);
-      __syncwarp();
-      const int64_t co = col_off[ch * 32 + lane];
-      for (int rr = 0; rr < 32; ++rr) {
-        const int64_t ro = row_off[warp * 32 + rr];
-        if (ro < 0 || co < 0) continue;
-        const float v = stage[rr * 33 + lane];
-        if (atomic)
-          atomicAdd(C + base + ro + co, v);
-        else
-          C[base + ro + co] = v;
-      }
-      __syncwarp();
-    } else {
-      const int64_t ro = row_off[row];
-      if (ro >= 0) {
-        for (int i = 0; i < 32; ++i) {
-          const int64_t co = col_off[ch * 32 + i];
-          if (co < 0) continue;
-          const float v = __uint_as_float(r[i]);
-          if (atomic)
-            atomicAdd(C + base + ro + co, v);
-          else
-            C[base + ro + co] = v;
+      for (int u = 0; u < 6; ++u) {
+        kcount[u] = P.kcount[u];
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          step_a[u][d] = P.kstep_a[u][d];
+          step_b[u][d] = P.kstep_b[u][d];
         }
       }
+      uint32_t gi = 0;  // global stage counter across tiles
+      Tile T;
+      for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        decode_tile(P, t, T);
+        int k0, k1;
+        k_range(P, T.split, k0, k1);
+        int baseA[5], baseB[5], dig[6];
+        coords(P.oa, T.val, baseA);
+        coords(P.ob, T.val, baseB);
+        int x = k0;
+#pragma unroll
+        for (int u = 0; u < 6; ++u) {
+          dig[u] = x % kcount[u];
+          x /= kcount[u];
+        }
+        for (int it = k0; it < k1; ++it, ++gi) {
+          const int s = static_cast<int>(gi % STAGES);
+          mbar_wait(&empty[s], ((gi / STAGES) & 1) ^ 1);
+          int ca[5], cb[5];
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            ca[d] = baseA[d];
+            cb[d] = baseB[d];
+#pragma unroll
+            for (int u = 0; u < 6; ++u) {
+              ca[d] += dig[u] * step_a[u][d];
+              cb[d] += dig[u] * step_b[u][d];
+            }
+          }
+          if (P.dbg & 2) {
+            mbar_arrive(&full[s]);
+          } else {
+            mbar_expect_tx(&full[s], bytes);
+            tma_load(sA + s * A_BYTES, &P.ta, &full[s], ca);
+            tma_load(sB + s * B_BYTES, &P.tb, &full[s], cb);
+          }
+#pragma unroll
+          for (int u = 0; u < 6; ++u) {
+            if (++dig[u] < kcount[u]) break;
+            dig[u] = 0;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- MMA issuer
+      uint32_t gi = 0, local = 0;
+      for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++local) {
+        const int acc = static_cast<int>(local & 1);
+        const int split = static_cast<int>(t / (n_tiles / static_cast<uint32_t>(P.k_split)));
+        int k0, k1;
+        k_range(P, split, k0, k1);
+        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d_tmem = tmem + static_cast<uint32_t>(acc * BN);
+        for (int it = k0; it < k1; ++it, ++gi) {
+          const int s = static_cast<int>(gi % STAGES);
+          mbar_wait(&full[s], (gi / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+          if (!(P.dbg & 1)) {
+#pragma unroll
+            for (int kk = 0; kk < TC_BK / 8; ++kk)  // K=8 per tf32 MMA: +32 B inside the 128-B row
+              mma_tf32(d_tmem, kmajor_desc(a0 + kk * 32), kmajor_desc(b0 + kk * 32), P.idesc,
+                       (it > k0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);  // frees the smem slot once these MMAs retire
+        }
+        mma_commit(&tfull[acc]);  // accumulator of this tile complete
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue warps
+    const int q = warp & 3;            // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;     // accumulator row owned by this thread
+    const int ew = warp - 2;           // 0..3
+    float* stage = stage_out + ew * 32 * 33;
+    const bool atomic = P.k_split > 1;
+    uint32_t local = 0;
+    Tile T;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++local) {
+      const int acc = static_cast<int>(local & 1);
+      decode_tile(P, t, T);
+      int k0, k1;
+      k_range(P, T.split, k0, k1);
+      // address tables for this tile (overlaps the MMAs)
+      int64_t* cols = col_off + acc * BN;
+      for (int c = threadIdx.x - 64; c < BN; c += 32 * kEpiWarps)
+        cols[c] = c < P.n_cols ? tile_offset(P, P.nt, P.nn, T.val, c) : -1;
+      int64_t base = 0;
+      for (int i = 0; i < P.ng; ++i) {
+        const TcUnit& u = P.u[P.gu[i]];
+        uint32_t v = static_cast<uint32_t>(T.val[P.gu[i]]);
+        for (int k = 0; k < u.nv; ++k) {
+          base += static_cast<int64_t>(v % static_cast<uint32_t>(u.vext[k])) * u.sc[k];
+          v /= static_cast<uint32_t>(u.vext[k]);
+        }
+      }
+      const int64_t ro = row < P.m_rows ? tile_offset(P, P.mt, P.nm, T.val, row) : -1;
+      float* crow = C + base + (ro < 0 ? 0 : ro);
+      epi_bar();  // column table visible to all epilogue warps
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const bool empty_k = k1 <= k0;
+      const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        if (ch * 32 >= P.n_cols) break;
+        uint32_t r[32];
+        tmem_ld32(t_base + ch * 32, r);
+        if (empty_k)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0;
+        if (P.transpose_store) {
+          // lanes write consecutive columns of one row: coalesced for column-contiguous outputs
+#pragma unroll
+          for (int i = 0; i < 32; ++i) stage[lane * 33 + i] = __uint_as_float(r[i]);
+          __syncwarp();
+          const int64_t co = cols[ch * 32 + lane];
+          float* cbase = C + base + co;
+#pragma unroll
+          for (int rr = 0; rr < 32; ++rr) {
+            const int64_t rrow = __shfl_sync(0xffffffffu, ro, rr);
+            const float v = stage[rr * 33 + lane];
+            if (rrow >= 0 && co >= 0) {
+              if (atomic)
+                atomicAdd(cbase + rrow, v);
+              else
+                cbase[rrow] = v;
+            }
+          }
+          __syncwarp();
+        } else if (ro >= 0) {
+          int64_t co[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) co[i] = cols[ch * 32 + i];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (co[i] < 0) continue;
+            if (atomic)
+              atomicAdd(crow + co[i], __uint_as_float(r[i]));
+            else
+              crow[co[i]] = __uint_as_float(r[i]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&tempty[acc]);  // accumulator may be overwritten by tile t+2
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -334,19 +414,40 @@ bool encode(CUtensorMap* map, const void* ptr, const uint64_t* gdim, const uint6
   return r == CUDA_SUCCESS;
 }
 
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 template <int BN, int STAGES>
 cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
-  constexpr int smem = STAGES * (TC_BM * 128 + BN * 128) + 1024 + 256 + (TC_BM + BN) * 8 + 64;
+  constexpr int smem = STAGES * (TC_BM * 128 + BN * 128) + kEpiWarps * 32 * 33 * 4 + 2 * BN * 8 + 128 + 1024;
+  static_assert(smem <= 227 * 1024, "shared memory budget");
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid(static_cast<unsigned>(P.tiles_m), static_cast<unsigned>(P.tiles_n),
-            static_cast<unsigned>(P.grid_z * P.k_split));
-  ce_tc_kernel<BN, STAGES><<<grid, 128, smem, s>>>(P, C);
+  const int64_t tiles = static_cast<int64_t>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_split;
+  const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
+  ce_tc_kernel<BN, STAGES><<<grid, kThreads, smem, s>>>(P, C);
   return cudaGetLastError();
+}
+
+int debug_flags() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CE_TC_DBG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 }  // namespace
@@ -354,11 +455,7 @@ cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
 cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C, cudaStream_t s) {
   if (!plan.valid) return cudaErrorInvalidValue;
   TcParams& P = plan.params;
-  P.mn_lbo = 4096;
-  P.mn_sbo = 1024;
-  if (const char* e = getenv("CE_MN_LBO")) P.mn_lbo = atoi(e);
-  if (const char* e = getenv("CE_MN_SBO")) P.mn_sbo = atoi(e);
-  if (const char* e = getenv("CE_IDESC_XOR")) P.idesc ^= static_cast<uint32_t>(strtoul(e, nullptr, 0));
+  P.dbg = debug_flags();
   if (plan.cached_a != A) {
     if (!encode(&P.ta, A, plan.gdim_a, plan.gstride_a, plan.box_a)) return cudaErrorInvalidValue;
     plan.cached_a = A;
@@ -367,6 +464,8 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
     if (!encode(&P.tb, B, plan.gdim_b, plan.gstride_b, plan.box_b)) return cudaErrorInvalidValue;
     plan.cached_b = B;
   }
+  if (static_cast<int64_t>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_split >= (1ll << 32))
+    return cudaErrorInvalidConfiguration;
   if (P.k_split > 1) {
     cudaError_t e = cudaMemsetAsync(C, 0, static_cast<size_t>(plan.out_span) * 4, s);
     if (e != cudaSuccess) return e;

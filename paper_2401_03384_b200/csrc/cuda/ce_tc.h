@@ -66,7 +66,12 @@ struct TcParams {
   int32_t transpose_store;// stage through smem so lanes write consecutive columns
   uint32_t idesc;         // tcgen05 instruction descriptor
   int32_t tiles_m, tiles_n, grid_z;
+  // K-loop odometer, precomputed on the host so the producer does no division:
+  // coordinate[d] = base[d] + sum_i digit_i * kstep_{a,b}[i][d], digit_i < kcount[i]
+  int32_t kcount[6];
+  int32_t kstep_a[6][5], kstep_b[6][5];
   int32_t mn_lbo, mn_sbo;  // MN-major descriptor strides (bytes)
+  int32_t dbg;             // debug: bit0 skip MMAs, bit1 skip TMA loads (timing experiments only)
 };
 
 // Host-side plan: everything except the pointer-dependent tensor maps.

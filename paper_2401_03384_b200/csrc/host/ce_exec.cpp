@@ -55,6 +55,54 @@ Executor::~Executor() {
       if (st.ev0) cudaEventDestroy(st.ev0);
       if (st.ev1) cudaEventDestroy(st.ev1);
     }
+  for (auto& g : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+}
+
+void Executor::launch_pass(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s, int which) {
+  if (!use_graphs_ || profiling_) {
+    run(steps, need, s);
+    return;
+  }
+  // replay key: every bound pointer plus the requested-gradient mask
+  std::vector<const void*> key;
+  key.reserve(steps.size() * 3 + 16);
+  for (const Step& st : steps) {
+    key.push_back(resolve(st.a));
+    key.push_back(resolve(st.b));
+    key.push_back(resolve(st.c));
+  }
+  if (need)
+    for (char c : *need) key.push_back(reinterpret_cast<const void*>(static_cast<uintptr_t>(c)));
+  GraphCache& g = graphs_[which];
+  if (g.exec && g.key == key) {
+    cuda_check(cudaGraphLaunch(g.exec, s), "cudaGraphLaunch");
+    last_launches_ = g.launches;
+    return;
+  }
+  cudaGraph_t graph = nullptr;
+  cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+  try {
+    run(steps, need, s);
+  } catch (...) {
+    cudaStreamEndCapture(s, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  cuda_check(cudaStreamEndCapture(s, &graph), "cudaStreamEndCapture");
+  if (g.exec) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(g.exec, graph, &info) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+    }
+  }
+  if (!g.exec) cuda_check(cudaGraphInstantiate(&g.exec, graph, 0), "cudaGraphInstantiate");
+  cudaGraphDestroy(graph);
+  g.key = std::move(key);
+  g.launches = last_launches_;
+  cuda_check(cudaGraphLaunch(g.exec, s), "cudaGraphLaunch");
 }
 
 namespace {
@@ -207,6 +255,22 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
         if (ce_tc_plan(q, &t)) {
           for (int side = 0; side < 2; ++side) {
             if (!(side ? pack_b : pack_a)) continue;
+            // an identical repack of the same buffer done by the forward pass is reused
+            // (forward always runs before backward on the same inputs)
+            const BufRef src = side ? b : a;
+            bool reused = false;
+            for (const PackRecord& r : packs_) {
+              if (r.src.kind != src.kind || r.src.index != src.index || r.pk.nv != pks[side].nv) continue;
+              bool same = true;
+              for (int v = 0; v < r.pk.nv && same; ++v)
+                same = r.pk.ext[v] == pks[side].ext[v] && r.pk.sa[v] == pks[side].sa[v] && r.pk.sc[v] == pks[side].sc[v];
+              if (same) {
+                (side ? b : a) = r.dst;
+                reused = true;
+                break;
+              }
+            }
+            if (reused) continue;
             Step ps;
             ps.kind = ce_permute_supported(pks[side]) ? Step::kPermute : Step::kDirect;
             ps.desc = simt_desc(pks[side]);
@@ -216,6 +280,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
             ps.label = label + (side ? ":packB" : ":packA");
             ps.bytes = 8.0 * operand_elems(pks[side], 0);
             (side ? b : a) = ps.c;
+            if (&list == &fwd_) packs_.push_back({src, pks[side], ps.c});
             list.push_back(ps);
           }
           p = q;
@@ -455,7 +520,7 @@ void Executor::forward(const float* const* inputs, float* out, cudaStream_t s) {
   inputs_.assign(inputs, inputs + n_);
   out_ = out;
   last_launches_ = 0;
-  run(fwd_, nullptr, s);
+  launch_pass(fwd_, nullptr, s, 0);
 }
 
 void Executor::backward(const float* const* inputs, const float* dout, float* const* dinputs, cudaStream_t s) {
@@ -472,7 +537,7 @@ void Executor::backward(const float* const* inputs, const float* dout, float* co
   dinputs_.assign(n_, nullptr);
   for (int i = 0; i < n_ && dinputs; ++i) dinputs_[static_cast<std::size_t>(i)] = dinputs[i];
   last_launches_ = 0;
-  run(bwd_, plan_.nodes.empty() ? nullptr : &need, s);
+  launch_pass(bwd_, plan_.nodes.empty() ? nullptr : &need, s, 1);
 }
 
 }  // namespace ce

@@ -101,6 +101,24 @@ class Executor {
   int last_launches_ = 0;
   bool profiling_ = false;
   double pending_flops_ = 0;  // FLOPs credited to the next add_problem (build time)
+  struct PackRecord {
+    BufRef src;
+    CeProblem pk;
+    BufRef dst;
+  };
+  std::vector<PackRecord> packs_;  // forward repacks, reusable by later steps
+  // CUDA-graph replay of a pass: valid while the bound pointers are unchanged
+  struct GraphCache {
+    std::vector<const void*> key;
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+  };
+  GraphCache graphs_[2];
+  bool use_graphs_ = false;
+  void launch_pass(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s, int which);
+
+ public:
+  void set_use_graphs(bool on) { use_graphs_ = on; }
 };
 
 }  // namespace ce

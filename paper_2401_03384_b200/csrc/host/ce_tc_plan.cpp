@@ -405,6 +405,24 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   }
   if (gz * split > 65535) return fail("grid z too large");
   P.k_split = split;
+  // K odometer steps: digit i of the K loop moves unit ku[i] by its box
+  for (int i = 0; i < 6; ++i) {
+    P.kcount[i] = 1;
+    for (int d = 0; d < 5; ++d) P.kstep_a[i][d] = P.kstep_b[i][d] = 0;
+  }
+  for (int i = 0; i < P.nk; ++i) {
+    const TcUnit& u = U[static_cast<std::size_t>(P.ku[i])];
+    P.kcount[i] = (u.ext + u.box - 1) / u.box;
+    for (int d = 0; d < 5; ++d) {
+      for (const auto* o : {&P.oa, &P.ob}) {
+        const TcDim& t = o->dim[d];
+        int step = 0;
+        if (t.u0 == P.ku[i]) step += t.c0 * u.box;
+        if (t.u1 == P.ku[i]) step += t.c1 * u.box;
+        (o == &P.oa ? P.kstep_a : P.kstep_b)[i][d] = step;
+      }
+    }
+  }
   // output span (for zeroing before split-K accumulation)
   int64_t span = 0;
   for (int v = 0; v < p.nv; ++v)

@@ -20,7 +20,8 @@ MATH = {"auto": 0, "tf32": 0, "fp32": 1, "simt": 1}
 class Context:
     """ce_ctx_create: binds a device and a stream (default: torch's current stream)."""
 
-    def __init__(self, device: int = 0, math: str = "auto", stream: Optional[torch.cuda.Stream] = None):
+    def __init__(self, device: int = 0, math: str = "auto", stream: Optional[torch.cuda.Stream] = None,
+                 graphs: bool = True):
         self.device = device
         self.math = math
         torch.cuda.set_device(device)
@@ -30,7 +31,7 @@ class Context:
             # use an explicit side stream instead so callers can order work on ctx.torch_stream
             st = torch.cuda.Stream(device)
         self.torch_stream = st
-        opts = _lib.Options(MATH[math], 0, ctypes.c_void_p(st.cuda_stream))
+        opts = _lib.Options(MATH[math], int(graphs), ctypes.c_void_p(st.cuda_stream))
         h = ctypes.c_void_p()
         check(lib().ce_ctx_create(device, ctypes.byref(opts), ctypes.byref(h)))
         self._h = h
