@@ -15,6 +15,7 @@
 
 #include "ce_device.h"
 #include "ce_kernels.h"
+#include "ce_launch.h"
 
 namespace {
 
@@ -33,6 +34,7 @@ __device__ __forceinline__ bool gather_index(const CeGather& g, int64_t p, int64
 // ----------------------------------------------------------------------------- direct
 __global__ void __launch_bounds__(256) ce_direct_kernel(const CeSimtDesc d, const float* __restrict__ A,
                                                         const float* __restrict__ B, float* __restrict__ C) {
+  ce_pdl_enter();
   const CeProblem& p = d.p;
   const int64_t total = d.Z * d.M * d.N;
   for (int64_t flat = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; flat < total;
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(256) ce_direct_kernel(const CeSimtDesc d, cons
 __global__ void __launch_bounds__(256) ce_reduce_kernel(const CeSimtDesc d, const float* __restrict__ A,
                                                         const float* __restrict__ B, float* __restrict__ C,
                                                         int64_t k_per_split) {
+  ce_pdl_enter();
   const CeProblem& p = d.p;
   __shared__ float warp_sum[8];
   int64_t val[CE_MAX_VARS];
@@ -160,6 +163,7 @@ __device__ __forceinline__ void decompose(int64_t x, const int32_t* vars, int n,
 __global__ void __launch_bounds__(256) ce_tiled_kernel(const CeSimtDesc d, const float* __restrict__ A,
                                                        const float* __restrict__ B, float* __restrict__ C,
                                                        int a_kfast, int b_kfast) {
+  ce_pdl_enter();
   const CeProblem& p = d.p;
   __shared__ float As[TK][TM + 4];
   __shared__ float Bs[TK][TN + 4];
@@ -319,18 +323,22 @@ __global__ void __launch_bounds__(256) ce_tiled_kernel(const CeSimtDesc d, const
 struct CePermDesc {
   int32_t nrest;
   int32_t vin, vout;       // indices into ext/sa/sc
+  int32_t same;            // 1: input and output share the unit-stride axis (vout = y axis)
   int64_t ext[CE_MAX_VARS], sa[CE_MAX_VARS], sc[CE_MAX_VARS];
   int32_t rest[CE_MAX_VARS];
   int64_t nbatch;
 };
 
+// 64x64 tile, 256 threads, 16 independent loads in flight per thread; 32-bit in-tile
+// index math, 64-bit only for the per-batch base.
 __global__ void __launch_bounds__(256) ce_transpose_kernel(const CePermDesc d, const float* __restrict__ A,
                                                            float* __restrict__ C) {
-  __shared__ float tile[32][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  const int64_t x0 = static_cast<int64_t>(blockIdx.x) * 32;  // along vin
-  const int64_t y0 = static_cast<int64_t>(blockIdx.y) * 32;  // along vout
-  const int64_t ein = d.ext[d.vin], eout = d.ext[d.vout];
+  ce_pdl_enter();
+  __shared__ float tile[64][65];
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+  const int x0 = static_cast<int>(blockIdx.x) * 64;          // along vin
+  const int y0 = static_cast<int>(blockIdx.y) * 64;          // along vout
+  const int ein = static_cast<int>(d.ext[d.vin]), eout = static_cast<int>(d.ext[d.vout]);
   const int64_t sa_out = d.sa[d.vout], sc_in = d.sc[d.vin];
   for (int64_t bt = blockIdx.z; bt < d.nbatch; bt += gridDim.z) {
     int64_t r = bt, bin = 0, bout = 0;
@@ -341,16 +349,39 @@ __global__ void __launch_bounds__(256) ce_transpose_kernel(const CePermDesc d, c
       bin += x * d.sa[v];
       bout += x * d.sc[v];
     }
+    const float* src = A + bin + x0 + tx + static_cast<int64_t>(y0) * sa_out;
+    const bool xin = x0 + tx < ein;
+    if (d.same) {
+      // both sides unit-stride along x: a strided row copy, coalesced without smem
+      float* dst = C + bout + x0 + tx + static_cast<int64_t>(y0) * d.sc[d.vout];
+      float v[16];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t y = y0 + ty + 8 * j, x = x0 + tx;
-      tile[ty + 8 * j][tx] = (x < ein && y < eout) ? __ldg(A + bin + x + y * sa_out) : 0.f;
+      for (int j = 0; j < 16; ++j) {
+        const int y = ty + 4 * j;
+        v[j] = (xin && y0 + y < eout) ? __ldg(src + static_cast<int64_t>(y) * sa_out) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int y = ty + 4 * j;
+        if (xin && y0 + y < eout) dst[static_cast<int64_t>(y) * d.sc[d.vout]] = v[j];
+      }
+      continue;
     }
-    __syncthreads();
+    float v[16];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t x = x0 + ty + 8 * j, y = y0 + tx;
-      if (x < ein && y < eout) C[bout + y + x * sc_in] = tile[tx][ty + 8 * j];
+    for (int j = 0; j < 16; ++j) {
+      const int y = ty + 4 * j;
+      v[j] = (xin && y0 + y < eout) ? __ldg(src + static_cast<int64_t>(y) * sa_out) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) tile[ty + 4 * j][tx] = v[j];
+    __syncthreads();
+    float* dst = C + bout + y0 + tx + static_cast<int64_t>(x0) * sc_in;
+    const bool yin = y0 + tx < eout;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int x = ty + 4 * j;
+      if (yin && x0 + x < ein) dst[static_cast<int64_t>(x) * sc_in] = tile[tx][x];
     }
     __syncthreads();
   }
@@ -358,6 +389,7 @@ __global__ void __launch_bounds__(256) ce_transpose_kernel(const CePermDesc d, c
 
 // ----------------------------------------------------------------------------- fill
 __global__ void ce_fill_kernel(float* __restrict__ dst, int64_t n, uint64_t seed) {
+  ce_pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t z = seed + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ULL;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -380,8 +412,7 @@ int grid_for(int64_t work, int threads) {
 cudaError_t ce_launch_direct(const CeSimtDesc& d, const float* A, const float* B, float* C, cudaStream_t s) {
   const int64_t total = d.Z * d.M * d.N;
   if (total == 0) return cudaSuccess;
-  ce_direct_kernel<<<grid_for(total, 256), 256, 0, s>>>(d, A, B, C);
-  return cudaGetLastError();
+  return ce_launch(ce_direct_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, d, A, B, C);
 }
 
 cudaError_t ce_launch_reduce(const CeSimtDesc& d, const float* A, const float* B, float* C, int64_t out_span,
@@ -398,8 +429,8 @@ cudaError_t ce_launch_reduce(const CeSimtDesc& d, const float* A, const float* B
     if (e != cudaSuccess) return e;
   }
   if (outs > 0x7fffffff) return cudaErrorInvalidConfiguration;
-  ce_reduce_kernel<<<dim3(static_cast<unsigned>(outs), static_cast<unsigned>(split)), 256, 0, s>>>(d, A, B, C, per);
-  return cudaGetLastError();
+  return ce_launch(ce_reduce_kernel, dim3(static_cast<unsigned>(outs), static_cast<unsigned>(split)), dim3(256), 0, s,
+                   d, A, B, C, per);
 }
 
 cudaError_t ce_launch_tiled(const CeSimtDesc& d, const float* A, const float* B, float* C, int a_kfast,
@@ -408,8 +439,7 @@ cudaError_t ce_launch_tiled(const CeSimtDesc& d, const float* A, const float* B,
   dim3 grid((unsigned)((d.M + TM - 1) / TM), (unsigned)((d.N + TN - 1) / TN),
             (unsigned)(d.Z < 65535 ? d.Z : 65535));
   if (grid.y > 65535) return cudaErrorInvalidConfiguration;
-  ce_tiled_kernel<<<grid, 256, 0, s>>>(d, A, B, C, a_kfast, b_kfast);
-  return cudaGetLastError();
+  return ce_launch(ce_tiled_kernel, grid, dim3(256), 0, s, d, A, B, C, a_kfast, b_kfast);
 }
 
 namespace {
@@ -451,8 +481,17 @@ bool perm_desc(const CeProblem& p, CePermDesc* out) {
     if (sa[v] == 1) d.vin = v;
     if (sc[v] == 1) d.vout = v;
   }
-  if (d.vin < 0 || d.vout < 0 || d.vin == d.vout) return false;
-  if ((ext[d.vout] + 31) / 32 > 65535) return false;
+  if (d.vin < 0 || d.vout < 0) return false;
+  if (d.vin == d.vout) {
+    // row copy: y = the axis with the smallest output stride among the others
+    int vy = -1;
+    for (int v = 0; v < n; ++v)
+      if (v != d.vin && (vy < 0 || sc[v] < sc[vy])) vy = v;
+    if (vy < 0) return false;
+    d.vout = vy;
+    d.same = 1;
+  }
+  if ((ext[d.vout] + 63) / 64 > 65535 || ext[d.vin] >= (1ll << 31) || ext[d.vout] >= (1ll << 31)) return false;
   d.nbatch = 1;
   for (int v = 0; v < n; ++v)
     if (v != d.vin && v != d.vout) {
@@ -472,16 +511,15 @@ bool ce_permute_supported(const CeProblem& p) {
 cudaError_t ce_launch_permute(const CeProblem& p, const float* A, float* C, cudaStream_t s) {
   CePermDesc d;
   if (!perm_desc(p, &d)) return cudaErrorInvalidValue;
-  const int64_t gx = (d.ext[d.vin] + 31) / 32, gy = (d.ext[d.vout] + 31) / 32;
+  const int64_t gx = (d.ext[d.vin] + 63) / 64, gy = (d.ext[d.vout] + 63) / 64;
   if (gx > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
   const int64_t gz = std::min<int64_t>(d.nbatch, 65535);
-  ce_transpose_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(gz)), 256, 0,
-                        s>>>(d, A, C);
-  return cudaGetLastError();
+  return ce_launch(ce_transpose_kernel,
+                   dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(gz)), dim3(256), 0,
+                   s, d, A, C);
 }
 
 cudaError_t ce_launch_fill(float* dst, int64_t n, uint64_t seed, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  ce_fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, n, seed);
-  return cudaGetLastError();
+  return ce_launch(ce_fill_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, dst, n, seed);
 }

@@ -18,12 +18,23 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "ce_launch.h"
 #include "ce_tc.h"
 
 namespace {
 
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
+
+// Debug-only phase timestamps (P.dbg & 32): [cta][slot] = %globaltimer (ns).
+__device__ unsigned long long g_tc_ts[160 * 8];
+__device__ __forceinline__ void stamp(const TcParams& P, int slot) {
+  if (P.dbg & 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 160) g_tc_ts[blockIdx.x * 8 + slot] = t;
+  }
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -180,6 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) stamp(P, 0);
   const uint32_t n_tiles = static_cast<uint32_t>(P.tiles_m) * static_cast<uint32_t>(P.tiles_n) *
                            static_cast<uint32_t>(P.grid_z) * static_cast<uint32_t>(P.k_split);
 
@@ -205,6 +217,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // setup above overlapped the previous kernel's tail (PDL); global memory only from here
+  ce_pdl_enter();
+  if (threadIdx.x == 0) stamp(P, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -263,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
           }
         }
       }
+      stamp(P, 2);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -287,10 +303,17 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
               mma_tf32(d_tmem, kmajor_desc(a0 + kk * 32), kmajor_desc(b0 + kk * 32), P.idesc,
                        (it > k0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&empty[s]);  // frees the smem slot once these MMAs retire
+          if (P.dbg & 16)
+            mbar_arrive(&empty[s]);  // timing experiment (only with MMAs skipped)
+          else
+            mma_commit(&empty[s]);  // frees the smem slot once these MMAs retire
         }
-        mma_commit(&tfull[acc]);  // accumulator of this tile complete
+        if (P.dbg & 16)
+          mbar_arrive(&tfull[acc]);
+        else
+          mma_commit(&tfull[acc]);  // accumulator of this tile complete
       }
+      stamp(P, 3);
     }
   } else {
     // ------------------------------------------------------------ epilogue warps
@@ -323,6 +346,12 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       float* crow = C + base + (ro < 0 ? 0 : ro);
       epi_bar();  // column table visible to all epilogue warps
       mbar_wait(&tfull[acc], (local >> 1) & 1);
+      if (threadIdx.x == 64 && local == 0) stamp(P, 4);
+      if (P.dbg & 8) {  // timing experiment: skip the epilogue body
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&tempty[acc]);
+        continue;
+      }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const bool empty_k = k1 <= k0;
       const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
@@ -334,7 +363,10 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
         if (empty_k)
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = 0;
-        if (P.transpose_store) {
+        if (P.dbg & 4) {
+          // timing experiment: TMEM loads only, no stores
+          if (r[0] == 0x7fffffffu) C[0] = 0.f;
+        } else if (P.transpose_store) {
           // lanes write consecutive columns of one row: coalesced for column-contiguous outputs
 #pragma unroll
           for (int i = 0; i < 32; ++i) stage[lane * 33 + i] = __uint_as_float(r[i]);
@@ -370,10 +402,12 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[acc]);  // accumulator may be overwritten by tile t+2
     }
+    if (threadIdx.x == 64) stamp(P, 5);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  if (threadIdx.x == 0) stamp(P, 6);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -437,8 +471,7 @@ cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
   }
   const int64_t tiles = static_cast<int64_t>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_split;
   const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
-  ce_tc_kernel<BN, STAGES><<<grid, kThreads, smem, s>>>(P, C);
-  return cudaGetLastError();
+  return ce_launch(ce_tc_kernel<BN, STAGES>, dim3(grid), dim3(kThreads), smem, s, P, C);
 }
 
 int debug_flags() {
@@ -475,4 +508,10 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
     case 128: return launch<128, 6>(P, C, s);
     default: return launch<256, 4>(P, C, s);
   }
+}
+
+// Debug only (not part of include/ce/ce.h): copy the phase timestamps of the last
+// launch with CE_TC_DBG & 32.  n <= 160*8.
+extern "C" int ce_debug_tc_timestamps(unsigned long long* out, int n) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_tc_ts, sizeof(unsigned long long) * n));
 }

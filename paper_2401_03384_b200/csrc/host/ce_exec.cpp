@@ -60,7 +60,28 @@ Executor::~Executor() {
 }
 
 void Executor::launch_pass(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s, int which) {
-  if (!use_graphs_ || profiling_) {
+  if (profiling_) {
+    // capture with per-step event records so the timings are back-to-back device time,
+    // free of host enqueue gaps; the graph is not cached
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    try {
+      run(steps, need, s);
+    } catch (...) {
+      cudaStreamEndCapture(s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    cuda_check(cudaStreamEndCapture(s, &graph), "cudaStreamEndCapture");
+    cuda_check(cudaGraphInstantiate(&exec, graph, 0), "cudaGraphInstantiate");
+    cuda_check(cudaGraphLaunch(exec, s), "cudaGraphLaunch");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    return;
+  }
+  if (!use_graphs_) {
     run(steps, need, s);
     return;
   }
@@ -486,7 +507,8 @@ void Executor::run(std::vector<Step>& steps, const std::vector<char>* need, cuda
         cuda_check(cudaEventCreate(&st.ev0), "cudaEventCreate");
         cuda_check(cudaEventCreate(&st.ev1), "cudaEventCreate");
       }
-      cuda_check(cudaEventRecord(st.ev0, s), "cudaEventRecord");
+      // External: inside stream capture this becomes an event-record node we can time
+      cuda_check(cudaEventRecordWithFlags(st.ev0, s, cudaEventRecordExternal), "cudaEventRecord");
     }
     cudaError_t e = cudaSuccess;
     switch (st.kind) {
@@ -498,7 +520,7 @@ void Executor::run(std::vector<Step>& steps, const std::vector<char>* need, cuda
       case Step::kPermute: e = ce_launch_permute(st.desc.p, A, C, s); break;
     }
     cuda_check(e, st.label.c_str());
-    if (profiling_) cuda_check(cudaEventRecord(st.ev1, s), "cudaEventRecord");
+    if (profiling_) cuda_check(cudaEventRecordWithFlags(st.ev1, s, cudaEventRecordExternal), "cudaEventRecord");
     ++last_launches_;
   }
 }

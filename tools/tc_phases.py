@@ -1,0 +1,32 @@
+"""Phase timestamps of one TC launch (CE_TC_DBG=32): python tools/tc_phases.py tk 0.1 <step-label>"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["CE_TC_DBG"] = str(32 | int(os.environ.get("EXTRA_DBG", "0")))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2401_03384_b200 as ce  # noqa: E402
+from paper_2401_03384_b200 import _lib  # noqa: E402
+from paper_2401_03384_b200.device import Context, pairwise_eval  # noqa: E402
+
+ctx = Context(0, "auto", graphs=False)
+torch.cuda.set_stream(ctx.torch_stream)
+# the first GEMM of the TK layer: X (packed) . W2
+expr = os.environ.get("EXPR", "bshw,rs->bhwr")
+dims = eval(os.environ.get("DIMS", "[[128,256,14,14],[57,256]]"))
+a = ctx.fill_random(dims[0], 1)
+b = ctx.fill_random(dims[1], 2)
+for _ in range(3):
+    pairwise_eval(ctx, expr, a, b)
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * (160 * 8))()
+_lib.lib().ce_debug_tc_timestamps(buf, 160 * 8)
+ts = np.array(buf, dtype=np.float64).reshape(160, 8)[:148]
+t0 = ts[:, 0].min()
+names = ["start", "setup", "producer_end", "mma_end", "epi_first_tile", "epi_end", "end"]
+for i, n in enumerate(names):
+    v = (ts[:, i] - t0) / 1e3
+    print(f"{n:16s} min {v.min():8.2f} us  median {np.median(v):8.2f} us  max {v.max():8.2f} us")
