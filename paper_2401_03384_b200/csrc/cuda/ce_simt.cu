@@ -324,6 +324,10 @@ struct CePermDesc {
   int32_t nrest;
   int32_t vin, vout;       // indices into ext/sa/sc
   int32_t same;            // 1: input and output share the unit-stride axis (vout = y axis)
+  // composite tile axes for short unit-stride axes: x = x1 + ext[vin]*x2 where x2 = vin2
+  // continues vin in the INPUT; y = y1 + ext[vout]*y2 where y2 = vout2 continues vout in
+  // the OUTPUT (-1: none)
+  int32_t vin2, vout2;
   int64_t ext[CE_MAX_VARS], sa[CE_MAX_VARS], sc[CE_MAX_VARS];
   int32_t rest[CE_MAX_VARS];
   int64_t nbatch;
@@ -334,12 +338,15 @@ struct CePermDesc {
 __global__ void __launch_bounds__(256) ce_transpose_kernel(const CePermDesc d, const float* __restrict__ A,
                                                            float* __restrict__ C) {
   ce_pdl_enter();
-  __shared__ float tile[64][65];
-  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
-  const int x0 = static_cast<int>(blockIdx.x) * 64;          // along vin
-  const int y0 = static_cast<int>(blockIdx.y) * 64;          // along vout
-  const int ein = static_cast<int>(d.ext[d.vin]), eout = static_cast<int>(d.ext[d.vout]);
-  const int64_t sa_out = d.sa[d.vout], sc_in = d.sc[d.vin];
+  __shared__ float tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int64_t x0 = static_cast<int64_t>(blockIdx.x) * 32;  // along vin (+vin2)
+  const int64_t y0 = static_cast<int64_t>(blockIdx.y) * 32;  // along vout (+vout2)
+  const uint32_t ex1 = static_cast<uint32_t>(d.ext[d.vin]), ey1 = static_cast<uint32_t>(d.ext[d.vout]);
+  const int64_t ein = d.ext[d.vin] * (d.vin2 >= 0 ? d.ext[d.vin2] : 1);
+  const int64_t eout = d.ext[d.vout] * (d.vout2 >= 0 ? d.ext[d.vout2] : 1);
+  const int64_t sa_y1 = d.sa[d.vout], sa_y2 = d.vout2 >= 0 ? d.sa[d.vout2] : 0;
+  const int64_t sc_x1 = d.sc[d.vin], sc_x2 = d.vin2 >= 0 ? d.sc[d.vin2] : 0;
   for (int64_t bt = blockIdx.z; bt < d.nbatch; bt += gridDim.z) {
     int64_t r = bt, bin = 0, bout = 0;
     for (int i = 0; i < d.nrest; ++i) {
@@ -349,41 +356,69 @@ __global__ void __launch_bounds__(256) ce_transpose_kernel(const CePermDesc d, c
       bin += x * d.sa[v];
       bout += x * d.sc[v];
     }
-    const float* src = A + bin + x0 + tx + static_cast<int64_t>(y0) * sa_out;
-    const bool xin = x0 + tx < ein;
-    if (d.same) {
-      // both sides unit-stride along x: a strided row copy, coalesced without smem
-      float* dst = C + bout + x0 + tx + static_cast<int64_t>(y0) * d.sc[d.vout];
-      float v[16];
+    if (d.vout2 >= 0) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int y = ty + 4 * j;
-        v[j] = (xin && y0 + y < eout) ? __ldg(src + static_cast<int64_t>(y) * sa_out) : 0.f;
+      for (int j = 0; j < 4; ++j) {
+        const int64_t y = y0 + ty + 8 * j, x = x0 + tx;
+        const uint32_t y1 = static_cast<uint32_t>(y) % ey1, y2 = static_cast<uint32_t>(y) / ey1;
+        tile[ty + 8 * j][tx] = (x < ein && y < eout) ? __ldg(A + bin + x + y1 * sa_y1 + y2 * sa_y2) : 0.f;
       }
+    } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int y = ty + 4 * j;
-        if (xin && y0 + y < eout) dst[static_cast<int64_t>(y) * d.sc[d.vout]] = v[j];
+      for (int j = 0; j < 4; ++j) {
+        const int64_t y = y0 + ty + 8 * j, x = x0 + tx;
+        tile[ty + 8 * j][tx] = (x < ein && y < eout) ? __ldg(A + bin + x + y * sa_y1) : 0.f;
       }
-      continue;
-    }
-    float v[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int y = ty + 4 * j;
-      v[j] = (xin && y0 + y < eout) ? __ldg(src + static_cast<int64_t>(y) * sa_out) : 0.f;
-    }
-#pragma unroll
-    for (int j = 0; j < 16; ++j) tile[ty + 4 * j][tx] = v[j];
-    __syncthreads();
-    float* dst = C + bout + y0 + tx + static_cast<int64_t>(x0) * sc_in;
-    const bool yin = y0 + tx < eout;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int x = ty + 4 * j;
-      if (yin && x0 + x < ein) dst[static_cast<int64_t>(x) * sc_in] = tile[tx][x];
     }
     __syncthreads();
+    if (d.vin2 >= 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t x = x0 + ty + 8 * j, y = y0 + tx;
+        const uint32_t x1 = static_cast<uint32_t>(x) % ex1, x2 = static_cast<uint32_t>(x) / ex1;
+        if (x < ein && y < eout) C[bout + y + x1 * sc_x1 + x2 * sc_x2] = tile[tx][ty + 8 * j];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t x = x0 + ty + 8 * j, y = y0 + tx;
+        if (x < ein && y < eout) C[bout + y + x * sc_x1] = tile[tx][ty + 8 * j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Input and output share the unit-stride axis x: a strided copy of rows (x, y) per
+// batch slice.  (x, y) is flattened so short rows still give coalesced warps.
+__global__ void __launch_bounds__(256, 4) ce_rowcopy_kernel(const CePermDesc d, const float* __restrict__ A,
+                                                            float* __restrict__ C) {
+  ce_pdl_enter();
+  const uint32_t ex = static_cast<uint32_t>(d.ext[d.vin]);
+  const uint32_t n = ex * static_cast<uint32_t>(d.ext[d.vout]);
+  const int64_t sa_y = d.sa[d.vout], sc_y = d.sc[d.vout];
+  for (int64_t bt = blockIdx.y; bt < d.nbatch; bt += gridDim.y) {
+    int64_t r = bt, bin = 0, bout = 0;
+    for (int i = 0; i < d.nrest; ++i) {
+      const int v = d.rest[i];
+      const int64_t x = r % d.ext[v];
+      r /= d.ext[v];
+      bin += x * d.sa[v];
+      bout += x * d.sc[v];
+    }
+    for (uint32_t f = blockIdx.x * 256 * 8 + threadIdx.x; f < n; f += gridDim.x * 256 * 8) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t g = f + j * 256;
+        v[j] = g < n ? __ldg(A + bin + (g % ex) + static_cast<int64_t>(g / ex) * sa_y) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t g = f + j * 256;
+        if (g < n) C[bout + (g % ex) + static_cast<int64_t>(g / ex) * sc_y] = v[j];
+      }
+    }
   }
 }
 
@@ -482,6 +517,19 @@ bool perm_desc(const CeProblem& p, CePermDesc* out) {
     if (sc[v] == 1) d.vout = v;
   }
   if (d.vin < 0 || d.vout < 0) return false;
+  d.vin2 = d.vout2 = -1;
+  if (d.vin != d.vout) {
+    // short unit-stride axes borrow the axis that continues them on their own side
+    if (ext[d.vin] < 32)
+      for (int v = 0; v < n; ++v)
+        if (v != d.vin && v != d.vout && sa[v] == ext[d.vin]) d.vin2 = v;
+    if (ext[d.vout] < 32)
+      for (int v = 0; v < n; ++v)
+        if (v != d.vin && v != d.vout && v != d.vin2 && sc[v] == ext[d.vout]) d.vout2 = v;
+    const int64_t ein = ext[d.vin] * (d.vin2 >= 0 ? ext[d.vin2] : 1);
+    const int64_t eout = ext[d.vout] * (d.vout2 >= 0 ? ext[d.vout2] : 1);
+    if (ein >= (1ll << 31) || eout >= (1ll << 31) || (eout + 31) / 32 > 65535) return false;
+  }
   if (d.vin == d.vout) {
     // row copy: y = the axis with the smallest output stride among the others
     int vy = -1;
@@ -491,10 +539,10 @@ bool perm_desc(const CeProblem& p, CePermDesc* out) {
     d.vout = vy;
     d.same = 1;
   }
-  if ((ext[d.vout] + 63) / 64 > 65535 || ext[d.vin] >= (1ll << 31) || ext[d.vout] >= (1ll << 31)) return false;
+  if ((ext[d.vout] + 31) / 32 > 65535 || ext[d.vin] >= (1ll << 31) || ext[d.vout] >= (1ll << 31)) return false;
   d.nbatch = 1;
   for (int v = 0; v < n; ++v)
-    if (v != d.vin && v != d.vout) {
+    if (v != d.vin && v != d.vout && v != d.vin2 && v != d.vout2) {
       d.rest[d.nrest++] = v;
       d.nbatch *= ext[v];
     }
@@ -511,7 +559,18 @@ bool ce_permute_supported(const CeProblem& p) {
 cudaError_t ce_launch_permute(const CeProblem& p, const float* A, float* C, cudaStream_t s) {
   CePermDesc d;
   if (!perm_desc(p, &d)) return cudaErrorInvalidValue;
-  const int64_t gx = (d.ext[d.vin] + 63) / 64, gy = (d.ext[d.vout] + 63) / 64;
+  if (d.same) {
+    const int64_t n = d.ext[d.vin] * d.ext[d.vout];
+    if (n >= (1ll << 31)) return cudaErrorInvalidConfiguration;
+    const int64_t per_slice = (n + 2047) / 2048;
+    const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(per_slice, (148 * 16 + d.nbatch - 1) / d.nbatch));
+    const int64_t gy = std::min<int64_t>(d.nbatch, 65535);
+    return ce_launch(ce_rowcopy_kernel, dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), dim3(256), 0, s, d,
+                     A, C);
+  }
+  const int64_t ein = d.ext[d.vin] * (d.vin2 >= 0 ? d.ext[d.vin2] : 1);
+  const int64_t eout = d.ext[d.vout] * (d.vout2 >= 0 ? d.ext[d.vout2] : 1);
+  const int64_t gx = (ein + 31) / 32, gy = (eout + 31) / 32;
   if (gx > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
   const int64_t gz = std::min<int64_t>(d.nbatch, 65535);
   return ce_launch(ce_transpose_kernel,
