@@ -177,6 +177,7 @@ def main():
 
     import paper_2401_03384_b200 as ce
     from paper_2401_03384_b200.device import Context, Executor
+    from paper_2401_03384_b200.parallel import allreduce_factor_grads
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -207,10 +208,8 @@ def main():
             launches += l["ex"].stats.kernels_launched
             grads = l["ex"].backward(l["xs"], l["dout"])
             launches += l["ex"].stats.kernels_launched
-            if world > 1:
-                for g in grads[1:]:  # factor gradients only; X gradients stay sharded
-                    dist.all_reduce(g)
-                    launches += 1
+            if world > 1:  # factor gradients only (one bucketed NCCL all-reduce); X gradients stay sharded
+                grads = allreduce_factor_grads(grads)
             l["grads"] = grads
         return launches
 
@@ -273,8 +272,7 @@ def main():
                 out = l["ex"].execute(din, l["out"])
                 grads = l["ex"].backward(din, ddout)
                 if world > 1:
-                    for g in grads[1:]:
-                        dist.all_reduce(g)
+                    grads = allreduce_factor_grads(grads)
                 hout.copy_(out, non_blocking=True)
                 for h, g in zip(hg, grads):
                     h.copy_(g, non_blocking=True)

@@ -364,11 +364,13 @@ __global__ void __launch_bounds__(256) ce_transpose_kernel(const CePermDesc d, c
         tile[ty + 8 * j][tx] = (x < ein && y < eout) ? __ldg(A + bin + x + y1 * sa_y1 + y2 * sa_y2) : 0.f;
       }
     } else {
+      // pointer increments + hoisted bounds: this kernel is instruction-bound otherwise
+      const bool xok = x0 + tx < ein;
+      const float* src = A + bin + x0 + tx + (y0 + ty) * sa_y1;
+      const int64_t step = 8 * sa_y1;
+      const int64_t yrem = eout - (y0 + ty);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t y = y0 + ty + 8 * j, x = x0 + tx;
-        tile[ty + 8 * j][tx] = (x < ein && y < eout) ? __ldg(A + bin + x + y * sa_y1) : 0.f;
-      }
+      for (int j = 0; j < 4; ++j) tile[ty + 8 * j][tx] = (xok && 8 * j < yrem) ? __ldg(src + j * step) : 0.f;
     }
     __syncthreads();
     if (d.vin2 >= 0) {
@@ -379,11 +381,13 @@ __global__ void __launch_bounds__(256) ce_transpose_kernel(const CePermDesc d, c
         if (x < ein && y < eout) C[bout + y + x1 * sc_x1 + x2 * sc_x2] = tile[tx][ty + 8 * j];
       }
     } else {
+      const bool yok = y0 + tx < eout;
+      float* dst = C + bout + y0 + tx + (x0 + ty) * sc_x1;
+      const int64_t step = 8 * sc_x1;
+      const int64_t xrem = ein - (x0 + ty);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t x = x0 + ty + 8 * j, y = y0 + tx;
-        if (x < ein && y < eout) C[bout + y + x * sc_x1] = tile[tx][ty + 8 * j];
-      }
+      for (int j = 0; j < 4; ++j)
+        if (yok && 8 * j < xrem) dst[j * step] = tile[tx][ty + 8 * j];
     }
     __syncthreads();
   }

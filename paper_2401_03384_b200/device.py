@@ -212,9 +212,10 @@ class _ConvEinsumFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dout):
         ts = ctx.saved_tensors
-        # re-run forward so the executor's intermediates match these inputs
+        # the executor's workspace holds the intermediates of its LAST forward; another
+        # call may have run since, so recompute them for these inputs
         ctx.ex.execute(list(ts))
-        grads = ctx.ex.backward(list(ts), dout.contiguous(), [t.requires_grad for t in ts] if False else None)
+        grads = ctx.ex.backward(list(ts), dout.contiguous(), list(ctx.needs_input_grad[3:]))
         return (None, None, None, *grads)
 
 

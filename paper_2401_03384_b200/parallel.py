@@ -1,0 +1,65 @@
+"""Batch-mode data parallelism for tensorized conv layers.
+
+`b` appears only in the layer input X and the output of every layer expression
+(reference layers.cpp:159-176, 180-318), so each sample's output depends only on
+its own X slice and the (replicated) factors.  One process per GPU:
+  * X and dY are split contiguously along `b` (shard_batch),
+  * factors are replicated (same SplitMix64 seeds on every rank),
+  * forward and backward run locally through libce,
+  * the only collective is a SUM all-reduce of the factor gradients
+    (allreduce_factor_grads), NCCL over NVLink on B200, gloo in the CPU tests.
+Input (X) gradients stay sharded.  The compute function is pluggable so the
+same host logic is exercised by the gloo tests with the FP64 oracle on CPU.
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(batch: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous [lo, hi) slice of the batch owned by `rank` (earlier ranks take the remainder)."""
+    base, rem = divmod(batch, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def shard_batch(x: torch.Tensor, rank: int, world: int, axis: int = 0) -> torch.Tensor:
+    lo, hi = shard_range(x.shape[axis], rank, world)
+    return x.narrow(axis, lo, hi - lo).contiguous()
+
+
+def allreduce_factor_grads(grads: Sequence[Optional[torch.Tensor]], group=None,
+                           skip: Sequence[int] = (0,)) -> List[Optional[torch.Tensor]]:
+    """SUM all-reduce of every gradient except those in `skip` (the batch-sharded X).
+
+    Factor gradients of one layer are flattened into a single buffer so the layer
+    costs one collective (bucketed like DDP), then scattered back in place."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return list(grads)
+    idx = [i for i, g in enumerate(grads) if g is not None and i not in skip]
+    if not idx:
+        return list(grads)
+    flat = torch.cat([grads[i].reshape(-1) for i in idx])
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    out = list(grads)
+    pos = 0
+    for i in idx:
+        n = grads[i].numel()
+        out[i] = flat[pos:pos + n].view_as(grads[i])
+        pos += n
+    return out
+
+
+def data_parallel_step(inputs: Sequence[torch.Tensor], dout: torch.Tensor, rank: int, world: int,
+                       fwd_bwd: Callable[[List[torch.Tensor], torch.Tensor], Tuple[torch.Tensor, List[torch.Tensor]]],
+                       group=None):
+    """Shard X and dY along b, run `fwd_bwd` on the local shard, all-reduce factor grads.
+
+    Returns (local output shard, [local dX shard, reduced factor grads...])."""
+    xs = [shard_batch(inputs[0], rank, world)] + list(inputs[1:])
+    dy = shard_batch(dout, rank, world)
+    out, grads = fwd_bwd(xs, dy)
+    return out, allreduce_factor_grads(grads, group)

@@ -205,6 +205,42 @@ def test_cp_layer_gradients_vs_oracle(any_ctx):
         assert nerr(g.cpu().numpy(), r) <= TOL[mode][1]
 
 
+def test_conv_einsum_autograd(ctx):
+    """The paper's call form conv_einsum("...", T1, T2, ...) as a torch autograd op."""
+    import paper_2401_03384_b200 as ce
+    le = _layer("cp", 16, 12, 8, 3, [4])
+    rng = np.random.default_rng(8)
+    ins = [f32(rng.uniform(-1, 1, d)) for d in le.dims]
+    xs = [dev(x).reshape(d).requires_grad_(True) for x, d in zip(ins, le.dims)]
+    y = ce.conv_einsum(le.expr, *xs)
+    dy = f32(rng.uniform(-1, 1, list(y.shape)))
+    y.backward(dev(dy).reshape(y.shape))
+    torch.cuda.synchronize()
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    nodes = [(n["left"], n["right"], n["result"]) for n in json.loads(plan.to_json())["nodes"]]
+    ref_y, _ = npo.execute(le.expr, le.dims, nodes, ins)
+    ref_g = npo.backward(le.expr, le.dims, nodes, ins, dy)
+    assert nerr(y.detach().cpu().numpy(), ref_y) <= TOL["auto"][0]
+    for x, r in zip(xs, ref_g):
+        assert nerr(x.grad.cpu().numpy(), r) <= TOL["auto"][1]
+
+
+def test_graph_replay_and_pointer_change(ctx):
+    """CUDA-graph replay must track new input pointers (re-capture) and stay correct."""
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import Executor
+    le = _layer("tk", 32, 24, 8, 4, [6, 5])
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    ex = Executor(ctx, plan, backward=True)
+    nodes = [(n["left"], n["right"], n["result"]) for n in json.loads(plan.to_json())["nodes"]]
+    for seed in (1, 2, 2, 3):
+        xs = [ctx.fill_random(d, seed * 100 + i) for i, d in enumerate(le.dims)]
+        y = ex.execute(xs)
+        torch.cuda.synchronize()
+        ref, _ = npo.execute(le.expr, le.dims, nodes, [x.double().cpu().numpy() for x in xs])
+        assert nerr(y.cpu().numpy(), ref) <= TOL["auto"][0]
+
+
 def test_native_library_loaded(ctx):
     maps = open("/proc/self/maps").read()
     assert "libce.so" in maps
