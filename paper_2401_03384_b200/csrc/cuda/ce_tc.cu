@@ -24,7 +24,8 @@
 namespace {
 
 constexpr int kEpiWarps = 4;
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kXposeWarps = 4;  // in-smem MN-major -> K-major transposers (warps 6..9)
+constexpr int kThreads = 64 + 32 * kEpiWarps + 32 * kXposeWarps;
 
 // Debug-only phase timestamps (P.dbg & 32): [cta][slot] = %globaltimer (ns).
 __device__ unsigned long long g_tc_ts[160 * 8];
@@ -110,6 +111,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
 
+// In-place transpose of one 4 KB SWIZZLE_128B block from the TMA MN-major layout
+// ([32 K rows][32 MN], row k at k*128, 16-B chunk c/4 stored at chunk (c/4)^(k%8))
+// to the UMMA K-major layout ([32 MN rows][32 K], chunk kk/4 of row r at (kk/4)^(r%8)).
+// Lane l reads MN column l (conflict-free: one 128-B row per step), then writes its
+// K-major row with 16-B stores (conflict-free per 8-lane phase).
+__device__ __forceinline__ void xpose_block(uint8_t* blk, int lane) {
+  float v[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    v[k] = *reinterpret_cast<const float*>(blk + k * 128 + (((lane >> 2) ^ (k & 7)) << 4) + ((lane & 3) << 2));
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(blk + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+}
+
 struct Tile {
   int32_t val[TC_MAX_UNITS];  // tile origins / grid digits per unit (K units 0)
   int split;
@@ -188,7 +206,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ready = tempty + 2;       // [STAGES] stage transposed to K-major (MN-major operands only)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + STAGES);
+  const bool xpose = P.oa.mn_major || P.ob.mn_major;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) stamp(P, 0);
@@ -199,6 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&ready[s], 32 * kXposeWarps);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -268,8 +289,15 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
             mbar_arrive(&full[s]);
           } else {
             mbar_expect_tx(&full[s], bytes);
-            tma_load(sA + s * A_BYTES, &P.ta, &full[s], ca);
-            tma_load(sB + s * B_BYTES, &P.tb, &full[s], cb);
+            // K-major: one box; MN-major: nsub boxes of [32 K rows][32 MN] at 4 KB steps
+            for (int j = 0; j < P.oa.nsub; ++j) {
+              const int cj[5] = {ca[0] + 32 * j, ca[1], ca[2], ca[3], ca[4]};
+              tma_load(sA + s * A_BYTES + j * 4096, &P.ta, &full[s], cj);
+            }
+            for (int j = 0; j < P.ob.nsub; ++j) {
+              const int cj[5] = {cb[0] + 32 * j, cb[1], cb[2], cb[3], cb[4]};
+              tma_load(sB + s * B_BYTES + j * 4096, &P.tb, &full[s], cj);
+            }
           }
 #pragma unroll
           for (int u = 0; u < 6; ++u) {
@@ -294,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
         const uint32_t d_tmem = tmem + static_cast<uint32_t>(acc * BN);
         for (int it = k0; it < k1; ++it, ++gi) {
           const int s = static_cast<int>(gi % STAGES);
-          mbar_wait(&full[s], (gi / STAGES) & 1);
+          mbar_wait(xpose ? &ready[s] : &full[s], (gi / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
           if (!(P.dbg & 1)) {
@@ -314,6 +342,29 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
           mma_commit(&tfull[acc]);  // accumulator of this tile complete
       }
       stamp(P, 3);
+    }
+  } else if (warp >= 2 + kEpiWarps) {
+    // ------------------------------------------------------------ transposer warps
+    // MN-major operand boxes -> K-major layout in place, then hand the stage to the MMA.
+    if (xpose) {
+      const int xw = warp - (2 + kEpiWarps);
+      uint32_t gi = 0;
+      for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int split = static_cast<int>(t / (n_tiles / static_cast<uint32_t>(P.k_split)));
+        int k0, k1;
+        k_range(P, split, k0, k1);
+        for (int it = k0; it < k1; ++it, ++gi) {
+          const int s = static_cast<int>(gi % STAGES);
+          mbar_wait(&full[s], (gi / STAGES) & 1);
+          if (P.oa.mn_major)
+            for (int j = xw; j < P.oa.nsub; j += kXposeWarps) xpose_block(sA + s * A_BYTES + j * 4096, lane);
+          if (P.ob.mn_major)
+            for (int j = xw; j < P.ob.nsub; j += kXposeWarps) xpose_block(sB + s * B_BYTES + j * 4096, lane);
+          // generic-proxy smem writes must be visible to the tensor core (async proxy)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&ready[s]);
+        }
+      }
     }
   } else {
     // ------------------------------------------------------------ epilogue warps
@@ -461,7 +512,8 @@ int sm_count() {
 
 template <int BN, int STAGES>
 cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
-  constexpr int smem = STAGES * (TC_BM * 128 + BN * 128) + kEpiWarps * 32 * 33 * 4 + 2 * BN * 8 + 128 + 1024;
+  constexpr int smem =
+      STAGES * (TC_BM * 128 + BN * 128) + kEpiWarps * 32 * 33 * 4 + 2 * BN * 8 + 8 * (2 * STAGES + 4) + 16 + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static bool configured = false;
   if (!configured) {

@@ -310,6 +310,34 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
         }
       }
     }
+    if (ok && st.tc.params.oa.mn_major && st.tc.params.ob.mn_major && st.tc.params.k_iters > 64) {
+      // Both operands would be transposed in shared memory every stage: over a long K
+      // loop that is smem-bandwidth bound (measured 2.2x slower than the MMA).  Repack B
+      // once with its largest shared K var innermost so only A is transposed in-kernel.
+      std::vector<int> order = shared_k_order(p, false);
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p.ext[x] > p.ext[y]; });
+      if (!order.empty() && p.ext[order[0]] >= 32) {
+        order.resize(1);
+        CeProblem q = p;
+        int64_t span = 0;
+        CeProblem pk = repack(q, true, order, &span, nullptr);
+        TcPlan t;
+        if (ce_tc_plan(q, &t) && !t.params.ob.mn_major) {
+          Step ps;
+          ps.kind = ce_permute_supported(pk) ? Step::kPermute : Step::kDirect;
+          ps.desc = simt_desc(pk);
+          ps.a = b;
+          ps.c = {BufRef::kWork, alloc(span)};
+          ps.node = node;
+          ps.label = label + ":packB";
+          ps.bytes = 8.0 * operand_elems(pk, 0);
+          b = ps.c;
+          list.push_back(ps);
+          p = q;
+          st.tc = t;
+        }
+      }
+    }
     if (ok) {
       st.kind = Step::kTc;
       st.a = a;

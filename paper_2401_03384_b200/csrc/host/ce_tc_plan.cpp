@@ -173,9 +173,9 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   const int innerA = A.front().v0, innerB = B.front().v0;
   const int ia_cls = ucls(innerA), ib_cls = ucls(innerB);
   // tcgen05 kind::tf32 with the MN-major (transpose) descriptor bits set returns zeros on
-  // sm_100a (measured: tests/tc_probe2.py); only K-major operands are planned.  The
-  // executor repacks operands whose unit-stride axis is not the shared K unit.
-  if (ia_cls != CE_K || ib_cls != CE_K) return fail("operand not K-major (tf32 requires K-major)");
+  // sm_100a (measured: tests/tc_probe2.py).  MN-major operands are therefore loaded by
+  // TMA as [K rows][32 MN] boxes and transposed in shared memory to the K-major layout
+  // by the kernel's transposer warps; the MMA always sees K-major operands.
   int a_mn = -1, b_mn = -1;
   std::vector<std::pair<int, int>> kblock;  // (unit, box)
   auto has_plain = [&](const std::vector<Axis>& ops, int u) {
@@ -431,8 +431,8 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   // transposed store when the fastest N var is unit-stride in the output
   const TcUnit& n0 = U[static_cast<std::size_t>(P.nt[0])];
   P.transpose_store = n0.sc[0] == 1 ? 1 : 0;
-  P.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
-            (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(P.n_mma >> 3) << 17) |
+  // both operands reach the MMA K-major (MN-major ones after the in-smem transpose)
+  P.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(P.n_mma >> 3) << 17) |
             (static_cast<uint32_t>(TC_BM >> 4) << 24);
   plan->valid = 1;
   plan->why = "ok";
