@@ -197,7 +197,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   constexpr int A_BYTES = TC_BM * 128;
   constexpr int B_BYTES = BN * 128;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment by pointer arithmetic on smem_raw (not an integer round trip) so the
+  // compiler keeps the shared address space and emits LDS/STS rather than generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   float* stage_out = reinterpret_cast<float*>(sB + STAGES * B_BYTES);      // [kEpiWarps][32][33]
@@ -424,15 +426,19 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
           __syncwarp();
           const int64_t co = cols[ch * 32 + lane];
           float* cbase = C + base + co;
+          if (atomic) {
 #pragma unroll
-          for (int rr = 0; rr < 32; ++rr) {
-            const int64_t rrow = __shfl_sync(0xffffffffu, ro, rr);
-            const float v = stage[rr * 33 + lane];
-            if (rrow >= 0 && co >= 0) {
-              if (atomic)
-                atomicAdd(cbase + rrow, v);
-              else
-                cbase[rrow] = v;
+            for (int rr = 0; rr < 32; ++rr) {
+              const int64_t rrow = __shfl_sync(0xffffffffu, ro, rr);
+              const float v = stage[rr * 33 + lane];
+              if (rrow >= 0 && co >= 0) atomicAdd(cbase + rrow, v);
+            }
+          } else {
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) {
+              const int64_t rrow = __shfl_sync(0xffffffffu, ro, rr);
+              const float v = stage[rr * 33 + lane];
+              if (rrow >= 0 && co >= 0) cbase[rrow] = v;
             }
           }
           __syncwarp();
@@ -440,13 +446,14 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
           int64_t co[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) co[i] = cols[ch * 32 + i];
+          if (atomic) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            if (co[i] < 0) continue;
-            if (atomic)
-              atomicAdd(crow + co[i], __uint_as_float(r[i]));
-            else
-              crow[co[i]] = __uint_as_float(r[i]);
+            for (int i = 0; i < 32; ++i)
+              if (co[i] >= 0) atomicAdd(crow + co[i], __uint_as_float(r[i]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (co[i] >= 0) crow[co[i]] = __uint_as_float(r[i]);
           }
         }
       }
