@@ -1,17 +1,19 @@
 // tcgen05 kind::tf32 implicit-GEMM kernel for sm_100a (families a + b1).
 //
-// Persistent and warp-specialised: grid = min(#tiles, #SMs), each CTA walks the
-// tile list (m fastest, so CTAs running together share the B tile in L2).
-// 192 threads:
-//   warp 0 lane 0 : TMA producer   (cp.async.bulk.tensor.5d -> STAGES-deep smem ring)
+// Persistent and warp-specialised: grid = min(#work groups, #SMs); a work group is one
+// CTA, or a CTA pair (cluster of 2 along M) that shares the B tile through TMA
+// multicast.  320 threads:
+//   warp 0 lane 0 : TMA producer   (cp.async.bulk.tensor.5d -> STAGES-deep smem ring;
+//                                    B halves multicast to both CTAs of a pair)
 //   warp 1 lane 0 : MMA issuer     (tcgen05.mma.cta_group::1.kind::tf32 into one of two
 //                                    TMEM accumulators, tcgen05.commit -> mbarriers)
 //   warps 2..5    : epilogue       (tcgen05.ld 32x32b -> registers -> [smem transpose] ->
 //                                    global scatter / atomic add for split-K)
-// The two TMEM accumulators let the epilogue of tile t overlap the mainloop of
-// tile t+1.  Operand tiles are 128-byte K-major rows with the 128B swizzle shared
-// by TMA and the UMMA descriptors.  Convolution taps are K-loop iterations whose
-// TMA coordinates are shifted (ce_tc.h); Same/Full padding is TMA's OOB zero fill.
+//   warps 6..9    : transposers    (MN-major TMA boxes -> K-major layout, in place)
+// Two TMEM accumulators let the epilogue of tile t overlap the mainloop of tile t+1.
+// Operand tiles are 128-byte K-major rows with the 128B swizzle shared by TMA and the
+// UMMA descriptors.  Convolution taps are K-loop iterations whose TMA coordinates are
+// shifted (ce_tc.h); Same/Full padding is TMA's OOB zero fill.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -24,7 +26,7 @@
 namespace {
 
 constexpr int kEpiWarps = 4;
-constexpr int kXposeWarps = 4;  // in-smem MN-major -> K-major transposers (warps 6..9)
+constexpr int kXposeWarps = 4;
 constexpr int kThreads = 64 + 32 * kEpiWarps + 32 * kXposeWarps;
 
 // Debug-only phase timestamps (P.dbg & 32): [cta][slot] = %globaltimer (ns).
@@ -73,6 +75,16 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
       : "memory");
 }
 
+// Same box delivered to the same smem offset (and mbarrier) of every CTA in `mask`.
+__device__ __forceinline__ void tma_load_mc(void* dst, const CUtensorMap* map, uint64_t* bar, const int c[5],
+                                            uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, "
+      "{%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
 // SM100 UMMA shared-memory descriptor, K-major SWIZZLE_128B: start>>4 [0,14),
 // LBO>>4 [16,30) (unused for swizzled K-major), SBO>>4 [32,46) = 1024 B between
 // 8-row groups, version 1 [46,48), layout SWIZZLE_128B (2) [61,64).
@@ -97,6 +109,15 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Arrive (when the MMAs retire) on the same mbarrier offset of every CTA in `mask`.
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
@@ -110,6 +131,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 // In-place transpose of one 4 KB SWIZZLE_128B block from the TMA MN-major layout
 // ([32 K rows][32 MN], row k at k*128, 16-B chunk c/4 stored at chunk (c/4)^(k%8))
@@ -133,14 +158,21 @@ struct Tile {
   int split;
 };
 
-// Decode linear tile index t (m fastest, then n, then z, then K split).
-__device__ __forceinline__ void decode_tile(const TcParams& P, uint32_t t, Tile& T) {
+// Work item w of a group of `csize` CTAs (rank within the group): m tiles are dealt
+// in groups of csize (m fastest), then n, z and the K split.  The highest M digit may
+// run past its extent for the last odd group: those rows are simply invalid (TMA OOB
+// zero fill, no store).
+__device__ __forceinline__ void decode_work(const TcParams& P, uint32_t w, uint32_t rank, uint32_t csize, Tile& T) {
   for (int i = 0; i < TC_MAX_UNITS; ++i) T.val[i] = 0;
+  const uint32_t pm = (static_cast<uint32_t>(P.tiles_m) + csize - 1) / csize;
+  uint32_t m = (w % pm) * csize + rank;
+  uint32_t t = w / pm;
   for (int i = 0; i < P.nm; ++i) {
     const TcUnit& u = P.u[P.mt[i]];
     const uint32_t n = static_cast<uint32_t>((u.ext + u.box - 1) / u.box);
-    T.val[P.mt[i]] = static_cast<int32_t>(t % n) * u.box;
-    t /= n;
+    const uint32_t digit = (i + 1 == P.nm) ? m : m % n;
+    T.val[P.mt[i]] = static_cast<int32_t>(digit) * u.box;
+    m /= n;
   }
   for (int i = 0; i < P.nn; ++i) {
     const TcUnit& u = P.u[P.nt[i]];
@@ -154,6 +186,11 @@ __device__ __forceinline__ void decode_tile(const TcParams& P, uint32_t t, Tile&
     t /= static_cast<uint32_t>(u.ext);
   }
   T.split = static_cast<int>(t);
+}
+
+__device__ __forceinline__ int work_split(const TcParams& P, uint32_t w, uint32_t csize) {
+  const uint32_t pm = (static_cast<uint32_t>(P.tiles_m) + csize - 1) / csize;
+  return static_cast<int>(w / (pm * static_cast<uint32_t>(P.tiles_n) * static_cast<uint32_t>(P.grid_z)));
 }
 
 __device__ __forceinline__ void coords(const TcOperand& o, const int32_t* val, int c[5]) {
@@ -211,16 +248,21 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   uint64_t* ready = tempty + 2;       // [STAGES] stage transposed to K-major (MN-major operands only)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + STAGES);
   const bool xpose = P.oa.mn_major || P.ob.mn_major;
+  const bool mc = P.mcast != 0;
+  const uint32_t csize = mc ? 2u : 1u;
+  uint32_t rank = 0;
+  if (mc) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const uint32_t group = blockIdx.x / csize, ngroups = gridDim.x / csize;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) stamp(P, 0);
-  const uint32_t n_tiles = static_cast<uint32_t>(P.tiles_m) * static_cast<uint32_t>(P.tiles_n) *
-                           static_cast<uint32_t>(P.grid_z) * static_cast<uint32_t>(P.k_split);
+  const uint32_t n_work = (static_cast<uint32_t>(P.tiles_m) + csize - 1) / csize * static_cast<uint32_t>(P.tiles_n) *
+                          static_cast<uint32_t>(P.grid_z) * static_cast<uint32_t>(P.k_split);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], csize);  // released by the MMA of every CTA that reads the stage
       mbar_init(&ready[s], 32 * kXposeWarps);
     }
     for (int a = 0; a < 2; ++a) {
@@ -237,12 +279,15 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (mc)
+    cluster_sync();  // partner's barriers initialised before any multicast lands
+  else
+    __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) stamp(P, 1);
   // setup above overlapped the previous kernel's tail (PDL); global memory only from here
   ce_pdl_enter();
-  if (threadIdx.x == 0) stamp(P, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -260,13 +305,14 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       }
       uint32_t gi = 0;  // global stage counter across tiles
       Tile T;
-      for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        decode_tile(P, t, T);
+      for (uint32_t w = group; w < n_work; w += ngroups) {
+        decode_work(P, w, rank, csize, T);
         int k0, k1;
         k_range(P, T.split, k0, k1);
         int baseA[5], baseB[5], dig[6];
         coords(P.oa, T.val, baseA);
         coords(P.ob, T.val, baseB);
+        if (mc) baseB[P.mc_ndim] += static_cast<int>(rank) * P.mc_half;  // this CTA's half of the B rows
         int x = k0;
 #pragma unroll
         for (int u = 0; u < 6; ++u) {
@@ -296,9 +342,13 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
               const int cj[5] = {ca[0] + 32 * j, ca[1], ca[2], ca[3], ca[4]};
               tma_load(sA + s * A_BYTES + j * 4096, &P.ta, &full[s], cj);
             }
-            for (int j = 0; j < P.ob.nsub; ++j) {
-              const int cj[5] = {cb[0] + 32 * j, cb[1], cb[2], cb[3], cb[4]};
-              tma_load(sB + s * B_BYTES + j * 4096, &P.tb, &full[s], cj);
+            if (mc) {
+              tma_load_mc(sB + s * B_BYTES + rank * P.mc_half * 128, &P.tb, &full[s], cb, 0x3);
+            } else {
+              for (int j = 0; j < P.ob.nsub; ++j) {
+                const int cj[5] = {cb[0] + 32 * j, cb[1], cb[2], cb[3], cb[4]};
+                tma_load(sB + s * B_BYTES + j * 4096, &P.tb, &full[s], cj);
+              }
             }
           }
 #pragma unroll
@@ -314,11 +364,10 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     if (lane == 0) {
       // ---------------------------------------------------------- MMA issuer
       uint32_t gi = 0, local = 0;
-      for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++local) {
+      for (uint32_t w = group; w < n_work; w += ngroups, ++local) {
         const int acc = static_cast<int>(local & 1);
-        const int split = static_cast<int>(t / (n_tiles / static_cast<uint32_t>(P.k_split)));
         int k0, k1;
-        k_range(P, split, k0, k1);
+        k_range(P, work_split(P, w, csize), k0, k1);
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d_tmem = tmem + static_cast<uint32_t>(acc * BN);
@@ -333,15 +382,12 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
               mma_tf32(d_tmem, kmajor_desc(a0 + kk * 32), kmajor_desc(b0 + kk * 32), P.idesc,
                        (it > k0 || kk > 0) ? 1u : 0u);
           }
-          if (P.dbg & 16)
-            mbar_arrive(&empty[s]);  // timing experiment (only with MMAs skipped)
+          if (mc)
+            mma_commit_mc(&empty[s], 0x3);  // both CTAs wrote this stage's B halves
           else
             mma_commit(&empty[s]);  // frees the smem slot once these MMAs retire
         }
-        if (P.dbg & 16)
-          mbar_arrive(&tfull[acc]);
-        else
-          mma_commit(&tfull[acc]);  // accumulator of this tile complete
+        mma_commit(&tfull[acc]);  // accumulator of this tile complete
       }
       stamp(P, 3);
     }
@@ -351,10 +397,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     if (xpose) {
       const int xw = warp - (2 + kEpiWarps);
       uint32_t gi = 0;
-      for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int split = static_cast<int>(t / (n_tiles / static_cast<uint32_t>(P.k_split)));
+      for (uint32_t w = group; w < n_work; w += ngroups) {
         int k0, k1;
-        k_range(P, split, k0, k1);
+        k_range(P, work_split(P, w, csize), k0, k1);
         for (int it = k0; it < k1; ++it, ++gi) {
           const int s = static_cast<int>(gi % STAGES);
           mbar_wait(&full[s], (gi / STAGES) & 1);
@@ -377,9 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     const bool atomic = P.k_split > 1;
     uint32_t local = 0;
     Tile T;
-    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++local) {
+    for (uint32_t w = group; w < n_work; w += ngroups, ++local) {
       const int acc = static_cast<int>(local & 1);
-      decode_tile(P, t, T);
+      decode_work(P, w, rank, csize, T);
       int k0, k1;
       k_range(P, T.split, k0, k1);
       // address tables for this tile (overlaps the MMAs)
@@ -465,6 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  if (mc) cluster_sync();  // no CTA exits while its partner may still signal its barriers
   if (threadIdx.x == 0) stamp(P, 6);
 }
 
@@ -520,17 +566,23 @@ int sm_count() {
 template <int BN, int STAGES>
 cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
   constexpr int smem =
-      STAGES * (TC_BM * 128 + BN * 128) + kEpiWarps * 32 * 33 * 4 + 2 * BN * 8 + 8 * (2 * STAGES + 4) + 16 + 1024;
+      STAGES * (TC_BM * 128 + BN * 128) + kEpiWarps * 32 * 33 * 4 + 2 * BN * 8 + 8 * (3 * STAGES + 4) + 16 + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
+    if (cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+        cudaSuccess)
+      cudaGetLastError();
     configured = true;
   }
-  const int64_t tiles = static_cast<int64_t>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_split;
-  const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
-  return ce_launch(ce_tc_kernel<BN, STAGES>, dim3(grid), dim3(kThreads), smem, s, P, C);
+  const int csize = P.mcast ? 2 : 1;
+  const int64_t groups = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
+  const int64_t max_groups = sm_count() / csize;
+  const int grid = static_cast<int>((groups < max_groups ? groups : max_groups) * csize);
+  return ce_launch_cluster(ce_tc_kernel<BN, STAGES>, dim3(grid), dim3(kThreads), smem, s, static_cast<unsigned>(csize),
+                           P, C);
 }
 
 int debug_flags() {

@@ -70,6 +70,11 @@ struct TcParams {
   // coordinate[d] = base[d] + sum_i digit_i * kstep_{a,b}[i][d], digit_i < kcount[i]
   int32_t kcount[6];
   int32_t kstep_a[6][5], kstep_b[6][5];
+  // 2-CTA cluster along M: each CTA TMA-loads mc_half rows of the B tile and multicasts
+  // them to both CTAs (B is read from L2 once per CTA pair instead of once per CTA)
+  int32_t mcast;           // 1: launched with cluster dims (2,1,1)
+  int32_t mc_half;         // B rows loaded per CTA (multiple of 8)
+  int32_t mc_ndim;         // TMA dim of B that carries the N tile
   int32_t mn_lbo, mn_sbo;  // MN-major descriptor strides (bytes)
   int32_t dbg;             // debug: bit0 skip MMAs, bit1 skip TMA loads (timing experiments only)
 };

@@ -498,9 +498,9 @@ std::string Executor::describe() const {
       if (st.kind == Step::kTc) {
         const TcParams& P = st.tc.params;
         std::snprintf(line + n, sizeof line - n,
-                      " bn=%d rows=%d cols=%d mma_n=%d tiles=%dx%dx%d split=%d kit=%d amn=%d bmn=%d tr=%d\n", st.tc.bn,
+                      " bn=%d rows=%d cols=%d mma_n=%d tiles=%dx%dx%d split=%d kit=%d amn=%d bmn=%d tr=%d mc=%d\n", st.tc.bn,
                       P.m_rows, P.n_cols, P.n_mma, P.tiles_m, P.tiles_n, P.grid_z, P.k_split, P.k_iters, P.oa.mn_major,
-                      P.ob.mn_major, P.transpose_store);
+                      P.ob.mn_major, P.transpose_store, P.mcast);
       } else {
         std::snprintf(line + n, sizeof line - n, " Z=%lld M=%lld N=%lld K=%lld (tc: %s)\n", (long long)st.desc.Z,
                       (long long)st.desc.M, (long long)st.desc.N, (long long)st.desc.K,

@@ -10,6 +10,7 @@
 // not multiple of 16 B, no unit-stride axis) returns false and the executor uses
 // the SIMT kernels (ce_simt.cu).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -434,6 +435,23 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   // both operands reach the MMA K-major (MN-major ones after the in-smem transpose)
   P.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(P.n_mma >> 3) << 17) |
             (static_cast<uint32_t>(TC_BM >> 4) << 24);
+  // 2-CTA cluster with B multicast: K-major B whose N tile is one unit (TMA dim 1)
+  static const bool mcast_enabled = [] {
+    const char* e = std::getenv("CE_TC_MCAST");
+    return !(e && *e == '0');
+  }();
+  P.mcast = 0;
+  if (mcast_enabled && b_mn == 0 && P.nn == 1 && P.tiles_m >= 2 && P.n_cols >= 64 &&
+      P.ob.dim[1].u0 == P.nt[0]) {
+    const int half = ((P.n_cols + 1) / 2 + 7) / 8 * 8;
+    if (2 * half <= plan->bn) {
+      P.mcast = 1;
+      P.mc_half = half;
+      P.mc_ndim = 1;
+      plan->box_b[1] = static_cast<uint32_t>(half);
+      P.ob.stage_bytes = 2 * half * 128;
+    }
+  }
   plan->valid = 1;
   plan->why = "ok";
   return true;
