@@ -241,6 +241,66 @@ def test_graph_replay_and_pointer_change(ctx):
         assert nerr(y.cpu().numpy(), ref) <= TOL["auto"][0]
 
 
+def test_layer_zoo_forward_backward(any_ctx):
+    """All 13 layer kinds (SPEC.md:569 toy dims) forward + every gradient vs the FP64 oracle."""
+    import paper_2401_03384_b200 as ce
+    c_, mode = any_ctx
+    for case in load("layers.json")["layers"]:
+        if case["cr"] > 0 or "cfg" in case["name"] or "dense" in case["name"]:
+            continue
+        rng = np.random.default_rng(17)
+        ins = [f32(rng.uniform(-1, 1, d)) for d in case["dims"]]
+        plan = ce.optimal(case["expr"], case["dims"], "same", "training")
+        dout = f32(rng.uniform(-1, 1, plan.out_dims))
+        plan, nodes, out, grads, _ = _run_plan(c_, case["expr"], case["dims"], "same", ins, dout, "training")
+        ref, _ = npo.execute(case["expr"], case["dims"], nodes, ins)
+        ref_g = npo.backward(case["expr"], case["dims"], nodes, ins, dout)
+        assert nerr(out, ref) <= TOL[mode][0], case["name"]
+        for i, (g, r) in enumerate(zip(grads, ref_g)):
+            assert nerr(g.cpu().numpy(), r) <= TOL[mode][1], (case["name"], i)
+
+
+@pytest.mark.parametrize("stage", ["conv1", "conv3_x", "conv5_x"])
+def test_cp_resnet34_stage_shapes(ctx, stage):
+    """cfg4 layer shapes (CP, cr=0.1) at batch 2: forward per sample + gradient identities."""
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import Executor
+    spec = dict(ce.resnet34_cp_blocks(2, 0.1))[stage]
+    le = ce.expression(spec)
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    ex = Executor(ctx, plan, backward=True)
+    xs = [ctx.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
+    dout = ctx.fill_random(plan.out_dims, 2000)
+    out = ex.execute(xs)
+    grads = ex.backward(xs, dout)
+    torch.cuda.synchronize()
+    nodes = [(n["left"], n["right"], n["result"]) for n in json.loads(plan.to_json())["nodes"]]
+    ins = [x.double().cpu().numpy() for x in xs]
+    ref, _ = npo.execute(le.expr, le.dims, nodes, ins)
+    assert nerr(out.cpu().numpy(), ref) <= TOL["auto"][0]
+    y_dot = float((out.double() * dout.double()).sum())
+    for x, g in zip(xs, grads):
+        gx = float((g.double() * x.double()).sum())
+        assert abs(gx - y_dot) <= 1e-1 * max(abs(y_dot), 1e-6), (stage, gx, y_dot)
+
+
+def test_rtr_cfg3_reduced(any_ctx):
+    """cfg3 tensor-ring reshaped layer (64->64 as 4x4x4, M=3) at 14x14, batch 2: fwd + all grads."""
+    import paper_2401_03384_b200 as ce
+    c_, mode = any_ctx
+    le = ce.expression(ce.LayerSpec("rtr", [4, 4, 4], [4, 4, 4], 3, 3, 14, 14, 2, [1, 1, 1, 1]), 0.1)
+    rng = np.random.default_rng(23)
+    ins = [f32(rng.uniform(-1, 1, d)) for d in le.dims]
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    dout = f32(rng.uniform(-1, 1, plan.out_dims))
+    plan, nodes, out, grads, _ = _run_plan(c_, le.expr, le.dims, "same", ins, dout, "training")
+    ref, _ = npo.execute(le.expr, le.dims, nodes, ins)
+    ref_g = npo.backward(le.expr, le.dims, nodes, ins, dout)
+    assert nerr(out, ref) <= TOL[mode][0]
+    for i, (g, r) in enumerate(zip(grads, ref_g)):
+        assert nerr(g.cpu().numpy(), r) <= TOL[mode][1], i
+
+
 def test_native_library_loaded(ctx):
     maps = open("/proc/self/maps").read()
     assert "libce.so" in maps
