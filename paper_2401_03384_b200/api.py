@@ -72,6 +72,7 @@ class Plan:
 
     def __init__(self, handle, expr, dims, mode, cost_mode):
         self._h = handle
+        self._destroy = lib().ce_plan_destroy
         self.expr, self.dims, self.mode, self.cost_mode = expr, [list(map(int, d)) for d in dims], mode, cost_mode
         info = _lib.PlanInfo()
         check(lib().ce_plan_get_info(self._h, ctypes.byref(info)))
@@ -137,8 +138,9 @@ class Plan:
         return out
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().ce_plan_destroy(self._h)
+        # the destroy entry point is bound at creation: module globals may be gone at exit
+        if getattr(self, "_h", None) and getattr(self, "_destroy", None):
+            self._destroy(self._h)
             self._h = None
 
 

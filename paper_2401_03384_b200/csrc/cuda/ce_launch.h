@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <mutex>
+#include <unordered_set>
 #include <utility>
 
 __device__ __forceinline__ void ce_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -29,9 +31,26 @@ inline bool ce_pdl_enabled() {
   return v == 1;
 }
 
+// Every kernel asks for the maximum shared-memory carveout: the tcgen05 kernels need
+// ~216 KB, and an SM whose carveout differs from the next kernel's must drain and
+// reconfigure before that kernel's CTAs can land (which also defeats PDL overlap).
+// CE_CARVEOUT=0 leaves the driver default.
+inline void ce_prefer_max_smem(const void* fn) {
+  static std::mutex mu;
+  static std::unordered_set<const void*> seen;
+  static const bool on = [] {
+    const char* e = std::getenv("CE_CARVEOUT");
+    return !(e && *e == '0');
+  }();
+  if (!on) return;
+  std::lock_guard<std::mutex> g(mu);
+  if (seen.insert(fn).second) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+
 template <typename... Exp, typename... Act>
 cudaError_t ce_launch_cluster(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               unsigned cluster_x, Act&&... args) {
+  ce_prefer_max_smem(reinterpret_cast<const void*>(kernel));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;

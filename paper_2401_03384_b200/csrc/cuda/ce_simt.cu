@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "ce_device.h"
 #include "ce_kernels.h"
@@ -393,14 +394,107 @@ __global__ void __launch_bounds__(256) ce_transpose_kernel(const CePermDesc d, c
   }
 }
 
-// Input and output share the unit-stride axis x: a strided copy of rows (x, y) per
-// batch slice.  (x, y) is flattened so short rows still give coalesced warps.
-__global__ void __launch_bounds__(256, 4) ce_rowcopy_kernel(const CePermDesc d, const float* __restrict__ A,
-                                                            float* __restrict__ C) {
+// Offset of row i along a tile axis that may be composite (i = i1 + e1*i2).
+struct CeRowMap {
+  uint32_t e1;
+  int64_t s1, s2;
+  bool comp;
+  __device__ __forceinline__ int64_t operator()(uint32_t i) const {
+    return comp ? static_cast<int64_t>(i % e1) * s1 + static_cast<int64_t>(i / e1) * s2 : static_cast<int64_t>(i) * s1;
+  }
+};
+
+// 64x64 tiles with 128-bit global accesses (VI: input rows along x, VO: output rows
+// along y are 16-B aligned and a multiple of 4 long).  Per element: a quarter of a
+// vector load and store plus one STS and one LDS; the 65-float row pitch keeps both
+// smem phases at 2-way bank conflicts.  Composite tile axes (short unit-stride axes
+// continued by a second axis, see CePermDesc) cost one division per row, not per element.
+template <bool VI, bool VO>
+__global__ void __launch_bounds__(256, 4) ce_transpose64_kernel(const CePermDesc d, const float* __restrict__ A,
+                                                             float* __restrict__ C) {
   ce_pdl_enter();
-  const uint32_t ex = static_cast<uint32_t>(d.ext[d.vin]);
-  const uint32_t n = ex * static_cast<uint32_t>(d.ext[d.vout]);
+  __shared__ float tile[64][65];
+  const uint32_t ein = static_cast<uint32_t>(d.ext[d.vin] * (d.vin2 >= 0 ? d.ext[d.vin2] : 1));
+  const uint32_t eout = static_cast<uint32_t>(d.ext[d.vout] * (d.vout2 >= 0 ? d.ext[d.vout2] : 1));
+  const CeRowMap in_row{static_cast<uint32_t>(d.ext[d.vout]), d.sa[d.vout], d.vout2 >= 0 ? d.sa[d.vout2] : 0,
+                        d.vout2 >= 0};
+  const CeRowMap out_row{static_cast<uint32_t>(d.ext[d.vin]), d.sc[d.vin], d.vin2 >= 0 ? d.sc[d.vin2] : 0,
+                         d.vin2 >= 0};
+  const uint32_t x0 = blockIdx.x * 64, y0 = blockIdx.y * 64;
+  const int t = threadIdx.x;
+  for (int64_t bt = blockIdx.z; bt < d.nbatch; bt += gridDim.z) {
+    int64_t r = bt, bin = 0, bout = 0;
+    for (int i = 0; i < d.nrest; ++i) {
+      const int v = d.rest[i];
+      const int64_t x = r % d.ext[v];
+      r /= d.ext[v];
+      bin += x * d.sa[v];
+      bout += x * d.sc[v];
+    }
+    if (VI) {
+      float4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int idx = t + 256 * j, row = idx >> 4, c4 = (idx & 15) * 4;
+        const uint32_t y = y0 + row, x = x0 + c4;
+        v[j] = (y < eout && x < ein) ? __ldg(reinterpret_cast<const float4*>(A + bin + in_row(y) + x))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int idx = t + 256 * j, row = idx >> 4, c4 = (idx & 15) * 4;
+        tile[row][c4] = v[j].x;
+        tile[row][c4 + 1] = v[j].y;
+        tile[row][c4 + 2] = v[j].z;
+        tile[row][c4 + 3] = v[j].w;
+      }
+    } else {
+      const int c = t & 63, row0 = t >> 6;
+      const bool xok = x0 + c < ein;
+      const float* src = A + bin + x0 + c;
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t y = y0 + row0 + 4 * j;
+        v[j] = (xok && y < eout) ? __ldg(src + in_row(y)) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) tile[row0 + 4 * j][c] = v[j];
+    }
+    __syncthreads();
+    if (VO) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int idx = t + 256 * j, xr = idx >> 4, c4 = (idx & 15) * 4;
+        const uint32_t x = x0 + xr, y = y0 + c4;
+        if (x < ein && y < eout)
+          *reinterpret_cast<float4*>(C + bout + out_row(x) + y) =
+              make_float4(tile[c4][xr], tile[c4 + 1][xr], tile[c4 + 2][xr], tile[c4 + 3][xr]);
+      }
+    } else {
+      const int c = t & 63, xr0 = t >> 6;
+      const bool yok = y0 + c < eout;
+      float* dst = C + bout + y0 + c;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t x = x0 + xr0 + 4 * j;
+        if (yok && x < ein) dst[out_row(x)] = tile[c][xr0 + 4 * j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Input and output share the unit-stride axis x: a strided copy of rows (x, y) per
+// batch slice.  A row is served by L = 2^lshift lanes (L >= min(ext x, 32)), so a warp
+// covers 32/L short rows without any per-element division; 4 rows per thread in flight.
+__global__ void __launch_bounds__(256) ce_rowcopy_kernel(const CePermDesc d, const float* __restrict__ A,
+                                                         float* __restrict__ C, int lshift) {
+  ce_pdl_enter();
+  const uint32_t ex = static_cast<uint32_t>(d.ext[d.vin]), ey = static_cast<uint32_t>(d.ext[d.vout]);
   const int64_t sa_y = d.sa[d.vout], sc_y = d.sc[d.vout];
+  const uint32_t L = 1u << lshift, lx = threadIdx.x & (L - 1), rows = 256u >> lshift;
+  const uint32_t ly = threadIdx.x >> lshift;
   for (int64_t bt = blockIdx.y; bt < d.nbatch; bt += gridDim.y) {
     int64_t r = bt, bin = 0, bout = 0;
     for (int i = 0; i < d.nrest; ++i) {
@@ -410,17 +504,19 @@ __global__ void __launch_bounds__(256, 4) ce_rowcopy_kernel(const CePermDesc d, 
       bin += x * d.sa[v];
       bout += x * d.sc[v];
     }
-    for (uint32_t f = blockIdx.x * 256 * 8 + threadIdx.x; f < n; f += gridDim.x * 256 * 8) {
-      float v[8];
+    for (uint32_t yb = blockIdx.x * rows * 4; yb < ey; yb += gridDim.x * rows * 4) {
+      for (uint32_t x = lx; x < ex; x += L) {
+        float v[4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t g = f + j * 256;
-        v[j] = g < n ? __ldg(A + bin + (g % ex) + static_cast<int64_t>(g / ex) * sa_y) : 0.f;
-      }
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t y = yb + ly + j * rows;
+          v[j] = y < ey ? __ldg(A + bin + static_cast<int64_t>(y) * sa_y + x) : 0.f;
+        }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t g = f + j * 256;
-        if (g < n) C[bout + (g % ex) + static_cast<int64_t>(g / ex) * sc_y] = v[j];
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t y = yb + ly + j * rows;
+          if (y < ey) C[bout + static_cast<int64_t>(y) * sc_y + x] = v[j];
+        }
       }
     }
   }
@@ -555,6 +651,17 @@ bool perm_desc(const CeProblem& p, CePermDesc* out) {
 }
 }  // namespace
 
+int ce_permute_describe(const CeProblem& p, char* buf, int n) {
+  CePermDesc d;
+  if (!perm_desc(p, &d)) return std::snprintf(buf, n, "unsupported");
+  int k = std::snprintf(buf, n, "%s vin=%d vout=%d vin2=%d vout2=%d |", d.same ? "rowcopy" : "transpose", d.vin, d.vout,
+                        d.vin2, d.vout2);
+  for (int v = 0; v < CE_MAX_VARS && k < n; ++v)
+    if (d.ext[v] > 0) k += std::snprintf(buf + k, n - k, " %lld:%lld/%lld", (long long)d.ext[v], (long long)d.sa[v],
+                                         (long long)d.sc[v]);
+  return k;
+}
+
 bool ce_permute_supported(const CeProblem& p) {
   CePermDesc d;
   return perm_desc(p, &d);
@@ -564,16 +671,38 @@ cudaError_t ce_launch_permute(const CeProblem& p, const float* A, float* C, cuda
   CePermDesc d;
   if (!perm_desc(p, &d)) return cudaErrorInvalidValue;
   if (d.same) {
-    const int64_t n = d.ext[d.vin] * d.ext[d.vout];
-    if (n >= (1ll << 31)) return cudaErrorInvalidConfiguration;
-    const int64_t per_slice = (n + 2047) / 2048;
+    int lshift = 0;
+    while (lshift < 5 && (1ll << lshift) < d.ext[d.vin]) ++lshift;
+    const int64_t rows_per_cta = (256 >> lshift) * 4;
+    const int64_t per_slice = (d.ext[d.vout] + rows_per_cta - 1) / rows_per_cta;
     const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(per_slice, (148 * 16 + d.nbatch - 1) / d.nbatch));
     const int64_t gy = std::min<int64_t>(d.nbatch, 65535);
     return ce_launch(ce_rowcopy_kernel, dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), dim3(256), 0, s, d,
-                     A, C);
+                     A, C, lshift);
   }
   const int64_t ein = d.ext[d.vin] * (d.vin2 >= 0 ? d.ext[d.vin2] : 1);
   const int64_t eout = d.ext[d.vout] * (d.vout2 >= 0 ? d.ext[d.vout2] : 1);
+  if (ein >= 16 && eout >= 16) {
+    // vector paths need every row start 16-B aligned on that side
+    bool vi = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && ein % 4 == 0 && d.sa[d.vout] % 4 == 0 &&
+              (d.vout2 < 0 || d.sa[d.vout2] % 4 == 0);
+    bool vo = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && eout % 4 == 0 && d.sc[d.vin] % 4 == 0 &&
+              (d.vin2 < 0 || d.sc[d.vin2] % 4 == 0);
+    for (int i = 0; i < d.nrest; ++i) {
+      vi = vi && d.sa[d.rest[i]] % 4 == 0;
+      vo = vo && d.sc[d.rest[i]] % 4 == 0;
+    }
+    const int64_t gx = (ein + 63) / 64, gy = (eout + 63) / 64;
+    if (gx <= 0x7fffffff && gy <= 65535) {
+      // enough CTAs to fill the machine, batch slices looped beyond that
+      const int64_t gz = std::max<int64_t>(1, std::min<int64_t>({d.nbatch, 65535, (148 * 24 + gx * gy - 1) / (gx * gy)}));
+      const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(gz));
+      if (vi && vo) return ce_launch(ce_transpose64_kernel<true, true>, grid, dim3(256), 0, s, d, A, C);
+      if (vi) return ce_launch(ce_transpose64_kernel<true, false>, grid, dim3(256), 0, s, d, A, C);
+      if (vo) return ce_launch(ce_transpose64_kernel<false, true>, grid, dim3(256), 0, s, d, A, C);
+      return ce_launch(ce_transpose64_kernel<false, false>, grid, dim3(256), 0, s, d, A, C);
+    }
+  }
   const int64_t gx = (ein + 31) / 32, gy = (eout + 31) / 32;
   if (gx > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
   const int64_t gz = std::min<int64_t>(d.nbatch, 65535);

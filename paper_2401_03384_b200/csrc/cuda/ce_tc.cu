@@ -31,6 +31,16 @@ constexpr int kThreads = 64 + 32 * kEpiWarps + 32 * kXposeWarps;
 
 // Debug-only phase timestamps (P.dbg & 32): [cta][slot] = %globaltimer (ns).
 __device__ unsigned long long g_tc_ts[160 * 8];
+// Debug-only per-iteration timestamps of CTA 0 (P.dbg & 512): [role][iteration], role 0
+// producer (after its empty wait), 1 MMA issuer (after its full wait).
+__device__ unsigned long long g_tc_it[3 * 256];
+__device__ __forceinline__ void stamp_it(const TcParams& P, int role, uint32_t gi) {
+  if ((P.dbg & 512) && blockIdx.x == 0 && gi < 256) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tc_it[role * 256 + gi] = t;
+  }
+}
 __device__ __forceinline__ void stamp(const TcParams& P, int slot) {
   if (P.dbg & 32) {
     unsigned long long t;
@@ -55,6 +65,31 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Shared::cluster address of the same smem location in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+
+// Arrive on an mbarrier of another CTA of the cluster (release at cluster scope).
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// Wait that also acquires what other CTAs of the cluster released into this barrier.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -72,6 +107,16 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
       "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
       "%6}], [%7];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// CTA-pair load: the box lands in this CTA's smem, completion is signalled on an
+// mbarrier that may live in the peer CTA (`bar_cluster` is a shared::cluster address).
+__device__ __forceinline__ void tma_load_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, const int c[5]) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar_cluster)
       : "memory");
 }
 
@@ -102,6 +147,27 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// M=256 MMA over a CTA pair (issued by the even CTA): A rows 0-127 from this CTA's smem,
+// 128-255 from the peer's; B columns split in halves the same way; D rows per CTA's TMEM.
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -229,10 +295,13 @@ __device__ __forceinline__ void k_range(const TcParams& P, int split, int& k0, i
   k1 = min(P.k_iters, k0 + per);
 }
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constant__ TcParams P, float* __restrict__ C) {
+// PAIR: CTA pair (cluster of 2) running M=256 tcgen05.mma.cta_group::2 issued by the even
+// CTA; each CTA stages its own 128 A rows and half of the B columns, so per-SM smem traffic
+// per MMA drops by a quarter and the ring gets deeper.
+template <int BN, int STAGES, bool PAIR>
+__global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constant__ TcParams Pg, float* __restrict__ C) {
   constexpr int A_BYTES = TC_BM * 128;
-  constexpr int B_BYTES = BN * 128;
+  constexpr int B_BYTES = PAIR ? BN * 64 : BN * 128;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment by pointer arithmetic on smem_raw (not an integer round trip) so the
   // compiler keeps the shared address space and emits LDS/STS rather than generic LD/ST
@@ -247,39 +316,57 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   uint64_t* tempty = tfull + 2;       // [2]
   uint64_t* ready = tempty + 2;       // [STAGES] stage transposed to K-major (MN-major operands only)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + STAGES);
-  const bool xpose = P.oa.mn_major || P.ob.mn_major;
-  const bool mc = P.mcast != 0;
-  const uint32_t csize = mc ? 2u : 1u;
+  // Kernel parameters are read through dependent, dynamically indexed loads (unit lists ->
+  // units -> extents); from the constant bank each of those is a cold miss on the start-up
+  // path of every role.  One coalesced copy into shared memory up front instead.
+  TcParams* sP = reinterpret_cast<TcParams*>(smem_raw + ((smem_u32(tmem_slot + 4) - smem_u32(smem_raw) + 63u) & ~63u));
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(&Pg);
+    uint4* dst = reinterpret_cast<uint4*>(sP);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(TcParams) / 16); i += kThreads) dst[i] = src[i];
+  }
+  const TcParams& P = *sP;
+  if (Pg.dbg & 128) return;  // timing experiment: launch cost only
+  const bool xpose = Pg.oa.mn_major || Pg.ob.mn_major;
+  const bool mc = !PAIR && Pg.mcast != 0;
+  const uint32_t csize = (mc || PAIR) ? 2u : 1u;
   uint32_t rank = 0;
-  if (mc) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  if (csize == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const bool leader = rank == 0;
   const uint32_t group = blockIdx.x / csize, ngroups = gridDim.x / csize;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (threadIdx.x == 0) stamp(P, 0);
-  const uint32_t n_work = (static_cast<uint32_t>(P.tiles_m) + csize - 1) / csize * static_cast<uint32_t>(P.tiles_n) *
-                          static_cast<uint32_t>(P.grid_z) * static_cast<uint32_t>(P.k_split);
+  if (threadIdx.x == 0) stamp(Pg, 0);
+  const uint32_t n_work = (static_cast<uint32_t>(Pg.tiles_m) + csize - 1) / csize * static_cast<uint32_t>(Pg.tiles_n) *
+                          static_cast<uint32_t>(Pg.grid_z) * static_cast<uint32_t>(Pg.k_split);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], csize);  // released by the MMA of every CTA that reads the stage
-      mbar_init(&ready[s], 32 * kXposeWarps);
+      mbar_init(&empty[s], mc ? csize : 1u);  // released by the MMA of every CTA that reads the stage
+      mbar_init(&ready[s], (PAIR ? 2 : 1) * 32 * kXposeWarps);  // PAIR: both CTAs' transposers
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 32 * kEpiWarps);
+      mbar_init(&tempty[a], (PAIR ? 2 : 1) * 32 * kEpiWarps);  // PAIR: both CTAs' epilogues
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&P.ta) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&P.tb) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&Pg.ta) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&Pg.tb) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  if (mc)
+  if (csize == 2)
     cluster_sync();  // partner's barriers initialised before any multicast lands
   else
     __syncthreads();
@@ -289,10 +376,13 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   // setup above overlapped the previous kernel's tail (PDL); global memory only from here
   ce_pdl_enter();
 
-  if (warp == 0) {
+  if (P.dbg & 64) {
+    // timing experiment: set-up and tear-down only
+  } else if (warp == 0) {
     if (lane == 0) {
       // ---------------------------------------------------------- TMA producer
       const uint32_t bytes = static_cast<uint32_t>(P.oa.stage_bytes + P.ob.stage_bytes);
+      const uint32_t full_lead = PAIR ? mapa(&full[0], 0) : 0u;
       int step_a[6][5], step_b[6][5], kcount[6];
 #pragma unroll
       for (int u = 0; u < 6; ++u) {
@@ -312,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
         int baseA[5], baseB[5], dig[6];
         coords(P.oa, T.val, baseA);
         coords(P.ob, T.val, baseB);
-        if (mc) baseB[P.mc_ndim] += static_cast<int>(rank) * P.mc_half;  // this CTA's half of the B rows
+        if (csize == 2) baseB[P.mc_ndim] += static_cast<int>(rank) * P.mc_half;  // this CTA's half of the B rows
         int x = k0;
 #pragma unroll
         for (int u = 0; u < 6; ++u) {
@@ -322,6 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
         for (int it = k0; it < k1; ++it, ++gi) {
           const int s = static_cast<int>(gi % STAGES);
           mbar_wait(&empty[s], ((gi / STAGES) & 1) ^ 1);
+          stamp_it(P, 0, gi);
           int ca[5], cb[5];
 #pragma unroll
           for (int d = 0; d < 5; ++d) {
@@ -334,20 +425,25 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
             }
           }
           if (P.dbg & 2) {
-            mbar_arrive(&full[s]);
+            if (!PAIR || xpose || leader) mbar_arrive(&full[s]);
+          } else if (PAIR && !xpose) {
+            // both halves complete on the even CTA's barrier, which expects the pair's bytes
+            if (leader) mbar_expect_tx(&full[s], 2 * bytes);
+            tma_load_pair(sA + s * A_BYTES, &Pg.ta, full_lead + 8u * s, ca);
+            tma_load_pair(sB + s * B_BYTES, &Pg.tb, full_lead + 8u * s, cb);
           } else {
             mbar_expect_tx(&full[s], bytes);
             // K-major: one box; MN-major: nsub boxes of [32 K rows][32 MN] at 4 KB steps
             for (int j = 0; j < P.oa.nsub; ++j) {
               const int cj[5] = {ca[0] + 32 * j, ca[1], ca[2], ca[3], ca[4]};
-              tma_load(sA + s * A_BYTES + j * 4096, &P.ta, &full[s], cj);
+              tma_load(sA + s * A_BYTES + j * 4096, &Pg.ta, &full[s], cj);
             }
             if (mc) {
-              tma_load_mc(sB + s * B_BYTES + rank * P.mc_half * 128, &P.tb, &full[s], cb, 0x3);
+              tma_load_mc(sB + s * B_BYTES + rank * P.mc_half * 128, &Pg.tb, &full[s], cb, 0x3);
             } else {
               for (int j = 0; j < P.ob.nsub; ++j) {
                 const int cj[5] = {cb[0] + 32 * j, cb[1], cb[2], cb[3], cb[4]};
-                tma_load(sB + s * B_BYTES + j * 4096, &P.tb, &full[s], cj);
+                tma_load(sB + s * B_BYTES + j * 4096, &Pg.tb, &full[s], cj);
               }
             }
           }
@@ -361,33 +457,57 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       stamp(P, 2);
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       // ---------------------------------------------------------- MMA issuer
       uint32_t gi = 0, local = 0;
       for (uint32_t w = group; w < n_work; w += ngroups, ++local) {
         const int acc = static_cast<int>(local & 1);
         int k0, k1;
         k_range(P, work_split(P, w, csize), k0, k1);
-        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+        if (PAIR)
+          mbar_wait_cluster(&tempty[acc], ((local >> 1) & 1) ^ 1);  // both epilogues drained it
+        else
+          mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d_tmem = tmem + static_cast<uint32_t>(acc * BN);
         for (int it = k0; it < k1; ++it, ++gi) {
           const int s = static_cast<int>(gi % STAGES);
-          mbar_wait(xpose ? &ready[s] : &full[s], (gi / STAGES) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (PAIR && xpose)
+            mbar_wait_cluster(&ready[s], (gi / STAGES) & 1);
+          else
+            mbar_wait(xpose ? &ready[s] : &full[s], (gi / STAGES) & 1);
+          if (gi == 0) stamp(P, 7);
+          stamp_it(P, 1, gi);
+          if (!(P.dbg & 256)) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
           if (!(P.dbg & 1)) {
 #pragma unroll
-            for (int kk = 0; kk < TC_BK / 8; ++kk)  // K=8 per tf32 MMA: +32 B inside the 128-B row
-              mma_tf32(d_tmem, kmajor_desc(a0 + kk * 32), kmajor_desc(b0 + kk * 32), P.idesc,
-                       (it > k0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < TC_BK / 8; ++kk) {  // K=8 per tf32 MMA: +32 B inside the 128-B row
+              if (PAIR)
+                mma_tf32_pair(d_tmem, kmajor_desc(a0 + kk * 32), kmajor_desc(b0 + kk * 32), P.idesc,
+                              (it > k0 || kk > 0) ? 1u : 0u);
+              else
+                mma_tf32(d_tmem, kmajor_desc(a0 + kk * 32), kmajor_desc(b0 + kk * 32), P.idesc,
+                         (it > k0 || kk > 0) ? 1u : 0u);
+            }
           }
-          if (mc)
+          if (P.dbg & 16)
+            mbar_arrive(&empty[s]);  // timing experiment (with bit 0, no multicast): plain arrive
+          else if (PAIR)
+            mma_commit_pair(&empty[s]);  // the slot of this stage in both CTAs
+          else if (mc)
             mma_commit_mc(&empty[s], 0x3);  // both CTAs wrote this stage's B halves
           else
             mma_commit(&empty[s]);  // frees the smem slot once these MMAs retire
+          if (P.dbg & 1024) {  // timing experiment: wait for this stage's MMAs + commit
+            mbar_wait(&empty[s], (gi / STAGES) & 1);
+            stamp_it(P, 2, gi);
+          }
         }
-        mma_commit(&tfull[acc]);  // accumulator of this tile complete
+        if (PAIR)
+          mma_commit_pair(&tfull[acc]);  // both CTAs' accumulators of this tile complete
+        else
+          mma_commit(&tfull[acc]);  // accumulator of this tile complete
       }
       stamp(P, 3);
     }
@@ -409,7 +529,10 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
             for (int j = xw; j < P.ob.nsub; j += kXposeWarps) xpose_block(sB + s * B_BYTES + j * 4096, lane);
           // generic-proxy smem writes must be visible to the tensor core (async proxy)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&ready[s]);
+          if (PAIR && !leader)
+            mbar_arrive_cluster(mapa(&ready[s], 0));  // the even CTA issues the pair's MMAs
+          else
+            mbar_arrive(&ready[s]);
         }
       }
     }
@@ -447,7 +570,10 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       if (threadIdx.x == 64 && local == 0) stamp(P, 4);
       if (P.dbg & 8) {  // timing experiment: skip the epilogue body
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        mbar_arrive(&tempty[acc]);
+        if (PAIR && !leader)
+          mbar_arrive_cluster(mapa(&tempty[acc], 0));
+        else
+          mbar_arrive(&tempty[acc]);
         continue;
       }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -503,14 +629,22 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&tempty[acc]);  // accumulator may be overwritten by tile t+2
+      if (PAIR && !leader)
+        mbar_arrive_cluster(mapa(&tempty[acc], 0));  // the even CTA's MMA owns the pair's TMEM writes
+      else
+        mbar_arrive(&tempty[acc]);  // accumulator may be overwritten by tile t+2
     }
     if (threadIdx.x == 64) stamp(P, 5);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
-  if (mc) cluster_sync();  // no CTA exits while its partner may still signal its barriers
+  if (PAIR) {
+    cluster_sync();  // the peer's MMAs and epilogue are done with this CTA's TMEM and barriers
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  } else {
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    if (mc) cluster_sync();  // no CTA exits while its partner may still signal its barriers
+  }
   if (threadIdx.x == 0) stamp(P, 6);
 }
 
@@ -563,16 +697,18 @@ int sm_count() {
   return n;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool PAIR>
 cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
   constexpr int smem =
-      STAGES * (TC_BM * 128 + BN * 128) + kEpiWarps * 32 * 33 * 4 + 2 * BN * 8 + 8 * (3 * STAGES + 4) + 16 + 1024;
+      STAGES * (TC_BM * 128 + (PAIR ? BN * 64 : BN * 128)) + kEpiWarps * 32 * 33 * 4 + 2 * BN * 8 + 8 * (3 * STAGES + 4) + 16 + 64 +
+      static_cast<int>(sizeof(TcParams)) + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    if (cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+    if (cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES, PAIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
         cudaSuccess)
       cudaGetLastError();
     configured = true;
@@ -581,7 +717,8 @@ cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
   const int64_t groups = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
   const int64_t max_groups = sm_count() / csize;
   const int grid = static_cast<int>((groups < max_groups ? groups : max_groups) * csize);
-  return ce_launch_cluster(ce_tc_kernel<BN, STAGES>, dim3(grid), dim3(kThreads), smem, s, static_cast<unsigned>(csize),
+  return ce_launch_cluster(ce_tc_kernel<BN, STAGES, PAIR>, dim3(grid), dim3(kThreads), smem, s,
+                           static_cast<unsigned>(csize),
                            P, C);
 }
 
@@ -614,10 +751,17 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
     cudaError_t e = cudaMemsetAsync(C, 0, static_cast<size_t>(plan.out_span) * 4, s);
     if (e != cudaSuccess) return e;
   }
+  if (P.mcast == 2) {
+    switch (plan.bn) {
+      case 64: return launch<64, 10, true>(P, C, s);
+      case 128: return launch<128, 8, true>(P, C, s);
+      default: return launch<256, 6, true>(P, C, s);
+    }
+  }
   switch (plan.bn) {
-    case 64: return launch<64, 8>(P, C, s);
-    case 128: return launch<128, 6>(P, C, s);
-    default: return launch<256, 4>(P, C, s);
+    case 64: return launch<64, 8, false>(P, C, s);
+    case 128: return launch<128, 6, false>(P, C, s);
+    default: return launch<256, 4, false>(P, C, s);
   }
 }
 
@@ -625,4 +769,7 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
 // launch with CE_TC_DBG & 32.  n <= 160*8.
 extern "C" int ce_debug_tc_timestamps(unsigned long long* out, int n) {
   return static_cast<int>(cudaMemcpyFromSymbol(out, g_tc_ts, sizeof(unsigned long long) * n));
+}
+extern "C" int ce_debug_tc_iter_timestamps(unsigned long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_tc_it, sizeof(unsigned long long) * 768));
 }

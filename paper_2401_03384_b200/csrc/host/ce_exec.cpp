@@ -45,6 +45,9 @@ Executor::Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cf
   }
   build_forward();
   if (want_backward_) build_backward();
+  compute_deps(fwd_);
+  compute_deps(bwd_);
+  if (const char* e = std::getenv("CE_CONCURRENT"); e && *e == '0') concurrent_ = false;
   if (const char* dbg = std::getenv("CE_DEBUG"); dbg && *dbg == '1') std::fputs(describe().c_str(), stderr);
 }
 
@@ -57,6 +60,34 @@ Executor::~Executor() {
     }
   for (auto& g : graphs_)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (auto* list : {&fwd_, &bwd_})
+    for (Step& st : *list)
+      if (st.done) cudaEventDestroy(st.done);
+  for (int k = 0; k < kStreams - 1; ++k) {
+    if (aux_[k]) cudaStreamDestroy(aux_[k]);
+    if (join_ev_[k]) cudaEventDestroy(join_ev_[k]);
+  }
+  if (fork_ev_) cudaEventDestroy(fork_ev_);
+}
+
+// Read-after-write, write-after-write and write-after-read hazards between the steps of
+// one pass.  Buffers are identified by their reference: workspace buffers come from a
+// bump allocator, so distinct offsets never overlap.
+void Executor::compute_deps(std::vector<Step>& steps) {
+  auto same = [](const BufRef& x, const BufRef& y) {
+    return x.kind != BufRef::kNone && x.kind == y.kind && x.index == y.index;
+  };
+  for (std::size_t i = 0; i < steps.size(); ++i) {
+    Step& si = steps[i];
+    si.deps.clear();
+    for (std::size_t j = 0; j < i; ++j) {
+      const Step& sj = steps[j];
+      const bool raw = same(sj.c, si.a) || same(sj.c, si.b);
+      const bool waw = same(sj.c, si.c);
+      const bool war = same(sj.a, si.c) || same(sj.b, si.c);
+      if (raw || waw || war) si.deps.push_back(static_cast<int>(j));
+    }
+  }
 }
 
 void Executor::launch_pass(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s, int which) {
@@ -501,6 +532,10 @@ std::string Executor::describe() const {
                       " bn=%d rows=%d cols=%d mma_n=%d tiles=%dx%dx%d split=%d kit=%d amn=%d bmn=%d tr=%d mc=%d\n", st.tc.bn,
                       P.m_rows, P.n_cols, P.n_mma, P.tiles_m, P.tiles_n, P.grid_z, P.k_split, P.k_iters, P.oa.mn_major,
                       P.ob.mn_major, P.transpose_store, P.mcast);
+      } else if (st.kind == Step::kPermute) {
+        char pd[256];
+        ce_permute_describe(st.desc.p, pd, sizeof pd);
+        std::snprintf(line + n, sizeof line - n, " %s\n", pd);
       } else {
         std::snprintf(line + n, sizeof line - n, " Z=%lld M=%lld N=%lld K=%lld (tc: %s)\n", (long long)st.desc.Z,
                       (long long)st.desc.M, (long long)st.desc.N, (long long)st.desc.K,
@@ -522,14 +557,87 @@ int Executor::tc_steps(bool bwd) const {
 }
 
 void Executor::run(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s) {
+  if (concurrent_ && !profiling_) {
+    run_concurrent(steps, need, s);
+    return;
+  }
   for (Step& st : steps) {
     st.ran = false;
     if (need && st.node >= 0 && !(*need)[static_cast<std::size_t>(st.node)]) continue;
-    const float* A = resolve(st.a);
-    const float* B = resolve(st.b);
-    float* C = resolve(st.c);
-    if (!C) continue;  // gradient not requested
+    if (!resolve(st.c)) continue;  // gradient not requested
     st.ran = true;
+    launch_step(st, s);
+  }
+}
+
+void Executor::run_concurrent(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s) {
+  for (int k = 0; k < kStreams - 1; ++k)
+    if (!aux_[k]) {
+      cuda_check(cudaStreamCreateWithFlags(&aux_[k], cudaStreamNonBlocking), "cudaStreamCreate");
+      cuda_check(cudaEventCreateWithFlags(&join_ev_[k], cudaEventDisableTiming), "cudaEventCreate");
+    }
+  if (!fork_ev_) cuda_check(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming), "cudaEventCreate");
+  cudaStream_t streams[kStreams] = {s};
+  for (int k = 1; k < kStreams; ++k) streams[k] = aux_[k - 1];
+  int last[kStreams];
+  bool joined[kStreams] = {true};
+  for (int k = 0; k < kStreams; ++k) last[k] = -1;
+  for (int k = 1; k < kStreams; ++k) joined[k] = false;
+  bool forked = false;
+  std::vector<int> sid(steps.size(), -1);
+  for (std::size_t i = 0; i < steps.size(); ++i) {
+    Step& st = steps[i];
+    st.ran = false;
+    if (need && st.node >= 0 && !(*need)[static_cast<std::size_t>(st.node)]) continue;
+    if (!resolve(st.c)) continue;
+    st.ran = true;
+    if (!st.done) cuda_check(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming), "cudaEventCreate");
+    // continue the chain of a dependency when it is the last step of its stream,
+    // otherwise take an idle stream, otherwise the stream whose tail is oldest
+    int pick = -1;
+    for (int j : st.deps)
+      if (steps[static_cast<std::size_t>(j)].ran && last[sid[static_cast<std::size_t>(j)]] == j) {
+        pick = sid[static_cast<std::size_t>(j)];
+        break;
+      }
+    if (pick < 0)
+      for (int k = 0; k < kStreams && pick < 0; ++k)
+        if (last[k] < 0) pick = k;
+    if (pick < 0) {
+      pick = 0;
+      for (int k = 1; k < kStreams; ++k)
+        if (last[k] < last[pick]) pick = k;
+    }
+    if (!joined[pick]) {
+      if (!forked) {
+        cuda_check(cudaEventRecord(fork_ev_, s), "cudaEventRecord");
+        forked = true;
+      }
+      cuda_check(cudaStreamWaitEvent(streams[pick], fork_ev_, 0), "cudaStreamWaitEvent");
+      joined[pick] = true;
+    }
+    for (int j : st.deps) {
+      const Step& dep = steps[static_cast<std::size_t>(j)];
+      if (dep.ran && sid[static_cast<std::size_t>(j)] != pick)
+        cuda_check(cudaStreamWaitEvent(streams[pick], dep.done, 0), "cudaStreamWaitEvent");
+    }
+    launch_step(st, streams[pick]);
+    cuda_check(cudaEventRecord(st.done, streams[pick]), "cudaEventRecord");
+    sid[i] = pick;
+    last[pick] = static_cast<int>(i);
+  }
+  for (int k = 1; k < kStreams; ++k)
+    if (joined[k]) {
+      cuda_check(cudaEventRecord(join_ev_[k - 1], streams[k]), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(s, join_ev_[k - 1], 0), "cudaStreamWaitEvent");
+    }
+}
+
+void Executor::launch_step(Step& st, cudaStream_t s) {
+  const float* A = resolve(st.a);
+  const float* B = resolve(st.b);
+  float* C = resolve(st.c);
+  {
     if (profiling_) {
       if (!st.ev0) {
         cuda_check(cudaEventCreate(&st.ev0), "cudaEventCreate");

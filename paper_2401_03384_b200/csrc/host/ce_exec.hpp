@@ -36,6 +36,8 @@ struct Step {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int node = -1;
   std::string label;
+  std::vector<int> deps;        // earlier steps of the same pass with a buffer hazard
+  cudaEvent_t done = nullptr;   // recorded after the step (cross-stream edges)
 };
 
 struct ExecConfig {
@@ -79,6 +81,9 @@ class Executor {
   void build_forward();
   void build_backward();
   void run(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s);
+  void run_concurrent(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s);
+  void launch_step(Step& st, cudaStream_t s);
+  static void compute_deps(std::vector<Step>& steps);
   float* resolve(const BufRef& r) const;
 
   EvaluationPlan plan_;
@@ -115,6 +120,12 @@ class Executor {
   };
   GraphCache graphs_[2];
   bool use_graphs_ = false;
+  // independent steps (e.g. the input- and factor-gradient of one node, a repack and the
+  // step before it) run on side streams, forked from and joined back into the caller's
+  static constexpr int kStreams = 4;
+  bool concurrent_ = true;
+  cudaStream_t aux_[kStreams - 1] = {};
+  cudaEvent_t fork_ev_ = nullptr, join_ev_[kStreams - 1] = {};
   void launch_pass(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s, int which);
 
  public:

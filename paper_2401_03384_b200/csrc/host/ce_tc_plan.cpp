@@ -283,7 +283,11 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   };
   P.m_rows = tile(A, a_mn == 1, CE_M, TC_BM, P.mt, &P.nm, TC_SRC_MTILE);
   // N tile: up to 256 columns
-  int ncap = 256;
+  static const int ncap_env = [] {
+    const char* e = std::getenv("CE_TC_NCAP");  // experiment knob: cap the N tile
+    return e ? std::atoi(e) : 256;
+  }();
+  int ncap = ncap_env;
   P.n_cols = tile(B, b_mn == 1, CE_N, ncap, P.nt, &P.nn, TC_SRC_NTILE);
   if (P.nm == 0 || P.nn == 0) return fail("no M or N tile unit");
   P.n_mma = static_cast<int32_t>((P.n_cols + 15) / 16 * 16);
@@ -397,15 +401,7 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   P.tiles_n = static_cast<int32_t>(tn);
   P.grid_z = static_cast<int32_t>(gz);
   P.k_iters = static_cast<int32_t>(ki);
-  // split-K when the output grid cannot fill the 148 SMs and K is long
-  const int64_t ctas = tm * tn * gz;
-  int split = 1;
-  if (ctas < 148 && ki >= 16) {
-    split = static_cast<int>(std::min<int64_t>((2 * 148 + ctas - 1) / ctas, ki / 8));
-    split = std::max(split, 1);
-  }
-  if (gz * split > 65535) return fail("grid z too large");
-  P.k_split = split;
+  P.k_split = 1;
   // K odometer steps: digit i of the K loop moves unit ku[i] by its box
   for (int i = 0; i < 6; ++i) {
     P.kcount[i] = 1;
@@ -445,12 +441,35 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
       P.ob.dim[1].u0 == P.nt[0]) {
     const int half = ((P.n_cols + 1) / 2 + 7) / 8 * 8;
     if (2 * half <= plan->bn) {
-      P.mcast = 1;
       P.mc_half = half;
       P.mc_ndim = 1;
       plan->box_b[1] = static_cast<uint32_t>(half);
-      P.ob.stage_bytes = 2 * half * 128;
+      static const bool pair_enabled = [] {
+        const char* e = std::getenv("CE_TC_PAIR");
+        return !(e && *e == '0');
+      }();
+      if (pair_enabled) {
+        // CTA pair, M=256 cta_group::2 MMAs: each CTA stages its own half of the B columns
+        P.mcast = 2;
+        P.ob.stage_bytes = half * 128;
+        P.n_mma = 2 * half;
+        P.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(P.n_mma >> 3) << 17) |
+                  (static_cast<uint32_t>((2 * TC_BM) >> 4) << 24);
+      } else {
+        P.mcast = 1;  // B halves multicast to both CTAs, M=128 MMAs per CTA
+        P.ob.stage_bytes = 2 * half * 128;
+      }
     }
+  }
+  // split-K when the output grid cannot fill the 148 SMs and K is long: as many K slices
+  // as fit in ONE wave of CTAs (a second, partial wave would cost a whole extra slice time)
+  {
+    const int64_t csize = P.mcast ? 2 : 1;
+    const int64_t ctas = (tm + csize - 1) / csize * csize * tn * gz;
+    int split = 1;
+    if (ctas < 148 && ki >= 16) split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 / ctas, ki / 8)));
+    if (gz * split > 65535) return fail("grid z too large");
+    P.k_split = split;
   }
   plan->valid = 1;
   plan->why = "ok";

@@ -35,6 +35,7 @@ class Context:
         h = ctypes.c_void_p()
         check(lib().ce_ctx_create(device, ctypes.byref(opts), ctypes.byref(h)))
         self._h = h
+        self._destroy = lib().ce_ctx_destroy
 
     @property
     def handle(self):
@@ -55,8 +56,9 @@ class Context:
         return t
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().ce_ctx_destroy(self._h)
+        # the destroy entry point is bound at creation: module globals may be gone at exit
+        if getattr(self, "_h", None) and getattr(self, "_destroy", None):
+            self._destroy(self._h)
             self._h = None
 
 
@@ -83,6 +85,7 @@ class Executor:
         h = ctypes.c_void_p()
         check(lib().ce_executor_create(ctx.handle, plan._h, int(backward), ctypes.byref(h)))
         self._h = h
+        self._destroy = lib().ce_executor_destroy
         self.stats = _lib.ExecStats()
 
     def _order_in(self):
@@ -152,8 +155,9 @@ class Executor:
         check(lib().ce_execute_host(self._h, ctypes.cast(ptrs, _lib.c_fpp), ctypes.c_void_p(host_out.ctypes.data)))
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().ce_executor_destroy(self._h)
+        # the destroy entry point is bound at creation: module globals may be gone at exit
+        if getattr(self, "_h", None) and getattr(self, "_destroy", None):
+            self._destroy(self._h)
             self._h = None
 
 

@@ -25,8 +25,18 @@ torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * (160 * 8))()
 _lib.lib().ce_debug_tc_timestamps(buf, 160 * 8)
 ts = np.array(buf, dtype=np.float64).reshape(160, 8)[:148]
+ts = ts[ts[:, 0] > 0]
 t0 = ts[:, 0].min()
-names = ["start", "setup", "producer_end", "mma_end", "epi_first_tile", "epi_end", "end"]
+names = ["start", "setup", "producer_end", "mma_end", "epi_first_tile", "epi_end", "end", "first_stage"]
 for i, n in enumerate(names):
     v = (ts[:, i] - t0) / 1e3
     print(f"{n:16s} min {v.min():8.2f} us  median {np.median(v):8.2f} us  max {v.max():8.2f} us")
+if int(os.environ["CE_TC_DBG"]) & 512:
+    it = (ctypes.c_ulonglong * 768)()
+    _lib.lib().ce_debug_tc_iter_timestamps(it)
+    a = np.array(it, dtype=np.float64).reshape(3, 256)
+    base = a[a > 0].min()
+    for role, nm in enumerate(["producer", "mma", "commit"]):
+        v = a[role]
+        v = (v[v > 0] - base) / 1e3
+        print(nm, " ".join(f"{x:.2f}" for x in v[:100]))

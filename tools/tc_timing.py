@@ -28,5 +28,5 @@ b = ex.profile(True)
 torch.cuda.synchronize()
 tag = os.environ.get("TAG", "")
 for n, k, t, fl, by in f + b:
-    if k == "tc":
-        print(f"{tag:10s} {n:16s} {t*1e3:9.1f} us  {fl/(t*1e-3)/1e12:7.1f} TF")
+    print(f"{tag:10s} {n:20s} {k:8s} {t*1e3:9.1f} us  {fl/(t*1e-3)/1e12:7.1f} TF {by/(t*1e-3)/1e9:7.0f} GB/s")
+print(f"{tag:10s} total {sum(r[2] for r in f + b)*1e3:9.1f} us")
