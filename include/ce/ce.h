@@ -166,6 +166,34 @@ ce_status ce_pairwise_eval(ce_ctx* ctx, const char* expr, const int64_t* dims, c
 ce_status ce_pairwise_grad(ce_ctx* ctx, const char* expr, const int64_t* dims, const int* ranks, const char* mode,
                            const float* a, const float* b, const float* dout, float* da, float* db);
 
+/* flops_actual (kernels.cpp:472-505) of the pairwise op built from expr "L,R->RES|convs"
+ * as in ce_pairwise_eval: exact executed multiply-adds, u128 as two u64. */
+ce_status ce_flops_actual(const char* expr, const int64_t* dims, const int* ranks, const char* mode, uint64_t* lo,
+                          uint64_t* hi);
+
+/* ------------------------------------------------------------ conv_einsum -- */
+/* The paper's call form conv_einsum("...", T1, T2, ...): parse ->
+ * make_shape_env -> resolve_conv_modes -> optimal(cost_mode) -> execute, with the
+ * plan and its executor cached in the context by (expression, shapes, mode,
+ * cost_mode).  inputs/out: device FP32 dense; stream-ordered on the ctx stream. */
+ce_status ce_conv_einsum(ce_ctx* ctx, const char* expr, const int64_t* dims, const int* ranks, int n_inputs,
+                         const char* mode, const char* cost_mode, const float* const* inputs, float* out);
+
+/* ------------------------------------------------------------ data parallel  */
+/* Batch-sharded training: factors are replicated, each rank runs its
+ * batch slice, and the factor gradients are summed across ranks.  NCCL is bound at
+ * run time (the libnccl.so.2 already in the process, e.g. torch's, else the system one).
+ * ce_nccl_unique_id: 128 bytes to hand from rank 0 to every rank (any transport). */
+ce_status ce_nccl_unique_id(void* id128);
+/* Joins the context to an nranks-wide communicator (one context per GPU). */
+ce_status ce_ctx_init_comm(ce_ctx* ctx, int nranks, int rank, const void* id128);
+/* In-place sum all-reduce of n FP32 device buffers, one NCCL group.  Runs on the
+ * context's communication stream after the work already queued on the ctx stream,
+ * so it overlaps later ctx work (e.g. the next layer's backward); ce_comm_wait
+ * orders the ctx stream after every collective issued so far. */
+ce_status ce_allreduce_grads(ce_ctx* ctx, float* const* bufs, const int64_t* counts, int n);
+ce_status ce_comm_wait(ce_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,19 +7,20 @@ is missing — there is no CPU fallback.
 """
 from . import _lib
 from .api import (CeError, LayerExpression, LayerSpec, ParseError, Plan, PlanError, ShapeError,  # noqa: F401
-                  classify, expression, left_to_right, optimal, parse, plan_from_joins, plan_to_json,
+                  classify, expression, flops_actual, left_to_right, optimal, parse, plan_from_joins, plan_to_json,
                   rank_for_compression, render, resnet34_cp_blocks, tree_encoding)
 
 _lib.lib()  # load now: no silent fallback
 
 __all__ = ["parse", "render", "classify", "optimal", "left_to_right", "plan_from_joins", "plan_to_json",
            "tree_encoding", "Plan", "LayerSpec", "LayerExpression", "expression", "rank_for_compression",
-           "resnet34_cp_blocks", "ParseError", "ShapeError", "PlanError", "CeError"]
+           "resnet34_cp_blocks", "flops_actual", "ParseError", "ShapeError", "PlanError", "CeError"]
 
 
 def __getattr__(name):
     # device layer is imported lazily so planner-only users need no torch.cuda
-    if name in ("Context", "Executor", "pairwise_eval", "pairwise_grad", "conv_einsum"):
+    if name in ("Context", "Executor", "pairwise_eval", "pairwise_grad", "conv_einsum", "conv_einsum_forward",
+                "nccl_unique_id"):
         from . import device
         return getattr(device, name)
     raise AttributeError(name)

@@ -82,6 +82,14 @@ SIGNATURES = {
     "ce_pairwise_grad": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, c_i64p, c_intp, ctypes.c_char_p,
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_void_p]),
+    "ce_flops_actual": (ctypes.c_int, [ctypes.c_char_p, c_i64p, c_intp, ctypes.c_char_p,
+                                       ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]),
+    "ce_conv_einsum": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, c_i64p, c_intp, ctypes.c_int,
+                                      ctypes.c_char_p, ctypes.c_char_p, c_fpp, ctypes.c_void_p]),
+    "ce_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+    "ce_ctx_init_comm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
+    "ce_allreduce_grads": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), c_i64p, ctypes.c_int]),
+    "ce_comm_wait": (ctypes.c_int, [ctypes.c_void_p]),
 }
 
 STATUS = {0: "OK", 1: "OTHER", 2: "PARSE", 3: "SHAPE", 4: "NUMERIC", 5: "PLAN", 6: "OVERFLOW",

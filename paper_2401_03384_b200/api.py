@@ -219,6 +219,14 @@ def expression(layer: LayerSpec, cr: Optional[float] = None) -> LayerExpression:
     return LayerExpression(ebuf.value.decode(), out, [int(rout[i]) for i in range(nrout.value)], int(pc.value))
 
 
+def flops_actual(expr: str, dims: Sequence[Sequence[int]], mode: str = "same") -> int:
+    """flops_actual (kernels.cpp:472-505) of the pairwise op "L,R->RES|convs" (exact MACs)."""
+    d, r, _ = _dims_arg(dims)
+    lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+    check(lib().ce_flops_actual(expr.encode(), d, r, mode.encode(), ctypes.byref(lo), ctypes.byref(hi)))
+    return _u128(lo.value, hi.value)
+
+
 def rank_for_compression(layer: LayerSpec, cr: float) -> int:
     return expression(layer, cr).ranks[0]
 

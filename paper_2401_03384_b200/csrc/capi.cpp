@@ -2,9 +2,13 @@
 // executor.  Exceptions never cross the ABI: they become ce_status codes with
 // a thread-local message (SPEC.md:542 exit-code mapping).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is bound with dlopen
 
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 
 #include "../../include/ce/ce.h"
@@ -23,6 +27,12 @@ struct ce_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   ce_options opts{};
+  // ce_conv_einsum cache: key = expression | shapes | mode | cost_mode
+  std::map<std::string, std::unique_ptr<Executor>> cached;
+  // data-parallel communicator (ce_ctx_init_comm)
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t comm_in = nullptr, comm_out = nullptr;
 };
 
 struct ce_executor {
@@ -35,6 +45,10 @@ namespace {
 thread_local std::string g_err;
 
 struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct NcclError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
@@ -58,6 +72,9 @@ ce_status guard(F&& f) {
   } catch (const CudaError& e) {
     g_err = e.what();
     return CE_ERR_CUDA;
+  } catch (const NcclError& e) {
+    g_err = e.what();
+    return CE_ERR_NCCL;
   } catch (const std::exception& e) {
     g_err = e.what();
     return std::string(e.what()).rfind("CUDA error", 0) == 0 ? CE_ERR_CUDA : CE_ERR_OTHER;
@@ -108,6 +125,49 @@ EvaluationPlan pairwise_plan(const char* expr, const int64_t* dims, const int* r
   plan.peak_intermediate_elements = static_cast<uint64_t>(node.op.result_elements());
   plan.nodes.push_back(std::move(node));
   return plan;
+}
+
+// NCCL entry points resolved at run time from the libnccl.so.2 already loaded in the
+// process (torch's) or, failing that, the system one.
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static std::once_flag once;
+  static NcclApi api;
+  static std::string why;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      why = dlerror();
+      return;
+    }
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(h, "ncclGroupStart"));
+    api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+  });
+  if (!api.all_reduce || !api.comm_init_rank || !api.get_unique_id || !api.group_start || !api.group_end)
+    throw NcclError("NCCL unavailable: " + (why.empty() ? std::string("missing symbols") : why));
+  return api;
+}
+
+void nccl_ok(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw NcclError(std::string("NCCL error in ") + what + ": " +
+                    (nccl().error_string ? nccl().error_string(r) : std::to_string(static_cast<int>(r))));
 }
 
 void fill_stats(const Executor& ex, ce_exec_stats* st, bool bwd) {
@@ -283,6 +343,14 @@ ce_status ce_ctx_create(int device, const ce_options* opts, ce_ctx** out) {
 
 void ce_ctx_destroy(ce_ctx* ctx) {
   if (!ctx) return;
+  ctx->cached.clear();
+  if (ctx->comm) {
+    cudaStreamSynchronize(ctx->comm_stream);
+    if (nccl().comm_destroy) nccl().comm_destroy(ctx->comm);
+    cudaStreamDestroy(ctx->comm_stream);
+    cudaEventDestroy(ctx->comm_in);
+    cudaEventDestroy(ctx->comm_out);
+  }
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -406,6 +474,83 @@ ce_status ce_pairwise_grad(ce_ctx* ctx, const char* expr, const int64_t* dims, c
     ex.backward(ins, dout, dins, ctx->stream);
     cuda_ok(cudaFreeAsync(scratch, ctx->stream), "cudaFreeAsync");
     cuda_ok(cudaStreamSynchronize(ctx->stream), "pairwise_grad");
+  });
+}
+
+ce_status ce_flops_actual(const char* expr, const int64_t* dims, const int* ranks, const char* mode, uint64_t* lo,
+                          uint64_t* hi) {
+  return guard([&] { split_u128(flops_actual(pairwise_plan(expr, dims, ranks, mode).nodes[0].op), lo, hi); });
+}
+
+ce_status ce_conv_einsum(ce_ctx* ctx, const char* expr, const int64_t* dims, const int* ranks, int n_inputs,
+                         const char* mode, const char* cost_mode, const float* const* inputs, float* out) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
+    std::string key = std::string(expr) + "|" + mode + "|" + cost_mode;
+    int64_t pos = 0;
+    for (int i = 0; i < n_inputs; ++i) {
+      key += "|";
+      for (int r = 0; r < ranks[i]; ++r) key += std::to_string(dims[pos++]) + ",";
+    }
+    auto it = ctx->cached.find(key);
+    if (it == ctx->cached.end()) {
+      ExpressionSpec spec = parse(expr);
+      ShapeEnv env = make_shape_env(spec, split_dims(dims, ranks, n_inputs));
+      EvaluationPlan plan =
+          optimal(spec, env, resolve_conv_modes(spec, conv_mode_from_string(mode)), cost_mode_from_string(cost_mode));
+      ExecConfig cfg;
+      cfg.math = ctx->opts.math;
+      auto ex = std::make_unique<Executor>(plan, false, cfg);
+      ex->set_use_graphs(ctx->opts.use_graphs != 0);
+      it = ctx->cached.emplace(key, std::move(ex)).first;
+    }
+    it->second->forward(inputs, out, ctx->stream);
+  });
+}
+
+ce_status ce_nccl_unique_id(void* id128) {
+  return guard([&] {
+    ncclUniqueId id;
+    nccl_ok(nccl().get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(id128, &id, sizeof id);
+  });
+}
+
+ce_status ce_ctx_init_comm(ce_ctx* ctx, int nranks, int rank, const void* id128) {
+  return guard([&] {
+    if (ctx->comm) throw std::runtime_error("context already has a communicator");
+    cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    nccl_ok(nccl().comm_init_rank(&ctx->comm, nranks, id, rank), "ncclCommInitRank");
+    cuda_ok(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_ok(cudaEventCreateWithFlags(&ctx->comm_in, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_ok(cudaEventCreateWithFlags(&ctx->comm_out, cudaEventDisableTiming), "cudaEventCreate");
+  });
+}
+
+ce_status ce_allreduce_grads(ce_ctx* ctx, float* const* bufs, const int64_t* counts, int n) {
+  return guard([&] {
+    if (!ctx->comm) throw std::runtime_error("ce_allreduce_grads: no communicator (ce_ctx_init_comm)");
+    cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cuda_ok(cudaEventRecord(ctx->comm_in, ctx->stream), "cudaEventRecord");
+    cuda_ok(cudaStreamWaitEvent(ctx->comm_stream, ctx->comm_in, 0), "cudaStreamWaitEvent");
+    const NcclApi& api = nccl();
+    nccl_ok(api.group_start(), "ncclGroupStart");
+    for (int i = 0; i < n; ++i)
+      if (bufs[i] && counts[i] > 0)
+        nccl_ok(api.all_reduce(bufs[i], bufs[i], static_cast<size_t>(counts[i]), ncclFloat32, ncclSum, ctx->comm,
+                               ctx->comm_stream),
+                "ncclAllReduce");
+    nccl_ok(api.group_end(), "ncclGroupEnd");
+    cuda_ok(cudaEventRecord(ctx->comm_out, ctx->comm_stream), "cudaEventRecord");
+  });
+}
+
+ce_status ce_comm_wait(ce_ctx* ctx) {
+  return guard([&] {
+    if (!ctx->comm) return;
+    cuda_ok(cudaStreamWaitEvent(ctx->stream, ctx->comm_out, 0), "cudaStreamWaitEvent");
   });
 }
 

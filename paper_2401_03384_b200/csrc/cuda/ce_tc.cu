@@ -36,9 +36,9 @@ __device__ unsigned long long g_tc_ts[160 * 8];
 __device__ unsigned long long g_tc_it[3 * 256];
 __device__ __forceinline__ void stamp_it(const TcParams& P, int role, uint32_t gi) {
   if ((P.dbg & 512) && blockIdx.x == 0 && gi < 256) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_tc_it[role * 256 + gi] = t;
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles (cheap; same SM for all roles)
+    g_tc_it[role * 256 + gi] = static_cast<unsigned long long>(t);
   }
 }
 __device__ __forceinline__ void stamp(const TcParams& P, int slot) {
@@ -432,13 +432,17 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
             tma_load_pair(sA + s * A_BYTES, &Pg.ta, full_lead + 8u * s, ca);
             tma_load_pair(sB + s * B_BYTES, &Pg.tb, full_lead + 8u * s, cb);
           } else {
-            mbar_expect_tx(&full[s], bytes);
+            // timing experiments: 2048 skips the A loads, 4096 the B loads
+            const uint32_t exp_bytes = bytes - ((P.dbg & 2048) ? P.oa.stage_bytes : 0) -
+                                       ((P.dbg & 4096) ? P.ob.stage_bytes : 0);
+            mbar_expect_tx(&full[s], exp_bytes);
             // K-major: one box; MN-major: nsub boxes of [32 K rows][32 MN] at 4 KB steps
-            for (int j = 0; j < P.oa.nsub; ++j) {
+            for (int j = 0; j < P.oa.nsub && !(P.dbg & 2048); ++j) {
               const int cj[5] = {ca[0] + 32 * j, ca[1], ca[2], ca[3], ca[4]};
               tma_load(sA + s * A_BYTES + j * 4096, &Pg.ta, &full[s], cj);
             }
-            if (mc) {
+            if (P.dbg & 4096) {
+            } else if (mc) {
               tma_load_mc(sB + s * B_BYTES + rank * P.mc_half * 128, &Pg.tb, &full[s], cb, 0x3);
             } else {
               for (int j = 0; j < P.ob.nsub; ++j) {
@@ -523,12 +527,12 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
         for (int it = k0; it < k1; ++it, ++gi) {
           const int s = static_cast<int>(gi % STAGES);
           mbar_wait(&full[s], (gi / STAGES) & 1);
-          if (P.oa.mn_major)
+          if (P.oa.mn_major && !(P.dbg & 8192))
             for (int j = xw; j < P.oa.nsub; j += kXposeWarps) xpose_block(sA + s * A_BYTES + j * 4096, lane);
-          if (P.ob.mn_major)
+          if (P.ob.mn_major && !(P.dbg & 8192))
             for (int j = xw; j < P.ob.nsub; j += kXposeWarps) xpose_block(sB + s * B_BYTES + j * 4096, lane);
           // generic-proxy smem writes must be visible to the tensor core (async proxy)
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (!(P.dbg & 16384)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (PAIR && !leader)
             mbar_arrive_cluster(mapa(&ready[s], 0));  // the even CTA issues the pair's MMAs
           else

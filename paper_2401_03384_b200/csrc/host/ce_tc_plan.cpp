@@ -425,9 +425,40 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   for (int v = 0; v < p.nv; ++v)
     if (p.cls[v] != CE_K) span += (p.ext[v] - 1) * p.sc[v];
   plan->out_span = span + 1;
-  // transposed store when the fastest N var is unit-stride in the output
-  const TcUnit& n0 = U[static_cast<std::size_t>(P.nt[0])];
-  P.transpose_store = n0.sc[0] == 1 ? 1 : 0;
+  // Epilogue store orientation: lanes along rows (plain) or along columns (transposed
+  // through smem).  Pick the one whose warp-wide store touches fewer 32-byte sectors,
+  // judged on the first 32 rows / columns of a tile (same offset math as the kernel).
+  {
+    auto offsets = [&](const int32_t* list, int n, int count) {
+      std::vector<int64_t> offs;
+      for (int local = 0; local < count; ++local) {
+        int64_t off = 0;
+        int64_t rest = local;
+        bool ok = true;
+        for (int i = 0; i < n; ++i) {
+          const TcUnit& u = U[static_cast<std::size_t>(list[i])];
+          int64_t v = rest % u.box;
+          rest /= u.box;
+          if (v >= u.ext) ok = false;
+          for (int k = 0; k < u.nv; ++k) {
+            off += (v % u.vext[k]) * u.sc[k];
+            v /= u.vext[k];
+          }
+        }
+        if (ok && rest == 0) offs.push_back(off);
+      }
+      return offs;
+    };
+    auto sectors = [](const std::vector<int64_t>& offs) {
+      std::vector<int64_t> sec;
+      for (int64_t o : offs) sec.push_back(o / 8);  // 8 floats per 32-B sector
+      std::sort(sec.begin(), sec.end());
+      return static_cast<int>(std::unique(sec.begin(), sec.end()) - sec.begin());
+    };
+    const int rows_sec = sectors(offsets(P.mt, P.nm, std::min(32, P.m_rows)));
+    const int cols_sec = sectors(offsets(P.nt, P.nn, std::min(32, P.n_cols)));
+    P.transpose_store = cols_sec < rows_sec ? 1 : 0;
+  }
   // both operands reach the MMA K-major (MN-major ones after the in-smem transpose)
   P.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(P.n_mma >> 3) << 17) |
             (static_cast<uint32_t>(TC_BM >> 4) << 24);

@@ -55,11 +55,64 @@ class Context:
             t.record_stream(cur)
         return t
 
+    # ------------------------------------------------------------ data parallel
+    def init_comm(self, world: int, rank: int, unique_id: bytes):
+        """Join an NCCL communicator of `world` contexts (ce_ctx_init_comm)."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        check(lib().ce_ctx_init_comm(self._h, world, rank, buf))
+        self.has_comm = True
+
+    def allreduce_grads(self, tensors: Sequence[torch.Tensor]):
+        """In-place SUM all-reduce of FP32 device tensors on the context's comm stream
+        (after the work queued on ctx.torch_stream); see comm_wait."""
+        ts = [t for t in tensors if t is not None]
+        if not ts:
+            return
+        self.torch_stream.wait_stream(torch.cuda.current_stream(self.device))
+        ptrs = (ctypes.c_void_p * len(ts))(*[ctypes.c_void_p(t.data_ptr()) for t in ts])
+        counts = (ctypes.c_int64 * len(ts))(*[t.numel() for t in ts])
+        check(lib().ce_allreduce_grads(self._h, ptrs, counts, len(ts)))
+
+    def comm_wait(self):
+        """Order the context stream (and the caller's current stream) after the collectives."""
+        check(lib().ce_comm_wait(self._h))
+        cur = torch.cuda.current_stream(self.device)
+        if cur.cuda_stream != self.torch_stream.cuda_stream:
+            cur.wait_stream(self.torch_stream)
+
     def __del__(self):
         # the destroy entry point is bound at creation: module globals may be gone at exit
         if getattr(self, "_h", None) and getattr(self, "_destroy", None):
             self._destroy(self._h)
             self._h = None
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through libce (rank 0 creates it, every rank passes it to init_comm)."""
+    buf = ctypes.create_string_buffer(128)
+    check(lib().ce_nccl_unique_id(buf))
+    return buf.raw
+
+
+def conv_einsum_forward(ctx: Context, expr: str, *tensors: torch.Tensor, mode: str = "same",
+                        cost_mode: str = "inference") -> torch.Tensor:
+    """ce_conv_einsum: plan + executor cached in the context by (expr, shapes, mode, cost_mode)."""
+    from .api import Plan as _P
+    dims = [list(t.shape) for t in tensors]
+    key = (expr, tuple(map(tuple, dims)), mode, cost_mode)
+    shapes = ctx.__dict__.setdefault("_out_shapes", {})
+    if key not in shapes:
+        shapes[key] = _P.optimal(expr, dims, mode, cost_mode).out_dims
+    ctx.torch_stream.wait_stream(torch.cuda.current_stream(ctx.device))
+    out = torch.empty(shapes[key], dtype=torch.float32, device=tensors[0].device)
+    d, r, _ = _dims_arg(dims)
+    ptrs = (ctypes.c_void_p * len(tensors))(*[ctypes.c_void_p(t.contiguous().data_ptr()) for t in tensors])
+    check(lib().ce_conv_einsum(ctx.handle, expr.encode(), d, r, len(tensors), mode.encode(), cost_mode.encode(),
+                               ctypes.cast(ptrs, _lib.c_fpp), ctypes.c_void_p(out.data_ptr())))
+    cur = torch.cuda.current_stream(ctx.device)
+    if cur.cuda_stream != ctx.torch_stream.cuda_stream:
+        cur.wait_stream(ctx.torch_stream)
+    return out
 
 
 def _ptrs(ts):

@@ -53,6 +53,26 @@ def allreduce_factor_grads(grads: Sequence[Optional[torch.Tensor]], group=None,
     return out
 
 
+def init_ce_comm(ctx, group=None) -> None:
+    """Join `ctx` (a device.Context, one per GPU) to a libce NCCL communicator over the
+    ranks of the torch.distributed group: rank 0 creates the unique id, a broadcast
+    (any backend) hands it out, then ce_ctx_init_comm."""
+    from .device import nccl_unique_id
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    ctx.init_comm(world, rank, obj[0])
+
+
+def allreduce_factor_grads_ce(ctx, grads: Sequence[Optional[torch.Tensor]],
+                              skip: Sequence[int] = (0,)) -> List[Optional[torch.Tensor]]:
+    """Factor-gradient SUM through libce's communicator (ce_allreduce_grads): one NCCL
+    group per layer on the context's comm stream, in place, overlapping whatever is
+    queued next on the context stream; call ctx.comm_wait() before reading the grads."""
+    ctx.allreduce_grads([g for i, g in enumerate(grads) if g is not None and i not in skip])
+    return list(grads)
+
+
 def data_parallel_step(inputs: Sequence[torch.Tensor], dout: torch.Tensor, rank: int, world: int,
                        fwd_bwd: Callable[[List[torch.Tensor], torch.Tensor], Tuple[torch.Tensor, List[torch.Tensor]]],
                        group=None):

@@ -304,3 +304,41 @@ def test_rtr_cfg3_reduced(any_ctx):
 def test_native_library_loaded(ctx):
     maps = open("/proc/self/maps").read()
     assert "libce.so" in maps
+
+
+@pytest.mark.gpu
+def test_flops_actual_and_conv_einsum_forward(ctx):
+    """ce_flops_actual against the oracle; ce_conv_einsum (cached plan) against the FP64 oracle."""
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import conv_einsum_forward
+    for e, d in [("bshw,rs->bhwr", [[8, 64, 32, 32], [16, 64]]), ("bhw(r2),(r1)(r2)hw->bhw(r1)|hw",
+                                                                   [[2, 14, 14, 5], [6, 5, 3, 3]])]:
+        assert ce.flops_actual(e, d) == npo.flops_actual(npo.pairwise_from_expr(e, d[0], d[1], "same"))
+    expr, dims = "bshw,rt,rs,rh,rw->bthw|hw", [[2, 8, 9, 9], [4, 6], [4, 8], [4, 3], [4, 3]]
+    rng = np.random.default_rng(5)
+    ins = [f32(rng.uniform(-1, 1, d)) for d in dims]
+    xs = [torch.from_numpy(x.astype(np.float32)).cuda() for x in ins]
+    for _ in range(2):  # second call replays the cached executor
+        out = conv_einsum_forward(ctx, expr, *xs)
+    torch.cuda.synchronize()
+    plan = ce.optimal(expr, dims, "same", "inference")
+    nodes = [(n["left"], n["right"], n["result"]) for n in json.loads(plan.to_json())["nodes"]]
+    ref, _ = npo.execute(expr, dims, nodes, ins)
+    assert nerr(out.cpu().numpy(), ref) <= TOL["auto"][0]
+
+
+@pytest.mark.gpu
+def test_single_rank_nccl_allreduce(ctx):
+    """ce_nccl_unique_id / ce_ctx_init_comm / ce_allreduce_grads / ce_comm_wait on a 1-rank
+    communicator: the SUM over one rank is the identity, and the comm stream is ordered
+    after the context stream."""
+    from paper_2401_03384_b200.device import Context, nccl_unique_id
+    c = Context(0, "auto")
+    c.init_comm(1, 0, nccl_unique_id())
+    g = [torch.arange(1000, dtype=torch.float32, device="cuda"), torch.ones(7, device="cuda")]
+    ref = [t.clone() for t in g]
+    c.allreduce_grads(g)
+    c.comm_wait()
+    torch.cuda.synchronize()
+    for a, b in zip(g, ref):
+        assert torch.equal(a, b)

@@ -38,5 +38,5 @@ if int(os.environ["CE_TC_DBG"]) & 512:
     base = a[a > 0].min()
     for role, nm in enumerate(["producer", "mma", "commit"]):
         v = a[role]
-        v = (v[v > 0] - base) / 1e3
+        v = (v[v > 0] - base) / 1.9e3  # SM cycles -> us at ~1.9 GHz
         print(nm, " ".join(f"{x:.2f}" for x in v[:100]))
