@@ -28,9 +28,10 @@ namespace {
 constexpr int kEpiWarps = 4;
 constexpr int kXposeWarps = 4;
 constexpr int kThreads = 64 + 32 * kEpiWarps + 32 * kXposeWarps;
+constexpr int kStagePitch = 36;  // floats per staged row: 16-B aligned, conflict-free float4 phases
 
 // Debug-only phase timestamps (P.dbg & 32): [cta][slot] = %globaltimer (ns).
-__device__ unsigned long long g_tc_ts[160 * 8];
+__device__ unsigned long long g_tc_ts[160 * 16];
 // Debug-only per-iteration timestamps of CTA 0 (P.dbg & 512): [role][iteration], role 0
 // producer (after its empty wait), 1 MMA issuer (after its full wait).
 __device__ unsigned long long g_tc_it[3 * 256];
@@ -45,7 +46,7 @@ __device__ __forceinline__ void stamp(const TcParams& P, int slot) {
   if (P.dbg & 32) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (blockIdx.x < 160) g_tc_ts[blockIdx.x * 8 + slot] = t;
+    if (blockIdx.x < 160) g_tc_ts[blockIdx.x * 16 + slot] = t;
   }
 }
 
@@ -196,6 +197,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Vector reduction into global memory (split-K epilogue): 4 consecutive floats, one request.
+__device__ __forceinline__ void red_add_v4(float* p, float4 v) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
 
 __device__ __forceinline__ void cluster_sync() {
@@ -222,6 +230,7 @@ __device__ __forceinline__ void xpose_block(uint8_t* blk, int lane) {
 struct Tile {
   int32_t val[TC_MAX_UNITS];  // tile origins / grid digits per unit (K units 0)
   int split;
+  int ntile;                  // linear N-tile index (the column tables depend only on it)
 };
 
 // Work item w of a group of `csize` CTAs (rank within the group): m tiles are dealt
@@ -233,6 +242,7 @@ __device__ __forceinline__ void decode_work(const TcParams& P, uint32_t w, uint3
   const uint32_t pm = (static_cast<uint32_t>(P.tiles_m) + csize - 1) / csize;
   uint32_t m = (w % pm) * csize + rank;
   uint32_t t = w / pm;
+  T.ntile = static_cast<int>(t % static_cast<uint32_t>(P.tiles_n));
   for (int i = 0; i < P.nm; ++i) {
     const TcUnit& u = P.u[P.mt[i]];
     const uint32_t n = static_cast<uint32_t>((u.ext + u.box - 1) / u.box);
@@ -308,9 +318,12 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  float* stage_out = reinterpret_cast<float*>(sB + STAGES * B_BYTES);      // [kEpiWarps][32][33]
-  int64_t* col_off = reinterpret_cast<int64_t*>(stage_out + kEpiWarps * 32 * 33);  // [2][BN]
-  uint64_t* full = reinterpret_cast<uint64_t*>(col_off + 2 * BN);
+  float* stage_out = reinterpret_cast<float*>(sB + STAGES * B_BYTES);  // [kEpiWarps][32][kStagePitch]
+  int64_t* col_off = reinterpret_cast<int64_t*>(stage_out + kEpiWarps * 32 * kStagePitch);  // [2][BN]
+  int64_t* grp_off = col_off + 2 * BN;                                  // [2][BN/4]: 16-B column groups
+  int64_t* row_tab = grp_off + 2 * (BN / 4);                            // [2][128]: row offsets in C
+  Tile* tiles = reinterpret_cast<Tile*>(row_tab + 2 * TC_BM);           // [0] producer, [1] epilogue
+  uint64_t* full = reinterpret_cast<uint64_t*>(tiles + 2);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;       // [2]
@@ -373,58 +386,66 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) stamp(P, 1);
-  // setup above overlapped the previous kernel's tail (PDL); global memory only from here
-  ce_pdl_enter();
+  // Let the next kernel of the stream be scheduled (PDL).  The wait for the previous kernel
+  // (griddepcontrol.wait) is deferred to each role's first global-memory access: the set-up
+  // above and the first tile's decoding / address tables overlap the predecessor's tail.
+  ce_pdl_trigger();
 
   if (P.dbg & 64) {
     // timing experiment: set-up and tear-down only
   } else if (warp == 0) {
     if (lane == 0) {
       // ---------------------------------------------------------- TMA producer
+      // Single issuing thread: everything in the per-stage loop is register arithmetic
+      // (the loop period is this thread's instruction latency when the ring is not full).
       const uint32_t bytes = static_cast<uint32_t>(P.oa.stage_bytes + P.ob.stage_bytes);
       const uint32_t full_lead = PAIR ? mapa(&full[0], 0) : 0u;
-      int step_a[6][5], step_b[6][5], kcount[6];
+      const int dbg = Pg.dbg;
+      const int nsub_a = P.oa.nsub, nsub_b = P.ob.nsub;
+      const int mc_ndim = P.mc_ndim, mc_half = P.mc_half;
+      // digit-0 deltas live in registers; carries (rare) and per-tile set-up read shared memory
+      int kd0_a[5], kd0_b[5];
 #pragma unroll
-      for (int u = 0; u < 6; ++u) {
-        kcount[u] = P.kcount[u];
-#pragma unroll
-        for (int d = 0; d < 5; ++d) {
-          step_a[u][d] = P.kstep_a[u][d];
-          step_b[u][d] = P.kstep_b[u][d];
-        }
+      for (int d = 0; d < 5; ++d) {
+        kd0_a[d] = P.kdelta_a[0][d];
+        kd0_b[d] = P.kdelta_b[0][d];
       }
+      const int kc0 = P.kcount[0];
       uint32_t gi = 0;  // global stage counter across tiles
-      Tile T;
+      Tile& T = tiles[0];
+      if (dbg & 32) stamp(P, 9);  // producer entered (after griddepcontrol.wait)
       for (uint32_t w = group; w < n_work; w += ngroups) {
         decode_work(P, w, rank, csize, T);
         int k0, k1;
         k_range(P, T.split, k0, k1);
-        int baseA[5], baseB[5], dig[6];
-        coords(P.oa, T.val, baseA);
-        coords(P.ob, T.val, baseB);
-        if (csize == 2) baseB[P.mc_ndim] += static_cast<int>(rank) * P.mc_half;  // this CTA's half of the B rows
-        int x = k0;
+        int ca[5], cb[5], dig[6];
+        coords(P.oa, T.val, ca);
+        coords(P.ob, T.val, cb);
+        if (csize == 2) cb[mc_ndim] += static_cast<int>(rank) * mc_half;  // this CTA's half of the B rows
 #pragma unroll
-        for (int u = 0; u < 6; ++u) {
-          dig[u] = x % kcount[u];
-          x /= kcount[u];
+        for (int u = 0; u < 6; ++u) dig[u] = 0;
+        if (k0 != 0) {  // split-K slice: start the odometer mid-way
+          int x = k0;
+#pragma unroll
+          for (int u = 0; u < 6; ++u) {
+            dig[u] = x % P.kcount[u];
+            x /= P.kcount[u];
+#pragma unroll
+            for (int d = 0; d < 5; ++d) {
+              ca[d] += dig[u] * P.kstep_a[u][d];
+              cb[d] += dig[u] * P.kstep_b[u][d];
+            }
+          }
+        }
+        if (gi == 0) {
+          if (dbg & 32) stamp(P, 8);  // producer ready to issue its first load
+          ce_pdl_wait();              // operands written by the previous kernel are visible
         }
         for (int it = k0; it < k1; ++it, ++gi) {
           const int s = static_cast<int>(gi % STAGES);
           mbar_wait(&empty[s], ((gi / STAGES) & 1) ^ 1);
-          stamp_it(P, 0, gi);
-          int ca[5], cb[5];
-#pragma unroll
-          for (int d = 0; d < 5; ++d) {
-            ca[d] = baseA[d];
-            cb[d] = baseB[d];
-#pragma unroll
-            for (int u = 0; u < 6; ++u) {
-              ca[d] += dig[u] * step_a[u][d];
-              cb[d] += dig[u] * step_b[u][d];
-            }
-          }
-          if (P.dbg & 2) {
+          if (dbg & 512) stamp_it(P, 0, gi);
+          if (dbg & 2) {
             if (!PAIR || xpose || leader) mbar_arrive(&full[s]);
           } else if (PAIR && !xpose) {
             // both halves complete on the even CTA's barrier, which expects the pair's bytes
@@ -433,28 +454,53 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
             tma_load_pair(sB + s * B_BYTES, &Pg.tb, full_lead + 8u * s, cb);
           } else {
             // timing experiments: 2048 skips the A loads, 4096 the B loads
-            const uint32_t exp_bytes = bytes - ((P.dbg & 2048) ? P.oa.stage_bytes : 0) -
-                                       ((P.dbg & 4096) ? P.ob.stage_bytes : 0);
+            const uint32_t exp_bytes =
+                bytes - ((dbg & 2048) ? P.oa.stage_bytes : 0) - ((dbg & 4096) ? P.ob.stage_bytes : 0);
             mbar_expect_tx(&full[s], exp_bytes);
             // K-major: one box; MN-major: nsub boxes of [32 K rows][32 MN] at 4 KB steps
-            for (int j = 0; j < P.oa.nsub && !(P.dbg & 2048); ++j) {
-              const int cj[5] = {ca[0] + 32 * j, ca[1], ca[2], ca[3], ca[4]};
-              tma_load(sA + s * A_BYTES + j * 4096, &Pg.ta, &full[s], cj);
+            if (!(dbg & 2048)) {
+              tma_load(sA + s * A_BYTES, &Pg.ta, &full[s], ca);
+              for (int j = 1; j < nsub_a; ++j) {
+                const int cj[5] = {ca[0] + 32 * j, ca[1], ca[2], ca[3], ca[4]};
+                tma_load(sA + s * A_BYTES + j * 4096, &Pg.ta, &full[s], cj);
+              }
             }
-            if (P.dbg & 4096) {
+            if (dbg & 4096) {
             } else if (mc) {
-              tma_load_mc(sB + s * B_BYTES + rank * P.mc_half * 128, &Pg.tb, &full[s], cb, 0x3);
+              tma_load_mc(sB + s * B_BYTES + rank * mc_half * 128, &Pg.tb, &full[s], cb, 0x3);
             } else {
-              for (int j = 0; j < P.ob.nsub; ++j) {
+              tma_load(sB + s * B_BYTES, &Pg.tb, &full[s], cb);
+              for (int j = 1; j < nsub_b; ++j) {
                 const int cj[5] = {cb[0] + 32 * j, cb[1], cb[2], cb[3], cb[4]};
                 tma_load(sB + s * B_BYTES + j * 4096, &Pg.tb, &full[s], cj);
               }
             }
           }
+          // advance the K odometer: digit 0 almost always, carries rarely
+          if (++dig[0] < kc0) {
 #pragma unroll
-          for (int u = 0; u < 6; ++u) {
-            if (++dig[u] < kcount[u]) break;
-            dig[u] = 0;
+            for (int d = 0; d < 5; ++d) {
+              ca[d] += kd0_a[d];
+              cb[d] += kd0_b[d];
+            }
+          } else {
+            dig[0] = 0;
+            bool carry = true;
+#pragma unroll
+            for (int u = 1; u < 6; ++u) {
+              if (carry) {
+                if (++dig[u] < P.kcount[u]) {
+                  carry = false;
+#pragma unroll
+                  for (int d = 0; d < 5; ++d) {
+                    ca[d] += P.kdelta_a[u][d];
+                    cb[d] += P.kdelta_b[u][d];
+                  }
+                } else {
+                  dig[u] = 0;
+                }
+              }
+            }
           }
         }
       }
@@ -463,11 +509,18 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ---------------------------------------------------------- MMA issuer
+      const int dbg = Pg.dbg;
+      const uint32_t idesc = P.idesc;
+      const int kc0 = P.kcount[0], ktail = P.ktail_kk;
+      // descriptors of stage 0; stage s and K step kk add (s * bytes + kk * 32) >> 4 to the
+      // 14-bit start-address field (smem < 256 KB, so the add never carries out of it)
+      const uint64_t adesc0 = kmajor_desc(smem_u32(sA)), bdesc0 = kmajor_desc(smem_u32(sB));
       uint32_t gi = 0, local = 0;
       for (uint32_t w = group; w < n_work; w += ngroups, ++local) {
         const int acc = static_cast<int>(local & 1);
         int k0, k1;
         k_range(P, work_split(P, w, csize), k0, k1);
+        int d0 = k0 % kc0;  // K digit 0 of the first iteration (for the K tail)
         if (PAIR)
           mbar_wait_cluster(&tempty[acc], ((local >> 1) & 1) ^ 1);  // both epilogues drained it
         else
@@ -480,22 +533,27 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
             mbar_wait_cluster(&ready[s], (gi / STAGES) & 1);
           else
             mbar_wait(xpose ? &ready[s] : &full[s], (gi / STAGES) & 1);
-          if (gi == 0) stamp(P, 7);
-          stamp_it(P, 1, gi);
-          if (!(P.dbg & 256)) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
-          if (!(P.dbg & 1)) {
+          if (dbg & 32) {
+            if (gi == 0) stamp(P, 7);
+            stamp_it(P, 1, gi);
+          }
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t ad = adesc0 + static_cast<uint64_t>((s * A_BYTES) >> 4);
+          const uint64_t bd = bdesc0 + static_cast<uint64_t>((s * B_BYTES) >> 4);
+          const int nkk = (d0 == kc0 - 1) ? ktail : TC_BK / 8;
+          if (++d0 == kc0) d0 = 0;
+          if (!(dbg & 1)) {
 #pragma unroll
             for (int kk = 0; kk < TC_BK / 8; ++kk) {  // K=8 per tf32 MMA: +32 B inside the 128-B row
-              if (PAIR)
-                mma_tf32_pair(d_tmem, kmajor_desc(a0 + kk * 32), kmajor_desc(b0 + kk * 32), P.idesc,
-                              (it > k0 || kk > 0) ? 1u : 0u);
-              else
-                mma_tf32(d_tmem, kmajor_desc(a0 + kk * 32), kmajor_desc(b0 + kk * 32), P.idesc,
-                         (it > k0 || kk > 0) ? 1u : 0u);
+              if (kk < nkk) {
+                if (PAIR)
+                  mma_tf32_pair(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (it > k0 || kk > 0) ? 1u : 0u);
+                else
+                  mma_tf32(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (it > k0 || kk > 0) ? 1u : 0u);
+              }
             }
           }
-          if (P.dbg & 16)
+          if (dbg & 16)
             mbar_arrive(&empty[s]);  // timing experiment (with bit 0, no multicast): plain arrive
           else if (PAIR)
             mma_commit_pair(&empty[s]);  // the slot of this stage in both CTAs
@@ -503,10 +561,6 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
             mma_commit_mc(&empty[s], 0x3);  // both CTAs wrote this stage's B halves
           else
             mma_commit(&empty[s]);  // frees the smem slot once these MMAs retire
-          if (P.dbg & 1024) {  // timing experiment: wait for this stage's MMAs + commit
-            mbar_wait(&empty[s], (gi / STAGES) & 1);
-            stamp_it(P, 2, gi);
-          }
         }
         if (PAIR)
           mma_commit_pair(&tfull[acc]);  // both CTAs' accumulators of this tile complete
@@ -542,22 +596,33 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     }
   } else {
     // ------------------------------------------------------------ epilogue warps
+    // Per tile: one thread decodes the work item, the warps fill the row / column offset
+    // tables (overlapping the MMAs), then each warp drains its TMEM lane quarter 32 columns
+    // at a time.  Columns that are contiguous and 16-B aligned in C (the padded channel-
+    // last intermediates) go out as 128-bit stores; anything else element by element.
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;     // accumulator row owned by this thread
     const int ew = warp - 2;           // 0..3
-    float* stage = stage_out + ew * 32 * 33;
+    const int et = threadIdx.x - 64;   // 0..127
+    float* stage = stage_out + ew * 32 * kStagePitch;
     const bool atomic = P.k_split > 1;
+    const int dbg = Pg.dbg;
+    const int n_cols = P.n_cols, m_rows = P.m_rows;
+    const bool tstore = P.transpose_store != 0;
+    const bool c_al = (reinterpret_cast<uintptr_t>(C) & 15u) == 0;
     uint32_t local = 0;
-    Tile T;
+    Tile& T = tiles[1];
+    int cols_for[2] = {-1, -1};  // N tile whose column tables each accumulator buffer holds
     for (uint32_t w = group; w < n_work; w += ngroups, ++local) {
       const int acc = static_cast<int>(local & 1);
-      decode_work(P, w, rank, csize, T);
+      if (et == 0) decode_work(P, w, rank, csize, T);
+      epi_bar();  // decoded tile visible (and the previous tile's tables are no longer read)
       int k0, k1;
       k_range(P, T.split, k0, k1);
       // address tables for this tile (overlaps the MMAs)
       int64_t* cols = col_off + acc * BN;
-      for (int c = threadIdx.x - 64; c < BN; c += 32 * kEpiWarps)
-        cols[c] = c < P.n_cols ? tile_offset(P, P.nt, P.nn, T.val, c) : -1;
+      int64_t* gcol = grp_off + acc * (BN / 4);
+      int64_t* rtab = row_tab + acc * TC_BM;
       int64_t base = 0;
       for (int i = 0; i < P.ng; ++i) {
         const TcUnit& u = P.u[P.gu[i]];
@@ -567,12 +632,27 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
           v /= static_cast<uint32_t>(u.vext[k]);
         }
       }
-      const int64_t ro = row < P.m_rows ? tile_offset(P, P.mt, P.nm, T.val, row) : -1;
-      float* crow = C + base + (ro < 0 ? 0 : ro);
-      epi_bar();  // column table visible to all epilogue warps
+      // column tables depend only on the N tile: most launches have a single N tile, so they
+      // are built once per accumulator buffer
+      if (T.ntile != cols_for[acc]) {
+        for (int c = et; c < BN; c += 32 * kEpiWarps) cols[c] = c < n_cols ? tile_offset(P, P.nt, P.nn, T.val, c) : -1;
+        epi_bar();
+        for (int g = et; g < BN / 4; g += 32 * kEpiWarps) {
+          const int64_t c0 = cols[4 * g];
+          const bool ok = c_al && c0 >= 0 && (c0 & 3) == 0 && cols[4 * g + 1] == c0 + 1 && cols[4 * g + 2] == c0 + 2 &&
+                          cols[4 * g + 3] == c0 + 3;
+          gcol[g] = ok ? c0 : -1;
+        }
+        cols_for[acc] = T.ntile;
+      }
+      const int64_t ro = row < m_rows ? tile_offset(P, P.mt, P.nm, T.val, row) : -1;
+      const int64_t roff = ro < 0 ? -1 : base + ro;  // row offset in C, -1 outside the tile
+      rtab[row] = roff;
+      epi_bar();  // tables visible to all epilogue warps
+      if ((dbg & 32) && et == 0 && local == 0) stamp(P, 10);
       mbar_wait(&tfull[acc], (local >> 1) & 1);
-      if (threadIdx.x == 64 && local == 0) stamp(P, 4);
-      if (P.dbg & 8) {  // timing experiment: skip the epilogue body
+      if ((dbg & 32) && et == 0 && local == 0) stamp(P, 4);
+      if (dbg & 8) {  // timing experiment: skip the epilogue body
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         if (PAIR && !leader)
           mbar_arrive_cluster(mapa(&tempty[acc], 0));
@@ -581,54 +661,89 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
         continue;
       }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (local == 0) ce_pdl_wait();  // (long complete: the producer waited before its loads)
       const bool empty_k = k1 <= k0;
       const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
       for (int ch = 0; ch < BN / 32; ++ch) {
-        if (ch * 32 >= P.n_cols) break;
+        if (ch * 32 >= n_cols) break;
         uint32_t r[32];
         tmem_ld32(t_base + ch * 32, r);
         if (empty_k)
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = 0;
-        if (P.dbg & 4) {
+        if (dbg & 4) {
           // timing experiment: TMEM loads only, no stores
           if (r[0] == 0x7fffffffu) C[0] = 0.f;
-        } else if (P.transpose_store) {
-          // lanes write consecutive columns of one row: coalesced for column-contiguous outputs
+        } else if (tstore) {
+          // stage this warp's 32x32 block row-major; then each lane writes 4 consecutive columns
+          // of one row (8 lanes cover a row: 128 B per row, 4 rows per instruction)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) stage[lane * 33 + i] = __uint_as_float(r[i]);
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(stage + lane * kStagePitch + 4 * j) =
+                make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                            __uint_as_float(r[4 * j + 3]));
           __syncwarp();
-          const int64_t co = cols[ch * 32 + lane];
-          float* cbase = C + base + co;
-          if (atomic) {
+          const int g = lane & 7, sub = lane >> 3;
+          const int64_t gc = gcol[ch * 8 + g];
+#pragma unroll 4
+          for (int k = 0; k < 8; ++k) {
+            const int rr = 4 * k + sub;
+            const int64_t rt = rtab[q * 32 + rr];
+            if (rt < 0) continue;
+            const float4 v = *reinterpret_cast<const float4*>(stage + rr * kStagePitch + 4 * g);
+            if (gc >= 0 && (rt & 3) == 0) {
+              float* dst = C + rt + gc;
+              if (atomic)
+                red_add_v4(dst, v);
+              else
+                *reinterpret_cast<float4*>(dst) = v;
+            } else {
+              const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-            for (int rr = 0; rr < 32; ++rr) {
-              const int64_t rrow = __shfl_sync(0xffffffffu, ro, rr);
-              const float v = stage[rr * 33 + lane];
-              if (rrow >= 0 && co >= 0) atomicAdd(cbase + rrow, v);
-            }
-          } else {
-#pragma unroll
-            for (int rr = 0; rr < 32; ++rr) {
-              const int64_t rrow = __shfl_sync(0xffffffffu, ro, rr);
-              const float v = stage[rr * 33 + lane];
-              if (rrow >= 0 && co >= 0) cbase[rrow] = v;
+              for (int i = 0; i < 4; ++i) {
+                const int64_t co = cols[ch * 32 + 4 * g + i];
+                if (co < 0) continue;
+                if (atomic)
+                  atomicAdd(C + rt + co, vv[i]);
+                else
+                  C[rt + co] = vv[i];
+              }
             }
           }
           __syncwarp();
-        } else if (ro >= 0) {
-          int64_t co[32];
+        } else if (roff >= 0) {
+          float* crow = C + roff;
+          bool vec = (roff & 3) == 0;
+          int64_t gc[8];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) co[i] = cols[ch * 32 + i];
-          if (atomic) {
+          for (int g = 0; g < 8; ++g) {
+            gc[g] = gcol[ch * 8 + g];
+            vec = vec && gc[g] >= 0;
+          }
+          if (vec) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (co[i] >= 0) atomicAdd(crow + co[i], __uint_as_float(r[i]));
+            for (int g = 0; g < 8; ++g) {
+              const float4 v = make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
+                                           __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3]));
+              if (atomic)
+                red_add_v4(crow + gc[g], v);
+              else
+                *reinterpret_cast<float4*>(crow + gc[g]) = v;
+            }
           } else {
+            int64_t co[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (co[i] >= 0) crow[co[i]] = __uint_as_float(r[i]);
+            for (int i = 0; i < 32; ++i) co[i] = cols[ch * 32 + i];
+            if (atomic) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (co[i] >= 0) atomicAdd(crow + co[i], __uint_as_float(r[i]));
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (co[i] >= 0) crow[co[i]] = __uint_as_float(r[i]);
+            }
           }
         }
       }
@@ -704,7 +819,8 @@ int sm_count() {
 template <int BN, int STAGES, bool PAIR>
 cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
   constexpr int smem =
-      STAGES * (TC_BM * 128 + (PAIR ? BN * 64 : BN * 128)) + kEpiWarps * 32 * 33 * 4 + 2 * BN * 8 + 8 * (3 * STAGES + 4) + 16 + 64 +
+      STAGES * (TC_BM * 128 + (PAIR ? BN * 64 : BN * 128)) + kEpiWarps * 32 * kStagePitch * 4 +
+      (2 * BN + 2 * (BN / 4) + 2 * TC_BM) * 8 + 2 * static_cast<int>(sizeof(Tile)) + 8 * (3 * STAGES + 4) + 16 + 64 +
       static_cast<int>(sizeof(TcParams)) + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static bool configured = false;
@@ -741,6 +857,15 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
   if (!plan.valid) return cudaErrorInvalidValue;
   TcParams& P = plan.params;
   P.dbg = debug_flags();
+  {
+    // debug: CE_TC_DBG_AT=n applies the debug flags to the n-th TC launch of the process only
+    static const int at = [] {
+      const char* e = getenv("CE_TC_DBG_AT");
+      return e ? atoi(e) : -1;
+    }();
+    static int counter = 0;
+    if (at >= 0 && counter++ != at) P.dbg = 0;
+  }
   if (plan.cached_a != A) {
     if (!encode(&P.ta, A, plan.gdim_a, plan.gstride_a, plan.box_a)) return cudaErrorInvalidValue;
     plan.cached_a = A;
@@ -771,7 +896,7 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
 
 // Debug only (not part of include/ce/ce.h): copy the phase timestamps of the last
 // launch with CE_TC_DBG & 32.  n <= 160*8.
-extern "C" int ce_debug_tc_timestamps(unsigned long long* out, int n) {
+extern "C" int ce_debug_tc_timestamps(unsigned long long* out, int n) {  // n <= 160*16
   return static_cast<int>(cudaMemcpyFromSymbol(out, g_tc_ts, sizeof(unsigned long long) * n));
 }
 extern "C" int ce_debug_tc_iter_timestamps(unsigned long long* out) {

@@ -70,6 +70,12 @@ struct TcParams {
   // coordinate[d] = base[d] + sum_i digit_i * kstep_{a,b}[i][d], digit_i < kcount[i]
   int32_t kcount[6];
   int32_t kstep_a[6][5], kstep_b[6][5];
+  // carry deltas: coordinate change when digit i increments and every lower digit wraps to 0
+  // (the producer advances its coordinates incrementally instead of re-deriving them)
+  int32_t kdelta_a[6][5], kdelta_b[6][5];
+  // MMAs (of K=8) issued for the last chunk of K digit 0 when it is the 32-wide K block of a
+  // single unit whose extent is not a multiple of 32 (its tail rows are TMA zero fill); else 4
+  int32_t ktail_kk;
   // 2-CTA cluster along M: each CTA TMA-loads mc_half rows of the B tile and multicasts
   // them to both CTAs (B is read from L2 once per CTA pair instead of once per CTA)
   int32_t mcast;           // 1: launched with cluster dims (2,1,1)

@@ -369,6 +369,52 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
         }
       }
     }
+    if (ok && (st.tc.params.oa.mn_major || st.tc.params.ob.mn_major) && st.tc.params.k_iters > 64) {
+      // One MN-major operand over a long K loop (factor gradients: K = every b,h,w): its
+      // 4 KB [32 K][32 MN] boxes plus the in-smem transpose make the TMA producer, not the
+      // MMA, the bottleneck (measured 1.4 us per stage against 0.39 us K-major).  A single
+      // repack to the partner's K unit costs one HBM round trip of that operand.
+      const bool side_b = !st.tc.params.oa.mn_major;
+      const int partner_inner = inner_var(p, !side_b);
+      std::vector<int> order;
+      int64_t kin = 0;  // K extent that becomes contiguous (one K unit) after the repack
+      if (partner_inner >= 0 && p.cls[partner_inner] == CE_K) {
+        // the partner's shared K vars in its stride order: the chained prefix merges into
+        // one K unit in both operands
+        order = shared_k_order(p, !side_b);
+        const int64_t* ps = side_b ? p.sa : p.sb;
+        kin = 1;
+        for (std::size_t i = 0; i < order.size(); ++i) {
+          if (i > 0 && ps[order[i]] != ps[order[i - 1]] * p.ext[order[i - 1]]) break;
+          kin *= p.ext[order[i]];
+        }
+      } else {
+        order = shared_k_order(p, side_b);
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p.ext[x] > p.ext[y]; });
+        if (!order.empty()) order.resize(1);
+        kin = order.empty() ? 0 : p.ext[order[0]];
+      }
+      if (!order.empty() && kin >= 32) {
+        CeProblem q = p;
+        int64_t span = 0;
+        CeProblem pk = repack(q, side_b, order, &span, side_b ? p.sa : p.sb);
+        TcPlan t;
+        if (ce_tc_plan(q, &t) && !t.params.oa.mn_major && !t.params.ob.mn_major) {
+          Step ps;
+          ps.kind = ce_permute_supported(pk) ? Step::kPermute : Step::kDirect;
+          ps.desc = simt_desc(pk);
+          ps.a = side_b ? b : a;
+          ps.c = {BufRef::kWork, alloc(span)};
+          ps.node = node;
+          ps.label = label + (side_b ? ":packB" : ":packA");
+          ps.bytes = 8.0 * operand_elems(pk, 0);
+          (side_b ? b : a) = ps.c;
+          list.push_back(ps);
+          p = q;
+          st.tc = t;
+        }
+      }
+    }
     if (ok) {
       st.kind = Step::kTc;
       st.a = a;

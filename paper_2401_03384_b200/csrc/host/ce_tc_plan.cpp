@@ -420,6 +420,22 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
       }
     }
   }
+  for (int i = 0; i < 6; ++i)
+    for (int d = 0; d < 5; ++d) {
+      int da = P.kstep_a[i][d], db = P.kstep_b[i][d];
+      for (int v = 0; v < i; ++v) {
+        da -= (P.kcount[v] - 1) * P.kstep_a[v][d];
+        db -= (P.kcount[v] - 1) * P.kstep_b[v][d];
+      }
+      P.kdelta_a[i][d] = da;
+      P.kdelta_b[i][d] = db;
+    }
+  P.ktail_kk = 4;
+  if (P.nk >= 1 && kblock.size() == 1 && kblock[0].second == TC_BK && P.ku[0] == kblock[0].first) {
+    const int64_t ext = U[static_cast<std::size_t>(P.ku[0])].ext;
+    const int64_t rem = ext - static_cast<int64_t>(TC_BK) * (P.kcount[0] - 1);
+    P.ktail_kk = static_cast<int32_t>((rem + 7) / 8);
+  }
   // output span (for zeroing before split-K accumulation)
   int64_t span = 0;
   for (int v = 0; v < p.nv; ++v)

@@ -1,0 +1,46 @@
+"""Phase + per-iteration stamps of ONE TC launch inside a cfg2 layer's fwd+bwd (graphs off).
+usage: CE_TC_DBG=544 CE_TC_DBG_AT=<n-th TC launch> python tools/tc_phases_layer.py tk 1.0"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2401_03384_b200 as ce  # noqa: E402
+from paper_2401_03384_b200 import _lib  # noqa: E402
+from paper_2401_03384_b200.device import Context, Executor  # noqa: E402
+
+kind, cr = sys.argv[1], float(sys.argv[2])
+ctx = Context(0, "auto", graphs=False)
+torch.cuda.set_stream(ctx.torch_stream)
+slots = {"tk": 2, "tt": 3, "cp": 1, "tr": 4}[kind]
+le = ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, 128, [1] * slots), cr)
+plan = ce.optimal(le.expr, le.dims, "same", "training")
+ex = Executor(ctx, plan, backward=True)
+xs = [ctx.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
+dout = ctx.fill_random(plan.out_dims, 2000)
+ex.execute(xs)
+ex.backward(xs, dout)
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * (160 * 16))()
+_lib.lib().ce_debug_tc_timestamps(buf, 160 * 16)
+ts = np.array(buf, dtype=np.float64).reshape(160, 16)[:148]
+ts = ts[ts[:, 0] > 0]
+t0 = ts[:, 0].min()
+names = ["start", "setup", "producer_end", "mma_end", "epi_first_tile", "epi_end", "end", "first_stage", "prod_first_issue", "prod_enter", "epi_tables"]
+for i, n in enumerate(names):
+    v = (ts[:, i] - t0) / 1e3
+    v = v[v >= 0]
+    if len(v):
+        print(f"{n:16s} min {v.min():8.2f} us  median {np.median(v):8.2f} us  max {v.max():8.2f} us")
+it = (ctypes.c_ulonglong * 768)()
+_lib.lib().ce_debug_tc_iter_timestamps(it)
+a = np.array(it, dtype=np.float64).reshape(3, 256)
+if (a > 0).any():
+    base = a[a > 0].min()
+    for role, nm in enumerate(["producer", "mma", "commit"]):
+        v = a[role]
+        v = (v[v > 0] - base) / 1.9e3
+        print(nm, " ".join(f"{x:.2f}" for x in v[:60]))
