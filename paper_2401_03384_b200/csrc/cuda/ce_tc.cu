@@ -239,34 +239,37 @@ struct Tile {
 // zero fill, no store).
 __device__ __forceinline__ void decode_work(const TcParams& P, uint32_t w, uint32_t rank, uint32_t csize, Tile& T) {
   for (int i = 0; i < TC_MAX_UNITS; ++i) T.val[i] = 0;
-  const uint32_t pm = (static_cast<uint32_t>(P.tiles_m) + csize - 1) / csize;
-  uint32_t m = (w % pm) * csize + rank;
-  uint32_t t = w / pm;
-  T.ntile = static_cast<int>(t % static_cast<uint32_t>(P.tiles_n));
+  uint32_t t = tc_quo(w, P.dpm);
+  uint32_t m = (w - t * P.dpm.d) * csize + rank;
+  const uint32_t tn = tc_quo(t, P.dtn);
+  T.ntile = static_cast<int>(t - tn * P.dtn.d);
   for (int i = 0; i < P.nm; ++i) {
     const TcUnit& u = P.u[P.mt[i]];
-    const uint32_t n = static_cast<uint32_t>((u.ext + u.box - 1) / u.box);
-    const uint32_t digit = (i + 1 == P.nm) ? m : m % n;
-    T.val[P.mt[i]] = static_cast<int32_t>(digit) * u.box;
-    m /= n;
+    if (i + 1 == P.nm) {
+      T.val[P.mt[i]] = static_cast<int32_t>(m) * u.box;
+    } else {
+      const uint32_t q = tc_quo(m, u.dtiles);
+      T.val[P.mt[i]] = static_cast<int32_t>(m - q * u.dtiles.d) * u.box;
+      m = q;
+    }
   }
   for (int i = 0; i < P.nn; ++i) {
     const TcUnit& u = P.u[P.nt[i]];
-    const uint32_t n = static_cast<uint32_t>((u.ext + u.box - 1) / u.box);
-    T.val[P.nt[i]] = static_cast<int32_t>(t % n) * u.box;
-    t /= n;
+    const uint32_t q = tc_quo(t, u.dtiles);
+    T.val[P.nt[i]] = static_cast<int32_t>(t - q * u.dtiles.d) * u.box;
+    t = q;
   }
   for (int i = 0; i < P.ng; ++i) {
     const TcUnit& u = P.u[P.gu[i]];
-    T.val[P.gu[i]] = static_cast<int32_t>(t % static_cast<uint32_t>(u.ext));
-    t /= static_cast<uint32_t>(u.ext);
+    const uint32_t q = tc_quo(t, u.dext);
+    T.val[P.gu[i]] = static_cast<int32_t>(t - q * u.dext.d);
+    t = q;
   }
   T.split = static_cast<int>(t);
 }
 
-__device__ __forceinline__ int work_split(const TcParams& P, uint32_t w, uint32_t csize) {
-  const uint32_t pm = (static_cast<uint32_t>(P.tiles_m) + csize - 1) / csize;
-  return static_cast<int>(w / (pm * static_cast<uint32_t>(P.tiles_n) * static_cast<uint32_t>(P.grid_z)));
+__device__ __forceinline__ int work_split(const TcParams& P, uint32_t w, uint32_t /*csize*/) {
+  return static_cast<int>(tc_quo(w, P.dsplit));
 }
 
 __device__ __forceinline__ void coords(const TcOperand& o, const int32_t* val, int c[5]) {
@@ -287,22 +290,23 @@ __device__ __forceinline__ int64_t tile_offset(const TcParams& P, const int32_t*
   uint32_t rest = static_cast<uint32_t>(local);
   for (int i = 0; i < n; ++i) {
     const TcUnit& u = P.u[list[i]];
-    const uint32_t d = rest % static_cast<uint32_t>(u.box);
-    rest /= static_cast<uint32_t>(u.box);
+    const uint32_t q = tc_quo(rest, u.dbox);
+    const uint32_t d = rest - q * u.dbox.d;
+    rest = q;
     uint32_t v = static_cast<uint32_t>(val[list[i]]) + d;
     if (v >= static_cast<uint32_t>(u.ext)) return -1;
     for (int k = 0; k < u.nv; ++k) {
-      off += static_cast<int64_t>(v % static_cast<uint32_t>(u.vext[k])) * u.sc[k];
-      v /= static_cast<uint32_t>(u.vext[k]);
+      const uint32_t vq = tc_quo(v, u.dvext[k]);
+      off += static_cast<int64_t>(v - vq * u.dvext[k].d) * u.sc[k];
+      v = vq;
     }
   }
   return rest == 0 ? off : -1;
 }
 
 __device__ __forceinline__ void k_range(const TcParams& P, int split, int& k0, int& k1) {
-  const int per = (P.k_iters + P.k_split - 1) / P.k_split;
-  k0 = split * per;
-  k1 = min(P.k_iters, k0 + per);
+  k0 = split * P.k_per;
+  k1 = min(P.k_iters, k0 + P.k_per);
 }
 
 // PAIR: CTA pair (cluster of 2) running M=256 tcgen05.mma.cta_group::2 issued by the even
@@ -628,8 +632,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
         const TcUnit& u = P.u[P.gu[i]];
         uint32_t v = static_cast<uint32_t>(T.val[P.gu[i]]);
         for (int k = 0; k < u.nv; ++k) {
-          base += static_cast<int64_t>(v % static_cast<uint32_t>(u.vext[k])) * u.sc[k];
-          v /= static_cast<uint32_t>(u.vext[k]);
+          const uint32_t vq = tc_quo(v, u.dvext[k]);
+          base += static_cast<int64_t>(v - vq * u.dvext[k].d) * u.sc[k];
+          v = vq;
         }
       }
       // column tables depend only on the N tile: most launches have a single N tile, so they

@@ -26,6 +26,30 @@
 
 enum TcSrc { TC_SRC_MTILE = 0, TC_SRC_NTILE = 1, TC_SRC_GRID = 2, TC_SRC_K = 3 };
 
+// Unsigned division by a launch constant d >= 1 as a multiply-high and shift (exact for
+// dividends below 2^31): the per-tile index decoding would otherwise be ~20 dependent
+// integer divisions on the start-up path of every role.
+struct TcDiv {
+  uint32_t d, mul, shr;
+};
+
+inline TcDiv tc_div(uint32_t d) {
+  TcDiv r{d, 0, 0};
+  if (d <= 1) return r;
+  int l = 0;
+  while ((1ull << l) < d) ++l;  // ceil(log2 d)
+  const int p = 31 + l;
+  r.mul = static_cast<uint32_t>(((1ull << p) + d - 1) / d);
+  r.shr = static_cast<uint32_t>(p - 32);
+  return r;
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t tc_quo(uint32_t x, const TcDiv& v) {
+  return v.d == 1 ? x : (__umulhi(x, v.mul) >> v.shr);
+}
+#endif
+
 struct TcUnit {
   int32_t ext;    // extent (product of member var extents)
   int32_t box;    // tile/block extent along this unit (1 for grid / loop units)
@@ -33,6 +57,7 @@ struct TcUnit {
   int32_t nv;     // member vars, innermost first
   int32_t vext[4];
   int64_t sc[4];  // out stride of each member var (0 for K units)
+  TcDiv dbox, dtiles, dext, dvext[4];  // fast division by box, ceil(ext/box), ext, vext[k]
 };
 
 struct TcDim {    // one TMA coordinate
@@ -76,6 +101,10 @@ struct TcParams {
   // MMAs (of K=8) issued for the last chunk of K digit 0 when it is the 32-wide K block of a
   // single unit whose extent is not a multiple of 32 (its tail rows are TMA zero fill); else 4
   int32_t ktail_kk;
+  TcDiv dpm;       // ceil(tiles_m / cluster size): M tiles are dealt per work group
+  TcDiv dtn;       // tiles_n
+  TcDiv dsplit;    // pm * tiles_n * grid_z: work items per K split
+  int32_t k_per;   // K iterations per split
   // 2-CTA cluster along M: each CTA TMA-loads mc_half rows of the B tile and multicasts
   // them to both CTAs (B is read from L2 once per CTA pair instead of once per CTA)
   int32_t mcast;           // 1: launched with cluster dims (2,1,1)

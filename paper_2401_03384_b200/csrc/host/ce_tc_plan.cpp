@@ -518,6 +518,23 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     if (gz * split > 65535) return fail("grid z too large");
     P.k_split = split;
   }
+  // fast-division constants for the per-tile index decoding (ce_tc.h TcDiv)
+  for (int i = 0; i < P.nunits; ++i) {
+    TcUnit& u = P.u[i];
+    u.dbox = tc_div(static_cast<uint32_t>(u.box));
+    u.dtiles = tc_div(static_cast<uint32_t>((u.ext + u.box - 1) / u.box));
+    u.dext = tc_div(static_cast<uint32_t>(u.ext));
+    for (int k = 0; k < 4; ++k) u.dvext[k] = tc_div(k < u.nv ? static_cast<uint32_t>(u.vext[k]) : 1u);
+  }
+  {
+    const int64_t csize = P.mcast ? 2 : 1;
+    const int64_t pm = (P.tiles_m + csize - 1) / csize;
+    P.dpm = tc_div(static_cast<uint32_t>(pm));
+    P.dtn = tc_div(static_cast<uint32_t>(P.tiles_n));
+    P.dsplit = tc_div(static_cast<uint32_t>(pm * P.tiles_n * P.grid_z));
+    P.k_per = (P.k_iters + P.k_split - 1) / P.k_split;
+    if (pm * P.tiles_n * P.grid_z * P.k_split >= (1ll << 31)) return fail("too many work items");
+  }
   plan->valid = 1;
   plan->why = "ok";
   return true;
