@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -268,8 +269,23 @@ __device__ __forceinline__ void decode_work(const TcParams& P, uint32_t w, uint3
   T.split = static_cast<int>(t);
 }
 
-__device__ __forceinline__ int work_split(const TcParams& P, uint32_t w, uint32_t /*csize*/) {
-  return static_cast<int>(tc_quo(w, P.dsplit));
+// Work item w -> index in the full decomposition (tiles x K splits) and its K range.
+__device__ __forceinline__ uint32_t work_item(const TcParams& P, uint32_t w, int& k0, int& k1) {
+  if (P.tail_s == 0 || w < static_cast<uint32_t>(P.tail_base)) {
+    const int split = static_cast<int>(tc_quo(w, P.dsplit));
+    k0 = split * P.k_per;
+    k1 = min(P.k_iters, k0 + P.k_per);
+    return w;
+  }
+  const uint32_t j = w - static_cast<uint32_t>(P.tail_base);
+  const uint32_t sl = tc_quo(j, P.dtail_r);
+  k0 = static_cast<int>(sl) * P.tail_per;
+  k1 = min(P.k_iters, k0 + P.tail_per);
+  return static_cast<uint32_t>(P.tail_base) + (j - sl * P.dtail_r.d);
+}
+
+__device__ __forceinline__ bool work_atomic(const TcParams& P, uint32_t w) {
+  return P.k_split > 1 || (P.tail_s > 0 && w >= static_cast<uint32_t>(P.tail_base));
 }
 
 __device__ __forceinline__ void coords(const TcOperand& o, const int32_t* val, int c[5]) {
@@ -302,11 +318,6 @@ __device__ __forceinline__ int64_t tile_offset(const TcParams& P, const int32_t*
     }
   }
   return rest == 0 ? off : -1;
-}
-
-__device__ __forceinline__ void k_range(const TcParams& P, int split, int& k0, int& k1) {
-  k0 = split * P.k_per;
-  k1 = min(P.k_iters, k0 + P.k_per);
 }
 
 // PAIR: CTA pair (cluster of 2) running M=256 tcgen05.mma.cta_group::2 issued by the even
@@ -354,7 +365,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) stamp(Pg, 0);
-  const uint32_t n_work = (static_cast<uint32_t>(Pg.tiles_m) + csize - 1) / csize * static_cast<uint32_t>(Pg.tiles_n) *
+  const uint32_t n_work =
+      Pg.tail_s > 0 ? static_cast<uint32_t>(Pg.tail_base + Pg.tail_r * Pg.tail_s)
+                    : (static_cast<uint32_t>(Pg.tiles_m) + csize - 1) / csize * static_cast<uint32_t>(Pg.tiles_n) *
                           static_cast<uint32_t>(Pg.grid_z) * static_cast<uint32_t>(Pg.k_split);
 
   if (threadIdx.x == 0) {
@@ -419,9 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       Tile& T = tiles[0];
       if (dbg & 32) stamp(P, 9);  // producer entered (after griddepcontrol.wait)
       for (uint32_t w = group; w < n_work; w += ngroups) {
-        decode_work(P, w, rank, csize, T);
         int k0, k1;
-        k_range(P, T.split, k0, k1);
+        decode_work(P, work_item(P, w, k0, k1), rank, csize, T);
         int ca[5], cb[5], dig[6];
         coords(P.oa, T.val, ca);
         coords(P.ob, T.val, cb);
@@ -523,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       for (uint32_t w = group; w < n_work; w += ngroups, ++local) {
         const int acc = static_cast<int>(local & 1);
         int k0, k1;
-        k_range(P, work_split(P, w, csize), k0, k1);
+        work_item(P, w, k0, k1);
         int d0 = k0 % kc0;  // K digit 0 of the first iteration (for the K tail)
         if (PAIR)
           mbar_wait_cluster(&tempty[acc], ((local >> 1) & 1) ^ 1);  // both epilogues drained it
@@ -581,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       uint32_t gi = 0;
       for (uint32_t w = group; w < n_work; w += ngroups) {
         int k0, k1;
-        k_range(P, work_split(P, w, csize), k0, k1);
+        work_item(P, w, k0, k1);
         for (int it = k0; it < k1; ++it, ++gi) {
           const int s = static_cast<int>(gi % STAGES);
           mbar_wait(&full[s], (gi / STAGES) & 1);
@@ -609,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     const int ew = warp - 2;           // 0..3
     const int et = threadIdx.x - 64;   // 0..127
     float* stage = stage_out + ew * 32 * kStagePitch;
-    const bool atomic = P.k_split > 1;
+
     const int dbg = Pg.dbg;
     const int n_cols = P.n_cols, m_rows = P.m_rows;
     const bool tstore = P.transpose_store != 0;
@@ -619,10 +631,11 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     int cols_for[2] = {-1, -1};  // N tile whose column tables each accumulator buffer holds
     for (uint32_t w = group; w < n_work; w += ngroups, ++local) {
       const int acc = static_cast<int>(local & 1);
-      if (et == 0) decode_work(P, w, rank, csize, T);
-      epi_bar();  // decoded tile visible (and the previous tile's tables are no longer read)
       int k0, k1;
-      k_range(P, T.split, k0, k1);
+      const uint32_t wf = work_item(P, w, k0, k1);
+      const bool atomic = work_atomic(P, w);
+      if (et == 0) decode_work(P, wf, rank, csize, T);
+      epi_bar();  // decoded tile visible (and the previous tile's tables are no longer read)
       // address tables for this tile (overlaps the MMAs)
       int64_t* cols = col_off + acc * BN;
       int64_t* gcol = grp_off + acc * (BN / 4);
@@ -842,6 +855,7 @@ cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
   const int64_t groups = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
   const int64_t max_groups = sm_count() / csize;
   const int grid = static_cast<int>((groups < max_groups ? groups : max_groups) * csize);
+  (void)grid;
   return ce_launch_cluster(ce_tc_kernel<BN, STAGES, PAIR>, dim3(grid), dim3(kThreads), smem, s,
                            static_cast<unsigned>(csize),
                            P, C);
@@ -881,7 +895,31 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
   }
   if (static_cast<int64_t>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_split >= (1ll << 32))
     return cudaErrorInvalidConfiguration;
-  if (P.k_split > 1) {
+  {
+    // tail split of a partial last round (see TcParams::tail_s)
+    const int64_t csize = P.mcast ? 2 : 1;
+    const int64_t groups = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
+    const int64_t ngroups = std::min<int64_t>(groups, sm_count() / csize);
+    P.tail_s = 0;
+    static const bool tail_on = [] {
+      const char* e = getenv("CE_TC_TAIL");
+      return !(e && *e == '0');
+    }();
+    // only for mainloop-dominated items: a short K loop is cheaper than the memset and the
+    // atomic epilogue the split needs (measured: 8-iteration GEMMs got 2x slower)
+    if (tail_on && P.k_split == 1 && groups > ngroups && P.k_iters >= 48) {
+      const int64_t r = groups % ngroups;
+      const int64_t sl = r > 0 ? std::min<int64_t>(ngroups / r, P.k_iters / 2) : 0;
+      if (r > 0 && 4 * r <= 3 * ngroups && sl >= 2) {
+        P.tail_base = static_cast<int32_t>(groups - r);
+        P.tail_r = static_cast<int32_t>(r);
+        P.tail_s = static_cast<int32_t>(sl);
+        P.tail_per = static_cast<int32_t>((P.k_iters + sl - 1) / sl);
+        P.dtail_r = tc_div(static_cast<uint32_t>(r));
+      }
+    }
+  }
+  if (P.k_split > 1 || P.tail_s > 0) {
     cudaError_t e = cudaMemsetAsync(C, 0, static_cast<size_t>(plan.out_span) * 4, s);
     if (e != cudaSuccess) return e;
   }

@@ -9,7 +9,7 @@ import paper_2401_03384_b200 as ce  # noqa: E402
 from paper_2401_03384_b200.device import Context, Executor  # noqa: E402
 
 kind, cr = sys.argv[1], float(sys.argv[2])
-ctx = Context(0, "auto")
+ctx = Context(0, os.environ.get("MATH", "auto"))
 torch.cuda.set_stream(ctx.torch_stream)
 slots = {"tk": 2, "tt": 3, "cp": 1, "tr": 4}[kind]
 le = ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, 128, [1] * slots), cr)
