@@ -333,17 +333,26 @@ def main():
     total_k = sum(k[2] for k in kern)
     top = max(kern, key=lambda k: k[2])
     name, kind, t_ms, fl, by = top
+    # DRAM traffic per launch of that kernel from the committed `ncu --set full` captures
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")) as f:
+            tj = json.load(f)
+        if name in tj.get("kernels", {}):
+            traffic = tj["kernels"][name]["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
     if kind == "tc":
         ach = fl / (t_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": tf32_peak, "unit": "TFLOP/s",
-                "frac": round(ach / tf32_peak, 4), "traffic": None,
+                "frac": round(ach / tf32_peak, 4), "traffic": traffic,
                 "kernel": name, "share_of_step": round(t_ms / total_k, 3),
                 "peak_note": f"TF32 dense = bf16_tflops/2 of {peak_kind} ({bf16} TF)",
                 "hbm_frac": round(by / (t_ms * 1e-3) / 1e9 / hbm, 4)}
     else:
         ach = by / (t_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(ach / hbm, 4), "traffic": None, "kernel": name,
+                "frac": round(ach / hbm, 4), "traffic": traffic, "kernel": name,
                 "share_of_step": round(t_ms / total_k, 3), "peak_note": f"{peak_kind} copy bandwidth"}
     if args.profile_json and rank == 0:
         with open(args.profile_json, "w") as f:

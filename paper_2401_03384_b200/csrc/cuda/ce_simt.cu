@@ -12,13 +12,24 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <vector>
 #include <cstdio>
 
 #include "ce_device.h"
 #include "ce_kernels.h"
 #include "ce_launch.h"
+#include "ce_tc.h"  // TcDiv fast division
 
 namespace {
+
+bool simt_stream_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CE_SIMT_STREAM");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
 
 __device__ __forceinline__ bool gather_index(const CeGather& g, int64_t p, int64_t q, int64_t* off) {
   int64_t x = g.sp * p + g.sq * q + g.c;
@@ -147,6 +158,326 @@ __global__ void __launch_bounds__(256) ce_reduce_kernel(const CeSimtDesc d, cons
         C[offC] = acc;
     }
   }
+}
+
+
+// ----------------------------------------------------------------------------- stream
+// Streaming SIMT kernel for small-K steps (depthwise / batch-only convolutions, Hadamard
+// and outer products, unary sums and broadcasts) and few-output long-K reductions (the
+// depthwise filter gradients): one thread per output element and K slice, with all index
+// state in 32-bit registers.  The host orders the output vars so that the lane var is
+// unit-stride in the streamed operand (coalesced 128-B warp accesses), replaces every
+// division by a multiply-shift (TcDiv) and rewrites each gathered (convolution) index
+// idx = sp*p + sq*q + c as an affine function of the output and K var values that the
+// K odometer updates incrementally.  A K slice > 1 accumulates with atomics into C.
+constexpr int SV_O = 8, SV_K = 6, SV_G = 2;
+struct SvDesc {
+  int32_t nout, nk, nga, ngb, unary, mode;  // mode 0 store, 1 accumulate, 2 atomic
+  int32_t vec, vec_b, vec_c;                // VEC=4 path (see ce_stream_kernel)
+  int32_t lext;                             // lane var extent (VEC=4: the last group may be partial)
+  int32_t oext[SV_O];
+  TcDiv odiv[SV_O];
+  int32_t osa[SV_O], osb[SV_O], osc[SV_O];
+  int32_t kext[SV_K];
+  TcDiv kdiv[SV_K];
+  int32_t ksa[SV_K], ksb[SV_K];
+  // gathers: g < nga on A, then g < ngb on B
+  int32_t gc[2 * SV_G], gext[2 * SV_G], gstride[2 * SV_G], gwrap[2 * SV_G];
+  int32_t go[2 * SV_G][SV_O];  // coefficient of output slot i in the gathered index
+  int32_t gk[2 * SV_G][SV_K];  // coefficient of K slot j
+  uint32_t outs, K, kper;
+};
+
+__device__ __forceinline__ int32_t sv_mod(int32_t x, int32_t e) {
+  const int32_t r = x % e;
+  return r < 0 ? r + e : r;
+}
+
+// VEC = 4: each thread owns 4 consecutive values of the lane var (slot 0, unit stride and
+// 16-B aligned in A, never gathered), loading A as float4; B and C use float4 when they
+// are unit-stride along the lane var too (flags set by the host), else 4 scalars.
+template <int VEC>
+__global__ void __launch_bounds__(256) ce_stream_kernel(const SvDesc d, const float* __restrict__ A,
+                                                        const float* __restrict__ B, float* __restrict__ C) {
+  ce_pdl_enter();
+  const uint32_t o = blockIdx.x * 256u + threadIdx.x;
+  if (o >= d.outs) return;  // outs counts threads (lane var divided by VEC)
+  int32_t offA = 0, offB = 0, offC = 0, lane0 = 0;
+  int32_t gidx[2 * SV_G];
+#pragma unroll
+  for (int g = 0; g < 2 * SV_G; ++g) gidx[g] = d.gc[g];
+  uint32_t rest = o;
+#pragma unroll
+  for (int i = 0; i < SV_O; ++i) {
+    if (i < d.nout) {
+      const uint32_t q = tc_quo(rest, d.odiv[i]);
+      int32_t v = static_cast<int32_t>(rest - q * static_cast<uint32_t>(d.oext[i]));
+      rest = q;
+      if (i == 0) {
+        v *= VEC;
+        lane0 = v;
+      }
+      offA += v * d.osa[i];
+      offB += v * d.osb[i];
+      offC += v * d.osc[i];
+#pragma unroll
+      for (int g = 0; g < 2 * SV_G; ++g) gidx[g] += v * d.go[g][i];
+    }
+  }
+  const uint32_t k0 = blockIdx.y * d.kper;
+  const uint32_t k1 = min(d.K, k0 + d.kper);
+  int32_t kv[SV_K];
+  rest = k0;
+#pragma unroll
+  for (int j = 0; j < SV_K; ++j) {
+    kv[j] = 0;
+    if (j < d.nk) {
+      const uint32_t q = tc_quo(rest, d.kdiv[j]);
+      kv[j] = static_cast<int32_t>(rest - q * static_cast<uint32_t>(d.kext[j]));
+      rest = q;
+      offA += kv[j] * d.ksa[j];
+      offB += kv[j] * d.ksb[j];
+#pragma unroll
+      for (int g = 0; g < 2 * SV_G; ++g) gidx[g] += kv[j] * d.gk[g][j];
+    }
+  }
+  float acc[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
+  const int32_t sb0 = d.osb[0];
+  for (uint32_t k = k0; k < k1; ++k) {
+    int32_t a = offA, b = offB;
+    bool ok = true;
+#pragma unroll
+    for (int g = 0; g < SV_G; ++g) {
+      if (g < d.nga) {
+        int32_t x = gidx[g];
+        if (d.gwrap[g]) x = sv_mod(x, d.gext[g]);
+        ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[g]);
+        a += x * d.gstride[g];
+      }
+      if (g < d.ngb) {
+        int32_t x = gidx[SV_G + g];
+        if (d.gwrap[SV_G + g]) x = sv_mod(x, d.gext[SV_G + g]);
+        ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[SV_G + g]);
+        b += x * d.gstride[SV_G + g];
+      }
+    }
+    if (ok) {
+      if (VEC == 1) {
+        acc[0] += d.unary ? __ldg(A + a) : __ldg(A + a) * __ldg(B + b);
+      } else {
+        const float4 va = __ldg(reinterpret_cast<const float4*>(A + a));
+        const float xa[4] = {va.x, va.y, va.z, va.w};
+        if (d.unary) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[e] += xa[e];
+        } else if (d.vec_b) {
+          const float4 vb = __ldg(reinterpret_cast<const float4*>(B + b));
+          acc[0] += xa[0] * vb.x;
+          acc[1] += xa[1] * vb.y;
+          acc[2] += xa[2] * vb.z;
+          acc[3] += xa[3] * vb.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e)
+            if (lane0 + e < d.lext) acc[e] += xa[e] * __ldg(B + b + e * sb0);
+        }
+      }
+    }
+    // K odometer (slot 0 fastest); the gathered indices move with it
+#pragma unroll
+    for (int j = 0; j < SV_K; ++j) {
+      if (j < d.nk) {
+        if (++kv[j] < d.kext[j]) {
+          offA += d.ksa[j];
+          offB += d.ksb[j];
+#pragma unroll
+          for (int g = 0; g < 2 * SV_G; ++g) gidx[g] += d.gk[g][j];
+          break;
+        }
+        const int32_t back = d.kext[j] - 1;
+        offA -= back * d.ksa[j];
+        offB -= back * d.ksb[j];
+#pragma unroll
+        for (int g = 0; g < 2 * SV_G; ++g) gidx[g] -= back * d.gk[g][j];
+        kv[j] = 0;
+      }
+    }
+  }
+  if (VEC == 4 && d.vec_c) {
+    float4* cp = reinterpret_cast<float4*>(C + offC);
+    const float4 v = make_float4(acc[0], acc[1], acc[2], acc[VEC - 1]);
+    if (d.mode == 2) {
+      asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(cp), "f"(v.x), "f"(v.y),
+                   "f"(v.z), "f"(v.w)
+                   : "memory");
+    } else if (d.mode == 1) {
+      float4 c = *cp;
+      c.x += v.x;
+      c.y += v.y;
+      c.z += v.z;
+      c.w += v.w;
+      *cp = c;
+    } else {
+      *cp = v;
+    }
+  } else {
+    const int32_t sc0 = d.osc[0];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      if (VEC > 1 && lane0 + e >= d.lext) break;
+      float* cp = C + offC + e * sc0;
+      if (d.mode == 2)
+        atomicAdd(cp, acc[e]);
+      else if (d.mode == 1)
+        *cp += acc[e];
+      else
+        *cp = acc[e];
+    }
+  }
+}
+
+// Builds the stream descriptor; false when the problem exceeds its limits (then the
+// int64 reference kernels run).  *span = elements of C an atomic reduction must zero.
+bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float* C, SvDesc* out, int64_t* span) {
+  const CeProblem& p = sd.p;
+  SvDesc d{};
+  if (p.ng_a > SV_G || p.ng_b > SV_G) return false;
+  // output vars: the lane var (unit stride in the operand that streams, else in C) first,
+  // then by ascending out stride
+  std::vector<int> ov(sd.ov, sd.ov + sd.nout);
+  std::vector<int> kvars(sd.kv, sd.kv + sd.nk);
+  ov.erase(std::remove_if(ov.begin(), ov.end(), [&](int v) { return p.ext[v] == 1; }), ov.end());
+  kvars.erase(std::remove_if(kvars.begin(), kvars.end(), [&](int v) { return p.ext[v] == 1; }), kvars.end());
+  if (static_cast<int>(ov.size()) > SV_O || static_cast<int>(kvars.size()) > SV_K) return false;
+  auto astride = [&](int v) -> int64_t {
+    if (p.sa[v]) return p.sa[v];
+    for (int g = 0; g < p.ng_a; ++g)
+      if (p.ga[g].pv == v || p.ga[g].qv == v) return p.ga[g].stride;
+    return 0;
+  };
+  int lane = -1;
+  for (int v : ov)
+    if (astride(v) == 1) lane = v;
+  if (lane < 0)
+    for (int v : ov)
+      if (p.sc[v] == 1) lane = v;
+  if (lane >= 0) {
+    ov.erase(std::find(ov.begin(), ov.end(), lane));
+    ov.insert(ov.begin(), lane);
+  }
+  // K vars: fastest in A first
+  std::stable_sort(kvars.begin(), kvars.end(), [&](int x, int y) {
+    const int64_t sx = astride(x) ? astride(x) : p.sb[x], sy = astride(y) ? astride(y) : p.sb[y];
+    return sx < sy;
+  });
+  int64_t outs = 1, K = 1, maxA = 0, maxB = 0, maxC = 0;
+  d.nout = static_cast<int32_t>(ov.size());
+  d.nk = static_cast<int32_t>(kvars.size());
+  for (int i = 0; i < d.nout; ++i) {
+    const int v = ov[static_cast<std::size_t>(i)];
+    d.oext[i] = static_cast<int32_t>(p.ext[v]);
+    d.odiv[i] = tc_div(static_cast<uint32_t>(p.ext[v]));
+    d.osa[i] = static_cast<int32_t>(p.sa[v]);
+    d.osb[i] = static_cast<int32_t>(p.sb[v]);
+    d.osc[i] = static_cast<int32_t>(p.sc[v]);
+    outs *= p.ext[v];
+    maxA += (p.ext[v] - 1) * p.sa[v];
+    maxB += (p.ext[v] - 1) * p.sb[v];
+    maxC += (p.ext[v] - 1) * p.sc[v];
+  }
+  for (int j = 0; j < d.nk; ++j) {
+    const int v = kvars[static_cast<std::size_t>(j)];
+    d.kext[j] = static_cast<int32_t>(p.ext[v]);
+    d.kdiv[j] = tc_div(static_cast<uint32_t>(p.ext[v]));
+    d.ksa[j] = static_cast<int32_t>(p.sa[v]);
+    d.ksb[j] = static_cast<int32_t>(p.sb[v]);
+    K *= p.ext[v];
+    maxA += (p.ext[v] - 1) * p.sa[v];
+    maxB += (p.ext[v] - 1) * p.sb[v];
+  }
+  for (int side = 0; side < 2; ++side) {
+    const int ng = side ? p.ng_b : p.ng_a;
+    const CeGather* gs = side ? p.gb : p.ga;
+    for (int g = 0; g < ng; ++g) {
+      const int slot = side * SV_G + g;
+      const CeGather& G = gs[g];
+      if (G.extent >= (1ll << 30) || std::llabs(G.c) >= (1ll << 30)) return false;
+      d.gc[slot] = static_cast<int32_t>(G.c);
+      d.gext[slot] = static_cast<int32_t>(G.extent);
+      d.gstride[slot] = static_cast<int32_t>(G.stride);
+      d.gwrap[slot] = G.wrap;
+      for (int i = 0; i < d.nout; ++i) {
+        const int v = ov[static_cast<std::size_t>(i)];
+        d.go[slot][i] = (G.pv == v ? G.sp : 0) + (G.qv == v ? G.sq : 0);
+      }
+      for (int j = 0; j < d.nk; ++j) {
+        const int v = kvars[static_cast<std::size_t>(j)];
+        d.gk[slot][j] = (G.pv == v ? G.sp : 0) + (G.qv == v ? G.sq : 0);
+      }
+      (side ? maxB : maxA) += (G.extent - 1) * G.stride;
+    }
+  }
+  d.nga = p.ng_a;
+  d.ngb = p.ng_b;
+  d.unary = p.unary;
+  // VEC=4 along the lane var: unit stride and 16-B aligned A, lane var never gathered
+  {
+    // a lane extent that is not a multiple of 4 needs a row pitch of >= round_up(ext, 4) in
+    // A (the last float4 reads the row's padding) and masks B loads / C stores past it
+    auto al = [](const float* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+    const int32_t ext0 = d.nout >= 1 ? d.oext[0] : 0, ext4 = (ext0 + 3) / 4 * 4;
+    auto padded = [&](const int32_t* os, const int32_t* ks, int gbase, int ng) {
+      for (int i = 1; i < d.nout; ++i)
+        if (os[i] % 4 || (os[i] && os[i] < ext4)) return false;
+      for (int j = 0; j < d.nk; ++j)
+        if (ks && (ks[j] % 4 || (ks[j] && ks[j] < ext4))) return false;
+      for (int g = 0; g < ng; ++g)
+        if (d.gstride[gbase + g] % 4 || d.gstride[gbase + g] < ext4) return false;
+      return true;
+    };
+    bool ok = al(A) && d.nout >= 1 && d.osa[0] == 1 && padded(d.osa, d.ksa, 0, p.ng_a);
+    for (int g = 0; g < 2 * SV_G && ok; ++g) ok = d.go[g][0] == 0;
+    d.vec = ok ? 1 : 0;
+    if (ok) {
+      const bool vb = !p.unary && al(B) && d.osb[0] == 1 && padded(d.osb, d.ksb, SV_G, p.ng_b);
+      const bool vc = al(C) && d.osc[0] == 1 && padded(d.osc, nullptr, 0, 0);
+      d.vec_b = vb ? 1 : 0;
+      d.vec_c = vc ? 1 : 0;
+      d.lext = ext0;
+      d.oext[0] = ext4 / 4;  // the kernel decomposes threads, each owning 4 lane values
+      d.odiv[0] = tc_div(static_cast<uint32_t>(d.oext[0]));
+      outs = outs / ext0 * d.oext[0];
+    }
+  }
+  const int64_t lim = (1ll << 31) - 1;
+  if (outs > lim || K > lim || maxA > lim || maxB > lim || maxC > lim) return false;
+  d.outs = static_cast<uint32_t>(outs);
+  d.K = static_cast<uint32_t>(K);
+  // K slices: enough CTAs for ~8 per SM when the outputs alone do not fill the GPU,
+  // each thread keeping >= 32 K terms
+  const int64_t blocks = (outs + 255) / 256;
+  int64_t split = 1;
+  if (blocks < 148 * 8 && K >= 64) split = std::min<int64_t>((148 * 8 + blocks - 1) / blocks, K / 32);
+  split = std::max<int64_t>(1, std::min<int64_t>(split, 65535));
+  d.kper = static_cast<uint32_t>((K + split - 1) / split);
+  d.mode = split > 1 ? 2 : (p.accumulate ? 1 : 0);
+  *span = maxC + 1;
+  *out = d;
+  return true;
+}
+
+cudaError_t sv_launch(const SvDesc& d, int64_t span, bool zero_first, const float* A, const float* B, float* C,
+                      cudaStream_t s) {
+  if (d.outs == 0) return cudaSuccess;
+  if (zero_first) {
+    cudaError_t e = cudaMemsetAsync(C, 0, static_cast<size_t>(span) * 4, s);
+    if (e != cudaSuccess) return e;
+  }
+  const unsigned gx = (d.outs + 255u) / 256u, gy = d.K ? (d.K + d.kper - 1) / d.kper : 1u;
+  if (d.vec) return ce_launch(ce_stream_kernel<4>, dim3(gx, gy), dim3(256), 0, s, d, A, B, C);
+  return ce_launch(ce_stream_kernel<1>, dim3(gx, gy), dim3(256), 0, s, d, A, B, C);
 }
 
 // ----------------------------------------------------------------------------- tiled
@@ -547,6 +878,10 @@ int grid_for(int64_t work, int threads) {
 cudaError_t ce_launch_direct(const CeSimtDesc& d, const float* A, const float* B, float* C, cudaStream_t s) {
   const int64_t total = d.Z * d.M * d.N;
   if (total == 0) return cudaSuccess;
+  SvDesc sv;
+  int64_t span = 0;
+  if (simt_stream_enabled() && sv_build(d, A, B, C, &sv, &span))
+    return sv_launch(sv, span, sv.mode == 2 && !d.p.accumulate, A, B, C, s);
   return ce_launch(ce_direct_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, d, A, B, C);
 }
 
@@ -554,6 +889,10 @@ cudaError_t ce_launch_reduce(const CeSimtDesc& d, const float* A, const float* B
                              cudaStream_t s) {
   const int64_t outs = d.Z * d.M * d.N;
   if (outs == 0) return cudaSuccess;
+  SvDesc sv;
+  int64_t span = 0;
+  if (simt_stream_enabled() && sv_build(d, A, B, C, &sv, &span))
+    return sv_launch(sv, span, sv.mode == 2 && !d.p.accumulate, A, B, C, s);
   // enough CTAs for ~4 waves, each thread doing >= 8 terms
   int64_t split = (148 * 4 + outs - 1) / outs;
   split = std::max<int64_t>(1, std::min<int64_t>(split, d.K / (256 * 8)));
