@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <numeric>
 #include <cstdlib>
 #include <vector>
 #include <cstdio>
@@ -175,6 +176,8 @@ struct SvDesc {
   int32_t nout, nk, nga, ngb, unary, mode;  // mode 0 store, 1 accumulate, 2 atomic
   int32_t vec, vec_b, vec_c;                // VEC=4 path (see ce_stream_kernel)
   int32_t lext;                             // lane var extent (VEC=4: the last group may be partial)
+  int32_t klane;                            // 1: warp per output, lanes along K
+  int32_t a_bcast;                          // VEC=4 with A independent of the lane var
   int32_t oext[SV_O];
   TcDiv odiv[SV_O];
   int32_t osa[SV_O], osb[SV_O], osc[SV_O];
@@ -267,8 +270,16 @@ __global__ void __launch_bounds__(256) ce_stream_kernel(const SvDesc d, const fl
       if (VEC == 1) {
         acc[0] += d.unary ? __ldg(A + a) : __ldg(A + a) * __ldg(B + b);
       } else {
-        const float4 va = __ldg(reinterpret_cast<const float4*>(A + a));
-        const float xa[4] = {va.x, va.y, va.z, va.w};
+        float xa[4];
+        if (d.a_bcast) {
+          xa[0] = xa[1] = xa[2] = xa[3] = __ldg(A + a);
+        } else {
+          const float4 va = __ldg(reinterpret_cast<const float4*>(A + a));
+          xa[0] = va.x;
+          xa[1] = va.y;
+          xa[2] = va.z;
+          xa[3] = va.w;
+        }
         if (d.unary) {
 #pragma unroll
           for (int e = 0; e < VEC; ++e) acc[e] += xa[e];
@@ -338,10 +349,112 @@ __global__ void __launch_bounds__(256) ce_stream_kernel(const SvDesc d, const fl
   }
 }
 
+
+// K-lane mode: a warp per output, lanes striding the K range (for steps whose streamed
+// operand is contiguous along a K var, e.g. the input gradient of RTR's first node:
+// 900 contiguous terms per output), combined with a warp-shuffle tree.
+__global__ void __launch_bounds__(256) ce_stream_klane_kernel(const SvDesc d, const float* __restrict__ A,
+                                                              const float* __restrict__ B, float* __restrict__ C) {
+  ce_pdl_enter();
+  const uint32_t o = blockIdx.x * 8u + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (o >= d.outs) return;  // warp-uniform
+  int32_t offA = 0, offB = 0, offC = 0;
+  int32_t gbase[2 * SV_G];
+#pragma unroll
+  for (int g = 0; g < 2 * SV_G; ++g) gbase[g] = d.gc[g];
+  uint32_t rest = o;
+#pragma unroll
+  for (int i = 0; i < SV_O; ++i) {
+    if (i < d.nout) {
+      const uint32_t q = tc_quo(rest, d.odiv[i]);
+      const int32_t v = static_cast<int32_t>(rest - q * static_cast<uint32_t>(d.oext[i]));
+      rest = q;
+      offA += v * d.osa[i];
+      offB += v * d.osb[i];
+      offC += v * d.osc[i];
+#pragma unroll
+      for (int g = 0; g < 2 * SV_G; ++g) gbase[g] += v * d.go[g][i];
+    }
+  }
+  const uint32_t k0 = blockIdx.y * d.kper;
+  const uint32_t k1 = min(d.K, k0 + d.kper);
+  float acc = 0.f;
+  for (uint32_t k = k0 + lane; k < k1; k += 32) {
+    int32_t a = offA, b = offB;
+    int32_t gidx[2 * SV_G];
+#pragma unroll
+    for (int g = 0; g < 2 * SV_G; ++g) gidx[g] = gbase[g];
+    uint32_t r = k;
+#pragma unroll
+    for (int j = 0; j < SV_K; ++j) {
+      if (j < d.nk) {
+        const uint32_t q = tc_quo(r, d.kdiv[j]);
+        const int32_t v = static_cast<int32_t>(r - q * static_cast<uint32_t>(d.kext[j]));
+        r = q;
+        a += v * d.ksa[j];
+        b += v * d.ksb[j];
+#pragma unroll
+        for (int g = 0; g < 2 * SV_G; ++g) gidx[g] += v * d.gk[g][j];
+      }
+    }
+    bool ok = true;
+#pragma unroll
+    for (int g = 0; g < SV_G; ++g) {
+      if (g < d.nga) {
+        int32_t x = gidx[g];
+        if (d.gwrap[g]) x = sv_mod(x, d.gext[g]);
+        ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[g]);
+        a += x * d.gstride[g];
+      }
+      if (g < d.ngb) {
+        int32_t x = gidx[SV_G + g];
+        if (d.gwrap[SV_G + g]) x = sv_mod(x, d.gext[SV_G + g]);
+        ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[SV_G + g]);
+        b += x * d.gstride[SV_G + g];
+      }
+    }
+    if (ok) acc += d.unary ? __ldg(A + a) : __ldg(A + a) * __ldg(B + b);
+  }
+#pragma unroll
+  for (int m = 16; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (lane == 0) {
+    if (d.mode == 2)
+      atomicAdd(C + offC, acc);
+    else if (d.mode == 1)
+      C[offC] += acc;
+    else
+      C[offC] = acc;
+  }
+}
+
 // Builds the stream descriptor; false when the problem exceeds its limits (then the
 // int64 reference kernels run).  *span = elements of C an atomic reduction must zero.
 bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float* C, SvDesc* out, int64_t* span) {
-  const CeProblem& p = sd.p;
+  // merge vars that are contiguous in every operand (same role, not gathered): fewer
+  // index digits per thread and longer lane runs (e.g. RTR's (r3)(r0) output pair)
+  CeProblem p = sd.p;
+  auto gathered = [&](int v) {
+    for (int g = 0; g < p.ng_a; ++g)
+      if (p.ga[g].pv == v || p.ga[g].qv == v) return true;
+    for (int g = 0; g < p.ng_b; ++g)
+      if (p.gb[g].pv == v || p.gb[g].qv == v) return true;
+    return false;
+  };
+  for (bool merged = true; merged;) {
+    merged = false;
+    for (int u = 0; u < p.nv && !merged; ++u)
+      for (int v = 0; v < p.nv && !merged; ++v) {
+        if (u == v || p.ext[u] <= 1 || p.ext[v] <= 1 || gathered(u) || gathered(v)) continue;
+        if ((p.cls[u] == CE_K) != (p.cls[v] == CE_K)) continue;
+        if (p.sa[u] == 0 && p.sb[u] == 0 && p.sc[u] == 0) continue;
+        if (p.sa[v] != p.sa[u] * p.ext[u] || p.sb[v] != p.sb[u] * p.ext[u] || p.sc[v] != p.sc[u] * p.ext[u]) continue;
+        if (p.ext[u] * p.ext[v] >= (1ll << 31)) continue;
+        p.ext[u] *= p.ext[v];
+        p.ext[v] = 1;
+        merged = true;
+      }
+  }
   SvDesc d{};
   if (p.ng_a > SV_G || p.ng_b > SV_G) return false;
   // output vars: the lane var (unit stride in the operand that streams, else in C) first,
@@ -357,12 +470,35 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
       if (p.ga[g].pv == v || p.ga[g].qv == v) return p.ga[g].stride;
     return 0;
   };
+  // lane var: fewest 32-B sectors per warp access summed over the large operands (an
+  // operand independent of the var is a broadcast: 1 sector; unit stride: 4; else 32)
+  double sz[3] = {1, 1, 1};
+  for (int v = 0; v < p.nv; ++v) {
+    if (p.sa[v] || astride(v)) sz[0] *= static_cast<double>(p.ext[v]);
+    if (p.sb[v]) sz[1] *= static_cast<double>(p.ext[v]);
+    if (p.cls[v] != CE_K) sz[2] *= static_cast<double>(p.ext[v]);
+  }
+  if (p.unary) sz[1] = 0;
+  const double big = std::max(sz[0], std::max(sz[1], sz[2])) / 8;
+  auto bstride = [&](int v) -> int64_t {
+    if (p.sb[v]) return p.sb[v];
+    for (int g = 0; g < p.ng_b; ++g)
+      if (p.gb[g].pv == v || p.gb[g].qv == v) return p.gb[g].stride;
+    return 0;
+  };
+  auto sectors = [](int64_t st) { return st == 0 ? 1.0 : st == 1 ? 4.0 : 32.0; };
   int lane = -1;
-  for (int v : ov)
-    if (astride(v) == 1) lane = v;
-  if (lane < 0)
-    for (int v : ov)
-      if (p.sc[v] == 1) lane = v;
+  double best = 1e30;
+  for (int v : ov) {
+    double c = 0;
+    if (sz[0] >= big) c += sectors(astride(v));
+    if (sz[1] >= big) c += sectors(bstride(v));
+    if (sz[2] >= big) c += sectors(p.sc[v]);
+    if (c < best - 1e-9 || (c < best + 1e-9 && astride(v) == 1)) {
+      best = c;
+      lane = v;
+    }
+  }
   if (lane >= 0) {
     ov.erase(std::find(ov.begin(), ov.end(), lane));
     ov.insert(ov.begin(), lane);
@@ -372,6 +508,10 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
     const int64_t sx = astride(x) ? astride(x) : p.sb[x], sy = astride(y) ? astride(y) : p.sb[y];
     return sx < sy;
   });
+  // K-lane mode when no output var streams A contiguously but the fastest K var does
+  const bool klane = sz[0] >= big && !kvars.empty() && astride(kvars[0]) == 1 && best >= 32 &&
+                     std::accumulate(kvars.begin(), kvars.end(), int64_t{1},
+                                     [&](int64_t acc_, int v) { return acc_ * p.ext[v]; }) >= 64;
   int64_t outs = 1, K = 1, maxA = 0, maxB = 0, maxC = 0;
   d.nout = static_cast<int32_t>(ov.size());
   d.nk = static_cast<int32_t>(kvars.size());
@@ -422,8 +562,9 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
   d.nga = p.ng_a;
   d.ngb = p.ng_b;
   d.unary = p.unary;
+  d.klane = klane ? 1 : 0;
   // VEC=4 along the lane var: unit stride and 16-B aligned A, lane var never gathered
-  {
+  if (!klane) {
     // a lane extent that is not a multiple of 4 needs a row pitch of >= round_up(ext, 4) in
     // A (the last float4 reads the row's padding) and masks B loads / C stores past it
     auto al = [](const float* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
@@ -437,8 +578,11 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
         if (d.gstride[gbase + g] % 4 || d.gstride[gbase + g] < ext4) return false;
       return true;
     };
-    bool ok = al(A) && d.nout >= 1 && d.osa[0] == 1 && padded(d.osa, d.ksa, 0, p.ng_a);
+    // A along the lane var: unit stride (float4) or independent of it (one scalar, broadcast)
+    const bool a_b = d.nout >= 1 && d.osa[0] == 0;
+    bool ok = d.nout >= 1 && (a_b || (al(A) && d.osa[0] == 1 && padded(d.osa, d.ksa, 0, p.ng_a)));
     for (int g = 0; g < 2 * SV_G && ok; ++g) ok = d.go[g][0] == 0;
+    d.a_bcast = a_b ? 1 : 0;
     d.vec = ok ? 1 : 0;
     if (ok) {
       const bool vb = !p.unary && al(B) && d.osb[0] == 1 && padded(d.osb, d.ksb, SV_G, p.ng_b);
@@ -457,9 +601,10 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
   d.K = static_cast<uint32_t>(K);
   // K slices: enough CTAs for ~8 per SM when the outputs alone do not fill the GPU,
   // each thread keeping >= 32 K terms
-  const int64_t blocks = (outs + 255) / 256;
+  const int64_t blocks = klane ? (outs + 7) / 8 : (outs + 255) / 256;
   int64_t split = 1;
-  if (blocks < 148 * 8 && K >= 64) split = std::min<int64_t>((148 * 8 + blocks - 1) / blocks, K / 32);
+  if (blocks < 148 * 8 && K >= 64)
+    split = std::min<int64_t>((148 * 8 + blocks - 1) / blocks, K / (klane ? 1024 : 32));
   split = std::max<int64_t>(1, std::min<int64_t>(split, 65535));
   d.kper = static_cast<uint32_t>((K + split - 1) / split);
   d.mode = split > 1 ? 2 : (p.accumulate ? 1 : 0);
@@ -475,7 +620,9 @@ cudaError_t sv_launch(const SvDesc& d, int64_t span, bool zero_first, const floa
     cudaError_t e = cudaMemsetAsync(C, 0, static_cast<size_t>(span) * 4, s);
     if (e != cudaSuccess) return e;
   }
-  const unsigned gx = (d.outs + 255u) / 256u, gy = d.K ? (d.K + d.kper - 1) / d.kper : 1u;
+  const unsigned gy = d.K ? (d.K + d.kper - 1) / d.kper : 1u;
+  if (d.klane) return ce_launch(ce_stream_klane_kernel, dim3((d.outs + 7u) / 8u, gy), dim3(256), 0, s, d, A, B, C);
+  const unsigned gx = (d.outs + 255u) / 256u;
   if (d.vec) return ce_launch(ce_stream_kernel<4>, dim3(gx, gy), dim3(256), 0, s, d, A, B, C);
   return ce_launch(ce_stream_kernel<1>, dim3(gx, gy), dim3(256), 0, s, d, A, B, C);
 }
