@@ -369,7 +369,12 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
         }
       }
     }
-    if (ok && (st.tc.params.oa.mn_major || st.tc.params.ob.mn_major) && st.tc.params.k_iters > 64) {
+    static const int repack_mn = [] {  // experiment knob: 1 = repack every MN-major operand
+      const char* e = std::getenv("CE_REPACK_MN");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (ok && (st.tc.params.oa.mn_major || st.tc.params.ob.mn_major) &&
+        (st.tc.params.k_iters > 64 || repack_mn == 1)) {
       // One MN-major operand over a long K loop (factor gradients: K = every b,h,w): its
       // 4 KB [32 K][32 MN] boxes plus the in-smem transpose make the TMA producer, not the
       // MMA, the bottleneck (measured 1.4 us per stage against 0.39 us K-major).  A single
@@ -400,16 +405,32 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
         CeProblem pk = repack(q, side_b, order, &span, side_b ? p.sa : p.sb);
         TcPlan t;
         if (ce_tc_plan(q, &t) && !t.params.oa.mn_major && !t.params.ob.mn_major) {
-          Step ps;
-          ps.kind = ce_permute_supported(pk) ? Step::kPermute : Step::kDirect;
-          ps.desc = simt_desc(pk);
-          ps.a = side_b ? b : a;
-          ps.c = {BufRef::kWork, alloc(span)};
-          ps.node = node;
-          ps.label = label + (side_b ? ":packB" : ":packA");
-          ps.bytes = 8.0 * operand_elems(pk, 0);
-          (side_b ? b : a) = ps.c;
-          list.push_back(ps);
+          const BufRef src = side_b ? b : a;
+          bool reused = false;
+          for (const PackRecord& r : packs_) {  // the forward pass may have packed it already
+            if (r.src.kind != src.kind || r.src.index != src.index || r.pk.nv != pk.nv) continue;
+            bool same = true;
+            for (int v = 0; v < r.pk.nv && same; ++v)
+              same = r.pk.ext[v] == pk.ext[v] && r.pk.sa[v] == pk.sa[v] && r.pk.sc[v] == pk.sc[v];
+            if (same) {
+              (side_b ? b : a) = r.dst;
+              reused = true;
+              break;
+            }
+          }
+          if (!reused) {
+            Step ps;
+            ps.kind = ce_permute_supported(pk) ? Step::kPermute : Step::kDirect;
+            ps.desc = simt_desc(pk);
+            ps.a = src;
+            ps.c = {BufRef::kWork, alloc(span)};
+            ps.node = node;
+            ps.label = label + (side_b ? ":packB" : ":packA");
+            ps.bytes = 8.0 * operand_elems(pk, 0);
+            (side_b ? b : a) = ps.c;
+            if (&list == &fwd_) packs_.push_back({src, pk, ps.c});
+            list.push_back(ps);
+          }
           p = q;
           st.tc = t;
         }

@@ -150,13 +150,21 @@ LAYER_CASES = [
     ("cfg2 TT cr0.1", "tt", 256, 256, 14, 128, 0.1),
     ("cfg2 TK cr1.0", "tk", 256, 256, 14, 128, 1.0),
     ("cfg2 TT cr1.0", "tt", 256, 256, 14, 128, 1.0),
+    # cfg5 compression-sweep end points and the dense baseline at the cfg2 shape
+    ("cfg5 CP cr0.5", "cp", 256, 256, 14, 128, 0.5),
+    ("cfg5 TR cr0.05", "tr", 256, 256, 14, 128, 0.05),
+    ("cfg5 TT cr0.05", "tt", 256, 256, 14, 128, 0.05),
+    ("cfg5 dense", "standard", 256, 256, 14, 128, []),
+    # cfg4 CP stack first layer (7x7 at 112x112, 3->64), reduced batch
+    ("cfg4 CP conv1 cr1.0", "cp", 64, 3, 112, 8, 1.0),
 ]
 
 
 def _layer(kind, T, S, Hp, B, cr):
     import paper_2401_03384_b200 as ce
-    slots = {"cp": 1, "tk": 2, "tt": 3, "tr": 4}[kind]
-    spec = ce.LayerSpec(kind, [T], [S], 3, 3, Hp, Hp, B, cr if isinstance(cr, list) else [1] * slots)
+    slots = {"cp": 1, "tk": 2, "tt": 3, "tr": 4, "standard": 0}[kind]
+    k = 7 if (S == 3 and Hp == 112) else 3  # ResNet-34 conv1 is 7x7
+    spec = ce.LayerSpec(kind, [T], [S], k, k, Hp, Hp, B, cr if isinstance(cr, list) else [1] * slots)
     return ce.expression(spec, None if isinstance(cr, list) else cr)
 
 
