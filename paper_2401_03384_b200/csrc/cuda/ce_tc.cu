@@ -198,6 +198,29 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Split TMEM load: issue without waiting, and a wait that ties the destination registers
+// (so no use can be scheduled before the data has landed).
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
 // Vector reduction into global memory (split-K epilogue): 4 consecutive floats, one request.
 __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
   asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
@@ -682,87 +705,99 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       if (local == 0) ce_pdl_wait();  // (long complete: the producer waited before its loads)
       const bool empty_k = k1 <= k0;
       const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
-#pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        if (ch * 32 >= n_cols) break;
-        uint32_t r[32];
-        tmem_ld32(t_base + ch * 32, r);
-        if (empty_k)
+      // TMEM loads double-buffered against the stores: chunk c+1 is read while chunk c drains
+      const int nch = min(BN / 32, (n_cols + 31) / 32);
+      auto process = [&](uint32_t (&r)[32], int ch) {
+          if (empty_k)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = 0;
-        if (dbg & 4) {
-          // timing experiment: TMEM loads only, no stores
-          if (r[0] == 0x7fffffffu) C[0] = 0.f;
-        } else if (tstore) {
-          // stage this warp's 32x32 block row-major; then each lane writes 4 consecutive columns
-          // of one row (8 lanes cover a row: 128 B per row, 4 rows per instruction)
+            for (int i = 0; i < 32; ++i) r[i] = 0;
+          if (dbg & 4) {
+            // timing experiment: TMEM loads only, no stores
+            if (r[0] == 0x7fffffffu) C[0] = 0.f;
+          } else if (tstore) {
+            // stage this warp's 32x32 block row-major; then each lane writes 4 consecutive columns
+            // of one row (8 lanes cover a row: 128 B per row, 4 rows per instruction)
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(stage + lane * kStagePitch + 4 * j) =
-                make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
-                            __uint_as_float(r[4 * j + 3]));
-          __syncwarp();
-          const int g = lane & 7, sub = lane >> 3;
-          const int64_t gc = gcol[ch * 8 + g];
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(stage + lane * kStagePitch + 4 * j) =
+                  make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                              __uint_as_float(r[4 * j + 3]));
+            __syncwarp();
+            const int g = lane & 7, sub = lane >> 3;
+            const int64_t gc = gcol[ch * 8 + g];
 #pragma unroll 4
-          for (int k = 0; k < 8; ++k) {
-            const int rr = 4 * k + sub;
-            const int64_t rt = rtab[q * 32 + rr];
-            if (rt < 0) continue;
-            const float4 v = *reinterpret_cast<const float4*>(stage + rr * kStagePitch + 4 * g);
-            if (gc >= 0 && (rt & 3) == 0) {
-              float* dst = C + rt + gc;
-              if (atomic)
-                red_add_v4(dst, v);
-              else
-                *reinterpret_cast<float4*>(dst) = v;
-            } else {
-              const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const int64_t co = cols[ch * 32 + 4 * g + i];
-                if (co < 0) continue;
+            for (int k = 0; k < 8; ++k) {
+              const int rr = 4 * k + sub;
+              const int64_t rt = rtab[q * 32 + rr];
+              if (rt < 0) continue;
+              const float4 v = *reinterpret_cast<const float4*>(stage + rr * kStagePitch + 4 * g);
+              if (gc >= 0 && (rt & 3) == 0) {
+                float* dst = C + rt + gc;
                 if (atomic)
-                  atomicAdd(C + rt + co, vv[i]);
+                  red_add_v4(dst, v);
                 else
-                  C[rt + co] = vv[i];
+                  *reinterpret_cast<float4*>(dst) = v;
+              } else {
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const int64_t co = cols[ch * 32 + 4 * g + i];
+                  if (co < 0) continue;
+                  if (atomic)
+                    atomicAdd(C + rt + co, vv[i]);
+                  else
+                    C[rt + co] = vv[i];
+                }
+              }
+            }
+            __syncwarp();
+          } else if (roff >= 0) {
+            float* crow = C + roff;
+            bool vec = (roff & 3) == 0;
+            int64_t gc[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              gc[g] = gcol[ch * 8 + g];
+              vec = vec && gc[g] >= 0;
+            }
+            if (vec) {
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                const float4 v = make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
+                                             __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3]));
+                if (atomic)
+                  red_add_v4(crow + gc[g], v);
+                else
+                  *reinterpret_cast<float4*>(crow + gc[g]) = v;
+              }
+            } else {
+              int64_t co[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) co[i] = cols[ch * 32 + i];
+              if (atomic) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (co[i] >= 0) atomicAdd(crow + co[i], __uint_as_float(r[i]));
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (co[i] >= 0) crow[co[i]] = __uint_as_float(r[i]);
               }
             }
           }
-          __syncwarp();
-        } else if (roff >= 0) {
-          float* crow = C + roff;
-          bool vec = (roff & 3) == 0;
-          int64_t gc[8];
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            gc[g] = gcol[ch * 8 + g];
-            vec = vec && gc[g] >= 0;
-          }
-          if (vec) {
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-              const float4 v = make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
-                                           __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3]));
-              if (atomic)
-                red_add_v4(crow + gc[g], v);
-              else
-                *reinterpret_cast<float4*>(crow + gc[g]) = v;
-            }
-          } else {
-            int64_t co[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) co[i] = cols[ch * 32 + i];
-            if (atomic) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (co[i] >= 0) atomicAdd(crow + co[i], __uint_as_float(r[i]));
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (co[i] >= 0) crow[co[i]] = __uint_as_float(r[i]);
-            }
-          }
+      };
+      uint32_t ra[32], rb[32];
+      tmem_ld32_issue(t_base, ra);
+      tmem_ld_wait(ra);
+#pragma unroll 1
+      for (int ch = 0; ch < nch; ch += 2) {
+        if (ch + 1 < nch) tmem_ld32_issue(t_base + (ch + 1) * 32, rb);
+        process(ra, ch);
+        if (ch + 1 < nch) {
+          tmem_ld_wait(rb);
+          if (ch + 2 < nch) tmem_ld32_issue(t_base + (ch + 2) * 32, ra);
+          process(rb, ch + 1);
+          if (ch + 2 < nch) tmem_ld_wait(ra);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
