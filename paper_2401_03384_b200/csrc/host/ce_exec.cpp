@@ -9,6 +9,7 @@
 #include "ce_exec.hpp"
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
@@ -246,6 +247,19 @@ CeProblem repack(CeProblem& p, bool side_b, const std::vector<int>& inner_order,
   return pk;
 }
 
+// Layout signature of a pack (a unary permute): (extent, input stride, output stride) of
+// every axis with extent > 1, in input-stride order.  Two packs with equal signatures
+// of the same buffer produce identical bytes.
+std::vector<int64_t> pack_signature(const CeProblem& pk) {
+  std::vector<std::array<int64_t, 3>> ax;
+  for (int v = 0; v < pk.nv; ++v)
+    if (pk.ext[v] > 1) ax.push_back({pk.sa[v], pk.ext[v], pk.sc[v]});
+  std::sort(ax.begin(), ax.end());
+  std::vector<int64_t> sig;
+  for (const auto& a : ax) sig.insert(sig.end(), a.begin(), a.end());
+  return sig;
+}
+
 int inner_var(const CeProblem& p, bool side_b) {
   const int64_t* s = side_b ? p.sb : p.sa;
   for (int v = 0; v < p.nv; ++v)
@@ -312,11 +326,8 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
             const BufRef src = side ? b : a;
             bool reused = false;
             for (const PackRecord& r : packs_) {
-              if (r.src.kind != src.kind || r.src.index != src.index || r.pk.nv != pks[side].nv) continue;
-              bool same = true;
-              for (int v = 0; v < r.pk.nv && same; ++v)
-                same = r.pk.ext[v] == pks[side].ext[v] && r.pk.sa[v] == pks[side].sa[v] && r.pk.sc[v] == pks[side].sc[v];
-              if (same) {
+              if (r.src.kind != src.kind || r.src.index != src.index) continue;
+              if (pack_signature(r.pk) == pack_signature(pks[side])) {
                 (side ? b : a) = r.dst;
                 reused = true;
                 break;
@@ -408,11 +419,8 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
           const BufRef src = side_b ? b : a;
           bool reused = false;
           for (const PackRecord& r : packs_) {  // the forward pass may have packed it already
-            if (r.src.kind != src.kind || r.src.index != src.index || r.pk.nv != pk.nv) continue;
-            bool same = true;
-            for (int v = 0; v < r.pk.nv && same; ++v)
-              same = r.pk.ext[v] == pk.ext[v] && r.pk.sa[v] == pk.sa[v] && r.pk.sc[v] == pk.sc[v];
-            if (same) {
+            if (r.src.kind != src.kind || r.src.index != src.index) continue;
+            if (pack_signature(r.pk) == pack_signature(pk)) {
               (side_b ? b : a) = r.dst;
               reused = true;
               break;
@@ -602,7 +610,8 @@ std::string Executor::describe() const {
       } else if (st.kind == Step::kPermute) {
         char pd[256];
         ce_permute_describe(st.desc.p, pd, sizeof pd);
-        std::snprintf(line + n, sizeof line - n, " %s\n", pd);
+        static const char* bk[] = {"none", "in", "out", "ws", "dout", "din"};
+        std::snprintf(line + n, sizeof line - n, " %s src=%s:%lld\n", pd, bk[st.a.kind], (long long)st.a.index);
       } else {
         std::snprintf(line + n, sizeof line - n, " Z=%lld M=%lld N=%lld K=%lld (tc: %s)\n", (long long)st.desc.Z,
                       (long long)st.desc.M, (long long)st.desc.N, (long long)st.desc.K,
@@ -730,12 +739,25 @@ void Executor::launch_step(Step& st, cudaStream_t s) {
 
 std::vector<Executor::StepTime> Executor::step_times(bool bwd) {
   std::vector<StepTime> out;
+  // debug: CE_TIMELINE=1 prints each step's start / end relative to the pass's first step
+  static const bool timeline = [] {
+    const char* e = std::getenv("CE_TIMELINE");
+    return e && *e == '1';
+  }();
+  cudaEvent_t first = nullptr;
   for (Step& st : bwd ? bwd_ : fwd_) {
     if (!st.ran || !st.ev0) continue;
     cuda_check(cudaEventSynchronize(st.ev1), "cudaEventSynchronize");
     float ms = 0;
     cuda_check(cudaEventElapsedTime(&ms, st.ev0, st.ev1), "cudaEventElapsedTime");
     out.push_back({st.label, static_cast<int>(st.kind), ms, st.flops, st.bytes});
+    if (timeline) {
+      if (!first) first = st.ev0;
+      float t0 = 0;
+      cudaEventElapsedTime(&t0, first, st.ev0);
+      std::fprintf(stderr, "timeline %s %-22s start %9.1f us  end %9.1f us\n", bwd ? "bwd" : "fwd", st.label.c_str(),
+                   t0 * 1e3, (t0 + ms) * 1e3);
+    }
   }
   return out;
 }
