@@ -292,23 +292,45 @@ __device__ __forceinline__ void decode_work(const TcParams& P, uint32_t w, uint3
   T.split = static_cast<int>(t);
 }
 
-// Work item w -> index in the full decomposition (tiles x K splits) and its K range.
-__device__ __forceinline__ uint32_t work_item(const TcParams& P, uint32_t w, int& k0, int& k1) {
-  if (P.tail_s == 0 || w < static_cast<uint32_t>(P.tail_base)) {
-    const int split = static_cast<int>(tc_quo(w, P.dsplit));
-    k0 = split * P.k_per;
-    k1 = min(P.k_iters, k0 + P.k_per);
-    return w;
+// Work sequence of one group: whole items group, group + ngroups, ... below sk_full,
+// then (stream-K) the group's contiguous share of the sk_r tail items' K iterations.
+struct WorkIter {
+  uint32_t w;         // next whole item
+  uint32_t pos, end;  // stream-K iteration range (relative to item sk_full, iteration 0)
+};
+
+__device__ __forceinline__ void work_begin(const TcParams& P, uint32_t group, uint32_t ngroups, WorkIter& it) {
+  it.w = group;
+  it.pos = it.end = 0;
+  if (P.sk_r > 0) {
+    const uint32_t total = P.sk_r * static_cast<uint32_t>(P.k_iters);
+    const uint32_t q = total / ngroups, r = total % ngroups;
+    it.pos = group * q + min(group, r);
+    it.end = it.pos + q + (group < r ? 1u : 0u);
   }
-  const uint32_t j = w - static_cast<uint32_t>(P.tail_base);
-  const uint32_t sl = tc_quo(j, P.dtail_r);
-  k0 = static_cast<int>(sl) * P.tail_per;
-  k1 = min(P.k_iters, k0 + P.tail_per);
-  return static_cast<uint32_t>(P.tail_base) + (j - sl * P.dtail_r.d);
 }
 
-__device__ __forceinline__ bool work_atomic(const TcParams& P, uint32_t w) {
-  return P.k_split > 1 || (P.tail_s > 0 && w >= static_cast<uint32_t>(P.tail_base));
+// Next segment: item (full-decomposition index), K range [k0, k1), atomic epilogue flag.
+__device__ __forceinline__ bool work_next(const TcParams& P, uint32_t ngroups, WorkIter& it, uint32_t& item, int& k0,
+                                          int& k1, bool& atomic) {
+  const uint32_t whole = P.sk_r > 0 ? P.sk_full : P.n_items;
+  if (it.w < whole) {
+    item = it.w;
+    it.w += ngroups;
+    const int split = static_cast<int>(tc_quo(item, P.dsplit));
+    k0 = split * P.k_per;
+    k1 = min(P.k_iters, k0 + P.k_per);
+    atomic = P.k_split > 1;
+    return true;
+  }
+  if (it.pos >= it.end) return false;
+  const uint32_t rel = tc_quo(it.pos, P.dkit);
+  k0 = static_cast<int>(it.pos - rel * static_cast<uint32_t>(P.k_iters));
+  k1 = min(P.k_iters, k0 + static_cast<int>(it.end - it.pos));
+  item = P.sk_full + rel;
+  atomic = true;
+  it.pos += static_cast<uint32_t>(k1 - k0);
+  return true;
 }
 
 __device__ __forceinline__ void coords(const TcOperand& o, const int32_t* val, int c[5]) {
@@ -388,10 +410,6 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) stamp(Pg, 0);
-  const uint32_t n_work =
-      Pg.tail_s > 0 ? static_cast<uint32_t>(Pg.tail_base + Pg.tail_r * Pg.tail_s)
-                    : (static_cast<uint32_t>(Pg.tiles_m) + csize - 1) / csize * static_cast<uint32_t>(Pg.tiles_n) *
-                          static_cast<uint32_t>(Pg.grid_z) * static_cast<uint32_t>(Pg.k_split);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -454,9 +472,13 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       uint32_t gi = 0;  // global stage counter across tiles
       Tile& T = tiles[0];
       if (dbg & 32) stamp(P, 9);  // producer entered (after griddepcontrol.wait)
-      for (uint32_t w = group; w < n_work; w += ngroups) {
-        int k0, k1;
-        decode_work(P, work_item(P, w, k0, k1), rank, csize, T);
+      WorkIter wi;
+      work_begin(P, group, ngroups, wi);
+      uint32_t item;
+      int k0, k1;
+      bool seg_atomic;
+      while (work_next(P, ngroups, wi, item, k0, k1, seg_atomic)) {
+        decode_work(P, item, rank, csize, T);
         int ca[5], cb[5], dig[6];
         coords(P.oa, T.val, ca);
         coords(P.ob, T.val, cb);
@@ -555,10 +577,13 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       // 14-bit start-address field (smem < 256 KB, so the add never carries out of it)
       const uint64_t adesc0 = kmajor_desc(smem_u32(sA)), bdesc0 = kmajor_desc(smem_u32(sB));
       uint32_t gi = 0, local = 0;
-      for (uint32_t w = group; w < n_work; w += ngroups, ++local) {
+      WorkIter wi;
+      work_begin(P, group, ngroups, wi);
+      uint32_t item;
+      int k0, k1;
+      bool seg_atomic;
+      for (; work_next(P, ngroups, wi, item, k0, k1, seg_atomic); ++local) {
         const int acc = static_cast<int>(local & 1);
-        int k0, k1;
-        work_item(P, w, k0, k1);
         int d0 = k0 % kc0;  // K digit 0 of the first iteration (for the K tail)
         if (PAIR)
           mbar_wait_cluster(&tempty[acc], ((local >> 1) & 1) ^ 1);  // both epilogues drained it
@@ -614,9 +639,12 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     if (xpose) {
       const int xw = warp - (2 + kEpiWarps);
       uint32_t gi = 0;
-      for (uint32_t w = group; w < n_work; w += ngroups) {
-        int k0, k1;
-        work_item(P, w, k0, k1);
+      WorkIter wi;
+      work_begin(P, group, ngroups, wi);
+      uint32_t item;
+      int k0, k1;
+      bool seg_atomic;
+      while (work_next(P, ngroups, wi, item, k0, k1, seg_atomic)) {
         for (int it = k0; it < k1; ++it, ++gi) {
           const int s = static_cast<int>(gi % STAGES);
           mbar_wait(&full[s], (gi / STAGES) & 1);
@@ -652,12 +680,14 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     uint32_t local = 0;
     Tile& T = tiles[1];
     int cols_for[2] = {-1, -1};  // N tile whose column tables each accumulator buffer holds
-    for (uint32_t w = group; w < n_work; w += ngroups, ++local) {
+    WorkIter wi;
+    work_begin(P, group, ngroups, wi);
+    uint32_t item;
+    int k0, k1;
+    bool atomic;
+    for (; work_next(P, ngroups, wi, item, k0, k1, atomic); ++local) {
       const int acc = static_cast<int>(local & 1);
-      int k0, k1;
-      const uint32_t wf = work_item(P, w, k0, k1);
-      const bool atomic = work_atomic(P, w);
-      if (et == 0) decode_work(P, wf, rank, csize, T);
+      if (et == 0) decode_work(P, item, rank, csize, T);
       epi_bar();  // decoded tile visible (and the previous tile's tables are no longer read)
       // address tables for this tile (overlaps the MMAs)
       int64_t* cols = col_off + acc * BN;
@@ -931,30 +961,34 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
   if (static_cast<int64_t>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_split >= (1ll << 32))
     return cudaErrorInvalidConfiguration;
   {
-    // tail split of a partial last round (see TcParams::tail_s)
+    // stream-K tail of a partial last round (see TcParams::sk_r)
     const int64_t csize = P.mcast ? 2 : 1;
-    const int64_t groups = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
-    const int64_t ngroups = std::min<int64_t>(groups, sm_count() / csize);
-    P.tail_s = 0;
-    static const bool tail_on = [] {
-      const char* e = getenv("CE_TC_TAIL");
-      return !(e && *e == '0');
+    const int64_t items = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
+    const int64_t ngroups = std::min<int64_t>(items, sm_count() / csize);
+    P.n_items = static_cast<uint32_t>(items);
+    P.sk_full = 0;
+    P.sk_r = 0;
+    P.dkit = tc_div(static_cast<uint32_t>(std::max(1, P.k_iters)));
+    // off by default: the C memset it needs is a separate graph node that breaks the PDL
+    // chain, which cost more than the shorter last round saved (measured on cfg2:
+    // tk1.0 node1 76 -> 68 us, layer 0.434 -> 0.456 ms).  CE_TC_SK=1 enables it.
+    static const bool sk_on = [] {
+      const char* e = getenv("CE_TC_SK");
+      return e && *e == '1';
     }();
-    // only for mainloop-dominated items: a short K loop is cheaper than the memset and the
-    // atomic epilogue the split needs (measured: 8-iteration GEMMs got 2x slower)
-    if (tail_on && P.k_split == 1 && groups > ngroups && P.k_iters >= 48) {
-      const int64_t r = groups % ngroups;
-      const int64_t sl = r > 0 ? std::min<int64_t>(ngroups / r, P.k_iters / 2) : 0;
-      if (r > 0 && 4 * r <= 3 * ngroups && sl >= 2) {
-        P.tail_base = static_cast<int32_t>(groups - r);
-        P.tail_r = static_cast<int32_t>(r);
-        P.tail_s = static_cast<int32_t>(sl);
-        P.tail_per = static_cast<int32_t>((P.k_iters + sl - 1) / sl);
-        P.dtail_r = tc_div(static_cast<uint32_t>(r));
+    if (sk_on && P.k_split == 1 && items > ngroups && items % ngroups != 0) {
+      // gain: the last round shrinks from one item time to r/ngroups of it; cost: zeroing C
+      // (and an atomic epilogue for those items).  Item time ~ 0.4 us per K stage.
+      const int64_t r = items % ngroups;
+      const double saved_us = 0.4 * P.k_iters * (1.0 - static_cast<double>(r) / static_cast<double>(ngroups));
+      const double cost_us = 2.0 + static_cast<double>(plan.out_span) * 4.0 / 5.0e6;
+      if (saved_us > 1.5 * cost_us) {
+        P.sk_full = static_cast<uint32_t>(items - r);
+        P.sk_r = static_cast<uint32_t>(r);
       }
     }
   }
-  if (P.k_split > 1 || P.tail_s > 0) {
+  if (P.k_split > 1 || P.sk_r > 0) {
     cudaError_t e = cudaMemsetAsync(C, 0, static_cast<size_t>(plan.out_span) * 4, s);
     if (e != cudaSuccess) return e;
   }

@@ -105,11 +105,14 @@ struct TcParams {
   TcDiv dtn;       // tiles_n
   TcDiv dsplit;    // pm * tiles_n * grid_z: work items per K split
   int32_t k_per;   // K iterations per split
-  // Tail split (set per launch): when the last round of work items would leave many SMs
-  // idle, its R items are split S ways along K (atomic epilogue into a pre-zeroed C) so
-  // the round finishes in ~1/S of a tile time.  tail_s == 0: off.
-  int32_t tail_base, tail_r, tail_s, tail_per;
-  TcDiv dtail_r;
+  // Stream-K tail (set per launch): the n_items work items are dealt in full rounds of
+  // ngroups; the sk_r items of a partial last round are instead spread over ALL groups as
+  // contiguous runs of K iterations (each group ~sk_r * k_iters / ngroups of them), with an
+  // atomic epilogue into a pre-zeroed C.  sk_r == 0: off.
+  uint32_t n_items;  // work items of the full decomposition (tiles x K splits)
+  uint32_t sk_full;  // items handled whole (a multiple of ngroups)
+  uint32_t sk_r;     // items handled stream-K
+  TcDiv dkit;        // k_iters
   // 2-CTA cluster along M: each CTA TMA-loads mc_half rows of the B tile and multicasts
   // them to both CTAs (B is read from L2 once per CTA pair instead of once per CTA)
   int32_t mcast;           // 1: launched with cluster dims (2,1,1)

@@ -10,6 +10,8 @@
 // not multiple of 16 B, no unit-stride axis) returns false and the executor uses
 // the SIMT kernels (ce_simt.cu).
 #include <algorithm>
+#include <functional>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -264,20 +266,57 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
       list[(*n)++] = u;
       return box;
     }
-    int remaining = cap;
+    // candidate tile units in the operand's stride order (up to 3)
+    std::vector<int> cand;
     for (const Axis& a : ops) {
-      if (remaining <= 1 || *n >= 3) break;
+      if (cand.size() >= 3) break;
       int u = -1;
       if (!a.gather && ucls(a.v0) == cls) u = uid(a.v0);
       if (a.gather && ucls(a.v0) == cls && a.c0 == 1) u = uid(a.v0);
       if (u < 0 || U[static_cast<std::size_t>(u)].src != TC_SRC_GRID) continue;
-      const int e = U[static_cast<std::size_t>(u)].ext;
-      const int box = std::min(e, remaining);
-      U[static_cast<std::size_t>(u)].box = box;
+      if (std::find(cand.begin(), cand.end(), u) != cand.end()) continue;
+      cand.push_back(u);
+    }
+    if (cand.empty()) return rows;
+    // Boxes minimising the number of tiles (every tile costs a full M=128 / N MMA), then
+    // maximising the rows used: e.g. a 14x14 image stack tiles as [14 w][1 h][9 b] (98%
+    // of the rows useful) instead of [14 w][9 h] (77%).
+    std::vector<int64_t> ext;
+    for (int u : cand) ext.push_back(U[static_cast<std::size_t>(u)].ext);
+    std::vector<int> best(cand.size(), 1);
+    int64_t best_tiles = INT64_MAX, best_rows = 0;
+    std::vector<int> b(cand.size(), 1);
+    std::function<void(std::size_t, int)> search = [&](std::size_t i, int room) {
+      if (i == cand.size()) {
+        int64_t tiles = 1, r = 1;
+        for (std::size_t j = 0; j < cand.size(); ++j) {
+          tiles *= (ext[j] + b[j] - 1) / b[j];
+          r *= b[j];
+        }
+        if (tiles < best_tiles || (tiles == best_tiles && r > best_rows)) {
+          best_tiles = tiles;
+          best_rows = r;
+          best = b;
+        }
+        return;
+      }
+      const int hi = static_cast<int>(std::min<int64_t>(ext[i], room));
+      for (int x = hi; x >= 1; --x) {
+        // only boxes that are the full extent or change the tile count are worth trying
+        if (x < hi && (ext[i] + x - 1) / x == (ext[i] + x) / (x + 1)) continue;
+        b[i] = x;
+        search(i + 1, room / x);
+      }
+      b[i] = 1;
+    };
+    search(0, cap);
+    for (std::size_t j = 0; j < cand.size(); ++j) {
+      if (best[j] <= 1 && j > 0) continue;  // box 1: leave it a grid unit
+      const int u = cand[j];
+      U[static_cast<std::size_t>(u)].box = best[j];
       U[static_cast<std::size_t>(u)].src = src;
       list[(*n)++] = u;
-      rows *= box;
-      remaining /= box;
+      rows *= best[j];
     }
     return rows;
   };
