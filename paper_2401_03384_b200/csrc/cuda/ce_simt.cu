@@ -178,13 +178,16 @@ struct SvDesc {
   int32_t lext;                             // lane var extent (VEC=4: the last group may be partial)
   int32_t klane;                            // 1: warp per output, lanes along K
   int32_t a_bcast;                          // VEC=4 with A independent of the lane var
+  int32_t jrep, l1ext;                      // output slot 1 values per thread, slot 1 extent
+  int32_t g_inv1, b_inv1, bfix1;            // gathers / B / B and its gathers independent of slot 1
   int32_t oext[SV_O];
   TcDiv odiv[SV_O];
   int32_t osa[SV_O], osb[SV_O], osc[SV_O];
   int32_t kext[SV_K];
   TcDiv kdiv[SV_K];
   int32_t ksa[SV_K], ksb[SV_K];
-  // gathers: g < nga on A, then g < ngb on B
+  // gathers, compacted: g < ng, on operand gop[g] (0 = A, 1 = B)
+  int32_t ng, gop[2 * SV_G];
   int32_t gc[2 * SV_G], gext[2 * SV_G], gstride[2 * SV_G], gwrap[2 * SV_G];
   int32_t go[2 * SV_G][SV_O];  // coefficient of output slot i in the gathered index
   int32_t gk[2 * SV_G][SV_K];  // coefficient of K slot j
@@ -199,16 +202,17 @@ __device__ __forceinline__ int32_t sv_mod(int32_t x, int32_t e) {
 // VEC = 4: each thread owns 4 consecutive values of the lane var (slot 0, unit stride and
 // 16-B aligned in A, never gathered), loading A as float4; B and C use float4 when they
 // are unit-stride along the lane var too (flags set by the host), else 4 scalars.
-template <int VEC>
+template <int VEC, int NG>
 __global__ void __launch_bounds__(256) ce_stream_kernel(const SvDesc d, const float* __restrict__ A,
                                                         const float* __restrict__ B, float* __restrict__ C) {
   ce_pdl_enter();
   const uint32_t o = blockIdx.x * 256u + threadIdx.x;
-  if (o >= d.outs) return;  // outs counts threads (lane var divided by VEC)
-  int32_t offA = 0, offB = 0, offC = 0, lane0 = 0;
-  int32_t gidx[2 * SV_G];
+  if (o >= d.outs) return;  // outs counts threads (lane var / VEC, slot 1 / jrep)
+  // ---- output index decoding, once per thread
+  int32_t offA = 0, offB = 0, offC = 0, lane0 = 0, lane1 = 0;
+  int32_t gidx0[NG > 0 ? NG : 1];
 #pragma unroll
-  for (int g = 0; g < 2 * SV_G; ++g) gidx[g] = d.gc[g];
+  for (int g = 0; g < NG; ++g) gidx0[g] = d.gc[g];
   uint32_t rest = o;
 #pragma unroll
   for (int i = 0; i < SV_O; ++i) {
@@ -219,12 +223,210 @@ __global__ void __launch_bounds__(256) ce_stream_kernel(const SvDesc d, const fl
       if (i == 0) {
         v *= VEC;
         lane0 = v;
+      } else if (i == 1) {
+        v *= d.jrep;
+        lane1 = v;
       }
       offA += v * d.osa[i];
       offB += v * d.osb[i];
       offC += v * d.osc[i];
 #pragma unroll
-      for (int g = 0; g < 2 * SV_G; ++g) gidx[g] += v * d.go[g][i];
+      for (int g = 0; g < NG; ++g) gidx0[g] += v * d.go[g][i];
+    }
+  }
+  // ---- K slice start, once per thread
+  const uint32_t k0 = blockIdx.y * d.kper;
+  const uint32_t k1 = min(d.K, k0 + d.kper);
+  int32_t kv0[SV_K];
+  rest = k0;
+#pragma unroll
+  for (int j = 0; j < SV_K; ++j) {
+    kv0[j] = 0;
+    if (j < d.nk) {
+      const uint32_t q = tc_quo(rest, d.kdiv[j]);
+      kv0[j] = static_cast<int32_t>(rest - q * static_cast<uint32_t>(d.kext[j]));
+      rest = q;
+      offA += kv0[j] * d.ksa[j];
+      offB += kv0[j] * d.ksb[j];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) gidx0[g] += kv0[j] * d.gk[g][j];
+    }
+  }
+  const int32_t sb0 = d.osb[0];
+  const int32_t sa1 = d.nout > 1 ? d.osa[1] : 0, sb1 = d.nout > 1 ? d.osb[1] : 0, sc1 = d.nout > 1 ? d.osc[1] : 0;
+  // ---- jrep consecutive values of output slot 1 per thread (amortises the decoding)
+  for (int jj = 0; jj < d.jrep; ++jj) {
+    if (jj > 0 && lane1 + jj >= d.l1ext) break;
+    int32_t pa = offA + jj * sa1, pb = offB + jj * sb1;
+    int32_t gidx[NG > 0 ? NG : 1];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) gidx[g] = gidx0[g] + jj * (d.nout > 1 ? d.go[g][1] : 0);
+    int32_t kv[SV_K];
+#pragma unroll
+    for (int j = 0; j < SV_K; ++j) kv[j] = kv0[j];
+    float acc[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
+    for (uint32_t k = k0; k < k1; ++k) {
+      int32_t a = pa, b = pb;
+      bool ok = true;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        int32_t x = gidx[g];
+        if (d.gwrap[g]) x = sv_mod(x, d.gext[g]);
+        ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[g]);
+        if (d.gop[g])
+          b += x * d.gstride[g];
+        else
+          a += x * d.gstride[g];
+      }
+      if (ok) {
+        if (VEC == 1) {
+          acc[0] += d.unary ? __ldg(A + a) : __ldg(A + a) * __ldg(B + b);
+        } else {
+          float xa[4];
+          if (d.a_bcast) {
+            xa[0] = xa[1] = xa[2] = xa[3] = __ldg(A + a);
+          } else {
+            const float4 va = __ldg(reinterpret_cast<const float4*>(A + a));
+            xa[0] = va.x;
+            xa[1] = va.y;
+            xa[2] = va.z;
+            xa[3] = va.w;
+          }
+          if (d.unary) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[e] += xa[e];
+          } else if (d.vec_b) {
+            const float4 vb = __ldg(reinterpret_cast<const float4*>(B + b));
+            acc[0] += xa[0] * vb.x;
+            acc[1] += xa[1] * vb.y;
+            acc[2] += xa[2] * vb.z;
+            acc[3] += xa[3] * vb.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e)
+              if (lane0 + e < d.lext) acc[e] += xa[e] * __ldg(B + b + e * sb0);
+          }
+        }
+      }
+      // K odometer (slot 0 fastest); the gathered indices move with it
+#pragma unroll
+      for (int j = 0; j < SV_K; ++j) {
+        if (j < d.nk) {
+          if (++kv[j] < d.kext[j]) {
+            pa += d.ksa[j];
+            pb += d.ksb[j];
+#pragma unroll
+            for (int g = 0; g < NG; ++g) gidx[g] += d.gk[g][j];
+            break;
+          }
+          const int32_t back = d.kext[j] - 1;
+          pa -= back * d.ksa[j];
+          pb -= back * d.ksb[j];
+#pragma unroll
+          for (int g = 0; g < NG; ++g) gidx[g] -= back * d.gk[g][j];
+          kv[j] = 0;
+        }
+      }
+    }
+    const int32_t pc = offC + jj * sc1;
+    if (VEC == 4 && d.vec_c) {
+      float4* cp = reinterpret_cast<float4*>(C + pc);
+      const float4 v = make_float4(acc[0], acc[1], acc[2], acc[VEC - 1]);
+      if (d.mode == 2) {
+        asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(cp), "f"(v.x), "f"(v.y),
+                     "f"(v.z), "f"(v.w)
+                     : "memory");
+      } else if (d.mode == 1) {
+        float4 c = *cp;
+        c.x += v.x;
+        c.y += v.y;
+        c.z += v.z;
+        c.w += v.w;
+        *cp = c;
+      } else {
+        *cp = v;
+      }
+    } else {
+      const int32_t sc0 = d.osc[0];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        if (VEC > 1 && lane0 + e >= d.lext) break;
+        float* cp = C + pc + e * sc0;
+        if (d.mode == 2)
+          atomicAdd(cp, acc[e]);
+        else if (d.mode == 1)
+          *cp += acc[e];
+        else
+          *cp = acc[e];
+      }
+    }
+  }
+}
+
+
+__device__ __forceinline__ void xa4(const SvDesc& d, const float* p, float (&xa)[4]) {
+  if (d.a_bcast) {
+    xa[0] = xa[1] = xa[2] = xa[3] = __ldg(p);
+  } else {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    xa[0] = v.x;
+    xa[1] = v.y;
+    xa[2] = v.z;
+    xa[3] = v.w;
+  }
+}
+__device__ __forceinline__ void xb4(const SvDesc& d, const float* p, bool full0, int32_t lane0, float (&xb)[4]) {
+  if (d.vec_b) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    xb[0] = v.x;
+    xb[1] = v.y;
+    xb[2] = v.z;
+    xb[3] = v.w;
+  } else if (full0) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) xb[e] = __ldg(p + e * d.osb[0]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) xb[e] = lane0 + e < d.lext ? __ldg(p + e * d.osb[0]) : 0.f;
+  }
+}
+
+// Register-blocked VEC=4 variant: a thread owns 4 lane values x 4 consecutive values of
+// output slot 1; per K term the B vector is loaded once (when it does not depend on slot 1,
+// e.g. the depthwise factor F[r, k]) and reused for the 4 slot-1 outputs, so a 3-tap
+// stencil costs ~1 float4 load + 4 FMAs per 4 outputs instead of a full index walk.
+template <int NG>
+__global__ void __launch_bounds__(256) ce_stream_blk_kernel(const SvDesc d, const float* __restrict__ A,
+                                                            const float* __restrict__ B, float* __restrict__ C) {
+  ce_pdl_enter();
+  constexpr int J = 4;
+  const uint32_t o = blockIdx.x * 256u + threadIdx.x;
+  if (o >= d.outs) return;
+  int32_t offA = 0, offB = 0, offC = 0, lane0 = 0, lane1 = 0;
+  int32_t gidx[NG > 0 ? NG : 1];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) gidx[g] = d.gc[g];
+  uint32_t rest = o;
+#pragma unroll
+  for (int i = 0; i < SV_O; ++i) {
+    if (i < d.nout) {
+      const uint32_t q = tc_quo(rest, d.odiv[i]);
+      int32_t v = static_cast<int32_t>(rest - q * static_cast<uint32_t>(d.oext[i]));
+      rest = q;
+      if (i == 0) {
+        v *= 4;
+        lane0 = v;
+      } else if (i == 1) {
+        v *= J;
+        lane1 = v;
+      }
+      offA += v * d.osa[i];
+      offB += v * d.osb[i];
+      offC += v * d.osc[i];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) gidx[g] += v * d.go[g][i];
     }
   }
   const uint32_t k0 = blockIdx.y * d.kper;
@@ -241,62 +443,107 @@ __global__ void __launch_bounds__(256) ce_stream_kernel(const SvDesc d, const fl
       offA += kv[j] * d.ksa[j];
       offB += kv[j] * d.ksb[j];
 #pragma unroll
-      for (int g = 0; g < 2 * SV_G; ++g) gidx[g] += kv[j] * d.gk[g][j];
+      for (int g = 0; g < NG; ++g) gidx[g] += kv[j] * d.gk[g][j];
     }
   }
-  float acc[VEC];
+  const int32_t sa1 = d.osa[1], sb1 = d.osb[1];
+  const bool full0 = lane0 + 4 <= d.lext;
+  int nj = d.l1ext - lane1;
+  nj = nj < J ? nj : J;
+  float acc[J][4];
 #pragma unroll
-  for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
-  const int32_t sb0 = d.osb[0];
+  for (int jj = 0; jj < J; ++jj)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[jj][e] = 0.f;
   for (uint32_t k = k0; k < k1; ++k) {
-    int32_t a = offA, b = offB;
-    bool ok = true;
+    if (d.g_inv1) {
+      // gathers and B independent of slot 1: one validity test and one B vector per term
+      int32_t a = offA, b = offB;
+      bool ok = true;
 #pragma unroll
-    for (int g = 0; g < SV_G; ++g) {
-      if (g < d.nga) {
+      for (int g = 0; g < NG; ++g) {
         int32_t x = gidx[g];
         if (d.gwrap[g]) x = sv_mod(x, d.gext[g]);
         ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[g]);
-        a += x * d.gstride[g];
+        if (d.gop[g])
+          b += x * d.gstride[g];
+        else
+          a += x * d.gstride[g];
       }
-      if (g < d.ngb) {
-        int32_t x = gidx[SV_G + g];
-        if (d.gwrap[SV_G + g]) x = sv_mod(x, d.gext[SV_G + g]);
-        ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[SV_G + g]);
-        b += x * d.gstride[SV_G + g];
-      }
-    }
-    if (ok) {
-      if (VEC == 1) {
-        acc[0] += d.unary ? __ldg(A + a) : __ldg(A + a) * __ldg(B + b);
-      } else {
-        float xa[4];
-        if (d.a_bcast) {
-          xa[0] = xa[1] = xa[2] = xa[3] = __ldg(A + a);
-        } else {
-          const float4 va = __ldg(reinterpret_cast<const float4*>(A + a));
-          xa[0] = va.x;
-          xa[1] = va.y;
-          xa[2] = va.z;
-          xa[3] = va.w;
-        }
-        if (d.unary) {
+      if (ok) {
+        float xb[4] = {1.f, 1.f, 1.f, 1.f};
+        if (!d.unary && d.b_inv1) xb4(d, B + b, full0, lane0, xb);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[e] += xa[e];
-        } else if (d.vec_b) {
-          const float4 vb = __ldg(reinterpret_cast<const float4*>(B + b));
-          acc[0] += xa[0] * vb.x;
-          acc[1] += xa[1] * vb.y;
-          acc[2] += xa[2] * vb.z;
-          acc[3] += xa[3] * vb.w;
-        } else {
+        for (int jj = 0; jj < J; ++jj) {
+          if (jj >= nj) break;
+          float xa[4];
+          xa4(d, A + a + jj * sa1, xa);
+          if (!d.unary && !d.b_inv1) xb4(d, B + b + jj * sb1, full0, lane0, xb);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e)
-            if (lane0 + e < d.lext) acc[e] += xa[e] * __ldg(B + b + e * sb0);
+          for (int e = 0; e < 4; ++e) acc[jj][e] += xa[e] * xb[e];
         }
       }
+    } else if (d.bfix1) {
+      // B (and its gathers) independent of slot 1, only A's gathers move with it (the
+      // depthwise filter gradient: dY[b,h,w,r] shared by the taps of X[b,h+kh-1,w,r])
+      int32_t b = offB;
+      bool okb = true;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        if (!d.gop[g]) continue;
+        int32_t x = gidx[g];
+        if (d.gwrap[g]) x = sv_mod(x, d.gext[g]);
+        okb = okb && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[g]);
+        b += x * d.gstride[g];
+      }
+      if (okb) {
+        float xb[4] = {1.f, 1.f, 1.f, 1.f};
+        if (!d.unary) xb4(d, B + b, full0, lane0, xb);
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) {
+          if (jj >= nj) break;
+          int32_t a = offA + jj * sa1;
+          bool ok = true;
+#pragma unroll
+          for (int g = 0; g < NG; ++g) {
+            if (d.gop[g]) continue;
+            int32_t x = gidx[g] + jj * d.go[g][1];
+            if (d.gwrap[g]) x = sv_mod(x, d.gext[g]);
+            ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[g]);
+            a += x * d.gstride[g];
+          }
+          if (!ok) continue;
+          float xa[4];
+          xa4(d, A + a, xa);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[jj][e] += xa[e] * xb[e];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < J; ++jj) {
+        if (jj >= nj) break;
+        int32_t a = offA + jj * sa1, b = offB + jj * sb1;
+        bool ok = true;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          int32_t x = gidx[g] + jj * d.go[g][1];
+          if (d.gwrap[g]) x = sv_mod(x, d.gext[g]);
+          ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[g]);
+          if (d.gop[g])
+            b += x * d.gstride[g];
+          else
+            a += x * d.gstride[g];
+        }
+        if (!ok) continue;
+        float xa[4], xb[4] = {1.f, 1.f, 1.f, 1.f};
+        xa4(d, A + a, xa);
+        if (!d.unary) xb4(d, B + b, full0, lane0, xb);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[jj][e] += xa[e] * xb[e];
+      }
     }
-    // K odometer (slot 0 fastest); the gathered indices move with it
+    // K odometer
 #pragma unroll
     for (int j = 0; j < SV_K; ++j) {
       if (j < d.nk) {
@@ -304,55 +551,60 @@ __global__ void __launch_bounds__(256) ce_stream_kernel(const SvDesc d, const fl
           offA += d.ksa[j];
           offB += d.ksb[j];
 #pragma unroll
-          for (int g = 0; g < 2 * SV_G; ++g) gidx[g] += d.gk[g][j];
+          for (int g = 0; g < NG; ++g) gidx[g] += d.gk[g][j];
           break;
         }
         const int32_t back = d.kext[j] - 1;
         offA -= back * d.ksa[j];
         offB -= back * d.ksb[j];
 #pragma unroll
-        for (int g = 0; g < 2 * SV_G; ++g) gidx[g] -= back * d.gk[g][j];
+        for (int g = 0; g < NG; ++g) gidx[g] -= back * d.gk[g][j];
         kv[j] = 0;
       }
     }
   }
-  if (VEC == 4 && d.vec_c) {
-    float4* cp = reinterpret_cast<float4*>(C + offC);
-    const float4 v = make_float4(acc[0], acc[1], acc[2], acc[VEC - 1]);
-    if (d.mode == 2) {
-      asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(cp), "f"(v.x), "f"(v.y),
-                   "f"(v.z), "f"(v.w)
-                   : "memory");
-    } else if (d.mode == 1) {
-      float4 c = *cp;
-      c.x += v.x;
-      c.y += v.y;
-      c.z += v.z;
-      c.w += v.w;
-      *cp = c;
-    } else {
-      *cp = v;
-    }
-  } else {
-    const int32_t sc0 = d.osc[0];
+  const int32_t sc1 = d.osc[1], sc0 = d.osc[0];
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      if (VEC > 1 && lane0 + e >= d.lext) break;
-      float* cp = C + offC + e * sc0;
-      if (d.mode == 2)
-        atomicAdd(cp, acc[e]);
-      else if (d.mode == 1)
-        *cp += acc[e];
-      else
-        *cp = acc[e];
+  for (int jj = 0; jj < J; ++jj) {
+    if (jj >= nj) break;
+    const int32_t pc = offC + jj * sc1;
+    if (d.vec_c) {
+      float4* cp = reinterpret_cast<float4*>(C + pc);
+      const float4 v = make_float4(acc[jj][0], acc[jj][1], acc[jj][2], acc[jj][3]);
+      if (d.mode == 2) {
+        asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(cp), "f"(v.x), "f"(v.y),
+                     "f"(v.z), "f"(v.w)
+                     : "memory");
+      } else if (d.mode == 1) {
+        float4 c = *cp;
+        c.x += v.x;
+        c.y += v.y;
+        c.z += v.z;
+        c.w += v.w;
+        *cp = c;
+      } else {
+        *cp = v;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (lane0 + e >= d.lext) break;
+        float* cp = C + pc + e * sc0;
+        if (d.mode == 2)
+          atomicAdd(cp, acc[jj][e]);
+        else if (d.mode == 1)
+          *cp += acc[jj][e];
+        else
+          *cp = acc[jj][e];
+      }
     }
   }
 }
 
-
 // K-lane mode: a warp per output, lanes striding the K range (for steps whose streamed
 // operand is contiguous along a K var, e.g. the input gradient of RTR's first node:
 // 900 contiguous terms per output), combined with a warp-shuffle tree.
+template <int NG>
 __global__ void __launch_bounds__(256) ce_stream_klane_kernel(const SvDesc d, const float* __restrict__ A,
                                                               const float* __restrict__ B, float* __restrict__ C) {
   ce_pdl_enter();
@@ -360,9 +612,9 @@ __global__ void __launch_bounds__(256) ce_stream_klane_kernel(const SvDesc d, co
   const int lane = threadIdx.x & 31;
   if (o >= d.outs) return;  // warp-uniform
   int32_t offA = 0, offB = 0, offC = 0;
-  int32_t gbase[2 * SV_G];
+  int32_t gbase[NG > 0 ? NG : 1];
 #pragma unroll
-  for (int g = 0; g < 2 * SV_G; ++g) gbase[g] = d.gc[g];
+  for (int g = 0; g < NG; ++g) gbase[g] = d.gc[g];
   uint32_t rest = o;
 #pragma unroll
   for (int i = 0; i < SV_O; ++i) {
@@ -374,7 +626,7 @@ __global__ void __launch_bounds__(256) ce_stream_klane_kernel(const SvDesc d, co
       offB += v * d.osb[i];
       offC += v * d.osc[i];
 #pragma unroll
-      for (int g = 0; g < 2 * SV_G; ++g) gbase[g] += v * d.go[g][i];
+      for (int g = 0; g < NG; ++g) gbase[g] += v * d.go[g][i];
     }
   }
   const uint32_t k0 = blockIdx.y * d.kper;
@@ -382,9 +634,9 @@ __global__ void __launch_bounds__(256) ce_stream_klane_kernel(const SvDesc d, co
   float acc = 0.f;
   for (uint32_t k = k0 + lane; k < k1; k += 32) {
     int32_t a = offA, b = offB;
-    int32_t gidx[2 * SV_G];
+    int32_t gidx[NG > 0 ? NG : 1];
 #pragma unroll
-    for (int g = 0; g < 2 * SV_G; ++g) gidx[g] = gbase[g];
+    for (int g = 0; g < NG; ++g) gidx[g] = gbase[g];
     uint32_t r = k;
 #pragma unroll
     for (int j = 0; j < SV_K; ++j) {
@@ -395,24 +647,19 @@ __global__ void __launch_bounds__(256) ce_stream_klane_kernel(const SvDesc d, co
         a += v * d.ksa[j];
         b += v * d.ksb[j];
 #pragma unroll
-        for (int g = 0; g < 2 * SV_G; ++g) gidx[g] += v * d.gk[g][j];
+        for (int g = 0; g < NG; ++g) gidx[g] += v * d.gk[g][j];
       }
     }
     bool ok = true;
 #pragma unroll
-    for (int g = 0; g < SV_G; ++g) {
-      if (g < d.nga) {
-        int32_t x = gidx[g];
-        if (d.gwrap[g]) x = sv_mod(x, d.gext[g]);
-        ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[g]);
+    for (int g = 0; g < NG; ++g) {
+      int32_t x = gidx[g];
+      if (d.gwrap[g]) x = sv_mod(x, d.gext[g]);
+      ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[g]);
+      if (d.gop[g])
+        b += x * d.gstride[g];
+      else
         a += x * d.gstride[g];
-      }
-      if (g < d.ngb) {
-        int32_t x = gidx[SV_G + g];
-        if (d.gwrap[SV_G + g]) x = sv_mod(x, d.gext[SV_G + g]);
-        ok = ok && static_cast<uint32_t>(x) < static_cast<uint32_t>(d.gext[SV_G + g]);
-        b += x * d.gstride[SV_G + g];
-      }
     }
     if (ok) acc += d.unary ? __ldg(A + a) : __ldg(A + a) * __ldg(B + b);
   }
@@ -503,6 +750,24 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
     ov.erase(std::find(ov.begin(), ov.end(), lane));
     ov.insert(ov.begin(), lane);
   }
+  // slot 1 (blocked 4x per thread in the register-blocked kernel): prefer a var outside
+  // every gather that B does not depend on, so one validity test and one B vector serve
+  // the 4 outputs; among those the smallest out stride
+  if (ov.size() > 2) {
+    auto in_gather = [&](int v) { return gathered(v); };
+    std::size_t best1 = 1;
+    int score1 = -1;
+    for (std::size_t i = 1; i < ov.size(); ++i) {
+      const int v = ov[i];
+      const int sc = (in_gather(v) ? 0 : 2) + (p.sb[v] == 0 ? 1 : 0);
+      if (sc > score1) {
+        score1 = sc;
+        best1 = i;
+      }
+    }
+    std::rotate(ov.begin() + 1, ov.begin() + static_cast<std::ptrdiff_t>(best1),
+                ov.begin() + static_cast<std::ptrdiff_t>(best1) + 1);
+  }
   // K vars: fastest in A first
   std::stable_sort(kvars.begin(), kvars.end(), [&](int x, int y) {
     const int64_t sx = astride(x) ? astride(x) : p.sb[x], sy = astride(y) ? astride(y) : p.sb[y];
@@ -541,7 +806,8 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
     const int ng = side ? p.ng_b : p.ng_a;
     const CeGather* gs = side ? p.gb : p.ga;
     for (int g = 0; g < ng; ++g) {
-      const int slot = side * SV_G + g;
+      const int slot = d.ng++;
+      d.gop[slot] = side;
       const CeGather& G = gs[g];
       if (G.extent >= (1ll << 30) || std::llabs(G.c) >= (1ll << 30)) return false;
       d.gc[slot] = static_cast<int32_t>(G.c);
@@ -569,24 +835,24 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
     // A (the last float4 reads the row's padding) and masks B loads / C stores past it
     auto al = [](const float* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
     const int32_t ext0 = d.nout >= 1 ? d.oext[0] : 0, ext4 = (ext0 + 3) / 4 * 4;
-    auto padded = [&](const int32_t* os, const int32_t* ks, int gbase, int ng) {
+    auto padded = [&](const int32_t* os, const int32_t* ks, int gbase) {
       for (int i = 1; i < d.nout; ++i)
         if (os[i] % 4 || (os[i] && os[i] < ext4)) return false;
       for (int j = 0; j < d.nk; ++j)
         if (ks && (ks[j] % 4 || (ks[j] && ks[j] < ext4))) return false;
-      for (int g = 0; g < ng; ++g)
-        if (d.gstride[gbase + g] % 4 || d.gstride[gbase + g] < ext4) return false;
+      for (int g = 0; g < d.ng; ++g)
+        if (d.gop[g] == gbase && (d.gstride[g] % 4 || d.gstride[g] < ext4)) return false;
       return true;
     };
     // A along the lane var: unit stride (float4) or independent of it (one scalar, broadcast)
     const bool a_b = d.nout >= 1 && d.osa[0] == 0;
-    bool ok = d.nout >= 1 && (a_b || (al(A) && d.osa[0] == 1 && padded(d.osa, d.ksa, 0, p.ng_a)));
+    bool ok = d.nout >= 1 && (a_b || (al(A) && d.osa[0] == 1 && padded(d.osa, d.ksa, 0)));
     for (int g = 0; g < 2 * SV_G && ok; ++g) ok = d.go[g][0] == 0;
     d.a_bcast = a_b ? 1 : 0;
     d.vec = ok ? 1 : 0;
     if (ok) {
-      const bool vb = !p.unary && al(B) && d.osb[0] == 1 && padded(d.osb, d.ksb, SV_G, p.ng_b);
-      const bool vc = al(C) && d.osc[0] == 1 && padded(d.osc, nullptr, 0, 0);
+      const bool vb = !p.unary && al(B) && d.osb[0] == 1 && padded(d.osb, d.ksb, 1);
+      const bool vc = al(C) && d.osc[0] == 1 && padded(d.osc, nullptr, 2);
       d.vec_b = vb ? 1 : 0;
       d.vec_c = vc ? 1 : 0;
       d.lext = ext0;
@@ -597,8 +863,28 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
   }
   const int64_t lim = (1ll << 31) - 1;
   if (outs > lim || K > lim || maxA > lim || maxB > lim || maxC > lim) return false;
-  d.outs = static_cast<uint32_t>(outs);
   d.K = static_cast<uint32_t>(K);
+  // several consecutive values of output slot 1 per thread when K is short: the index
+  // decoding (~10 instructions per var) otherwise dominates a 3-term stencil
+  d.jrep = 1;
+  d.l1ext = d.nout > 1 ? d.oext[1] : 1;
+  if (!klane && d.vec && d.nout > 1 && K <= 32 && outs >= 148 * 256 * 8) {
+    d.jrep = 4;
+    d.oext[1] = (d.l1ext + 3) / 4;
+    d.odiv[1] = tc_div(static_cast<uint32_t>(d.oext[1]));
+    outs = outs / d.l1ext * d.oext[1];
+  }
+  d.outs = static_cast<uint32_t>(outs);
+  d.g_inv1 = d.b_inv1 = d.bfix1 = 0;
+  if (d.nout > 1) {
+    bool gi = true;
+    for (int g = 0; g < d.ng; ++g) gi = gi && d.go[g][1] == 0;
+    d.g_inv1 = gi ? 1 : 0;
+    d.b_inv1 = d.osb[1] == 0 ? 1 : 0;
+    bool bf = d.b_inv1 != 0;
+    for (int g = 0; g < d.ng; ++g) bf = bf && (d.gop[g] == 0 || d.go[g][1] == 0);
+    d.bfix1 = bf ? 1 : 0;
+  }
   // K slices: enough CTAs for ~8 per SM when the outputs alone do not fill the GPU,
   // each thread keeping >= 32 K terms
   const int64_t blocks = klane ? (outs + 7) / 8 : (outs + 255) / 256;
@@ -621,10 +907,33 @@ cudaError_t sv_launch(const SvDesc& d, int64_t span, bool zero_first, const floa
     if (e != cudaSuccess) return e;
   }
   const unsigned gy = d.K ? (d.K + d.kper - 1) / d.kper : 1u;
-  if (d.klane) return ce_launch(ce_stream_klane_kernel, dim3((d.outs + 7u) / 8u, gy), dim3(256), 0, s, d, A, B, C);
-  const unsigned gx = (d.outs + 255u) / 256u;
-  if (d.vec) return ce_launch(ce_stream_kernel<4>, dim3(gx, gy), dim3(256), 0, s, d, A, B, C);
-  return ce_launch(ce_stream_kernel<1>, dim3(gx, gy), dim3(256), 0, s, d, A, B, C);
+  const dim3 gk((d.outs + 7u) / 8u, gy), g1((d.outs + 255u) / 256u, gy), blk(256);
+  if (d.vec && d.jrep == 4) {
+    switch (d.ng) {
+      case 0: return ce_launch(ce_stream_blk_kernel<0>, g1, blk, 0, s, d, A, B, C);
+      case 1: return ce_launch(ce_stream_blk_kernel<1>, g1, blk, 0, s, d, A, B, C);
+      case 2: return ce_launch(ce_stream_blk_kernel<2>, g1, blk, 0, s, d, A, B, C);
+      case 3: return ce_launch(ce_stream_blk_kernel<3>, g1, blk, 0, s, d, A, B, C);
+      default: return ce_launch(ce_stream_blk_kernel<4>, g1, blk, 0, s, d, A, B, C);
+    }
+  }
+  switch (d.klane ? 10 + d.ng : d.vec ? 20 + d.ng : d.ng) {
+    case 10: return ce_launch(ce_stream_klane_kernel<0>, gk, blk, 0, s, d, A, B, C);
+    case 11: return ce_launch(ce_stream_klane_kernel<1>, gk, blk, 0, s, d, A, B, C);
+    case 12: return ce_launch(ce_stream_klane_kernel<2>, gk, blk, 0, s, d, A, B, C);
+    case 13: return ce_launch(ce_stream_klane_kernel<3>, gk, blk, 0, s, d, A, B, C);
+    case 14: return ce_launch(ce_stream_klane_kernel<4>, gk, blk, 0, s, d, A, B, C);
+    case 20: return ce_launch(ce_stream_kernel<4, 0>, g1, blk, 0, s, d, A, B, C);
+    case 21: return ce_launch(ce_stream_kernel<4, 1>, g1, blk, 0, s, d, A, B, C);
+    case 22: return ce_launch(ce_stream_kernel<4, 2>, g1, blk, 0, s, d, A, B, C);
+    case 23: return ce_launch(ce_stream_kernel<4, 3>, g1, blk, 0, s, d, A, B, C);
+    case 24: return ce_launch(ce_stream_kernel<4, 4>, g1, blk, 0, s, d, A, B, C);
+    case 0: return ce_launch(ce_stream_kernel<1, 0>, g1, blk, 0, s, d, A, B, C);
+    case 1: return ce_launch(ce_stream_kernel<1, 1>, g1, blk, 0, s, d, A, B, C);
+    case 2: return ce_launch(ce_stream_kernel<1, 2>, g1, blk, 0, s, d, A, B, C);
+    case 3: return ce_launch(ce_stream_kernel<1, 3>, g1, blk, 0, s, d, A, B, C);
+    default: return ce_launch(ce_stream_kernel<1, 4>, g1, blk, 0, s, d, A, B, C);
+  }
 }
 
 // ----------------------------------------------------------------------------- tiled
