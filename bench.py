@@ -177,7 +177,7 @@ def main():
 
     import paper_2401_03384_b200 as ce
     from paper_2401_03384_b200.device import Context, Executor
-    from paper_2401_03384_b200.parallel import allreduce_factor_grads
+    from paper_2401_03384_b200.parallel import allreduce_factor_grads, allreduce_factor_grads_async
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -203,14 +203,21 @@ def main():
 
     def one_step(collect=None):
         launches = 0
+        works = []
         for l in layers:
             l["ex"].execute(l["xs"], l["out"])
             launches += l["ex"].stats.kernels_launched
             grads = l["ex"].backward(l["xs"], l["dout"])
             launches += l["ex"].stats.kernels_launched
-            if world > 1:  # factor gradients only (one bucketed NCCL all-reduce); X gradients stay sharded
-                grads = allreduce_factor_grads(grads)
+            if world > 1:
+                # factor gradients only (one bucketed NCCL all-reduce per layer, overlapping the
+                # next layer's work); X gradients stay sharded
+                grads, work = allreduce_factor_grads_async(grads)
+                works.append(work)
             l["grads"] = grads
+        for w in works:  # the step ends when every factor gradient is reduced
+            if w is not None:
+                w.wait()
         return launches
 
     for _ in range(args.warmup):

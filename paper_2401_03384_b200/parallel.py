@@ -37,20 +37,32 @@ def allreduce_factor_grads(grads: Sequence[Optional[torch.Tensor]], group=None,
 
     Factor gradients of one layer are flattened into a single buffer so the layer
     costs one collective (bucketed like DDP), then scattered back in place."""
+    out, work = allreduce_factor_grads_async(grads, group, skip)
+    if work is not None:
+        work.wait()
+    return out
+
+
+def allreduce_factor_grads_async(grads: Sequence[Optional[torch.Tensor]], group=None,
+                                 skip: Sequence[int] = (0,)):
+    """As allreduce_factor_grads, but returns (views, work) without ordering the caller's
+    stream after the collective: the next layer's backward overlaps it, and
+    `work.wait()` (stream-side, no host sync) orders whatever reads the reduced
+    gradients.  work is None when there is nothing to reduce."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
-        return list(grads)
+        return list(grads), None
     idx = [i for i, g in enumerate(grads) if g is not None and i not in skip]
     if not idx:
-        return list(grads)
+        return list(grads), None
     flat = torch.cat([grads[i].reshape(-1) for i in idx])
-    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    work = dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group, async_op=True)
     out = list(grads)
     pos = 0
     for i in idx:
         n = grads[i].numel()
         out[i] = flat[pos:pos + n].view_as(grads[i])
         pos += n
-    return out
+    return out, work
 
 
 def init_ce_comm(ctx, group=None) -> None:

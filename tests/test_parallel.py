@@ -97,6 +97,42 @@ def test_gloo_world2_matches_full_batch():
             np.testing.assert_allclose(r[2][i], grads[i].numpy(), rtol=1e-10, atol=1e-12)
 
 
+def _async_worker(rank, world, port, result_q):
+    import os
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2401_03384_b200.parallel import allreduce_factor_grads_async
+    grads = [torch.full((3,), float(rank)), torch.arange(4.0) * (rank + 1), None, torch.ones(2, 2) * rank]
+    out, work = allreduce_factor_grads_async(grads)
+    assert work is not None
+    work.wait()
+    result_q.put((rank, [None if g is None else g.numpy() for g in out]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_async_allreduce():
+    """Asynchronous bucketed factor-gradient all-reduce (bench.py overlaps it with the next
+    layer): X (index 0) untouched, every factor gradient summed over the ranks."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_async_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, g in res:
+        np.testing.assert_array_equal(g[0], np.full(3, float(rank)))
+        np.testing.assert_array_equal(g[1], np.arange(4.0) * 3)
+        assert g[2] is None
+        np.testing.assert_array_equal(g[3], np.ones((2, 2)))
+
+
 def test_allreduce_is_identity_without_process_group():
     g = [torch.ones(3), torch.ones(2)]
     out = allreduce_factor_grads(g)
