@@ -35,8 +35,14 @@ for expr, dims in CASES:
         e1.record(st)
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    ms = sorted(ts)[len(ts) // 2]
+    ms_call = sorted(ts)[len(ts) // 2]
+    ex.set_profiling(True)
+    ex.execute([x])
+    prof = ex.profile(False)
+    ex.set_profiling(False)
+    ms = sum(p[2] for p in prof)
     nbytes = 2 * x.numel() * 4
     d = plan.describe_steps(False).splitlines()[0]
-    print(f"{expr:24s} {x.numel()*4/1e6:8.1f} MB  {ms*1e3:8.1f} us  {nbytes/(ms*1e-3)/1e9:7.0f} GB/s   {d}")
+    print(f"{expr:24s} {x.numel()*4/1e6:8.1f} MB  kernel {ms*1e3:8.1f} us  {nbytes/(ms*1e-3)/1e9:7.0f} GB/s"
+          f"  (call {ms_call*1e3:7.1f} us)  {d}")
     del ex
