@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <numeric>
 #include <cstdlib>
 #include <vector>
@@ -1275,10 +1276,14 @@ __global__ void __launch_bounds__(256, 8) ce_transpose64_kernel(const CePermDesc
 // Input and output share the unit-stride axis x: a strided copy of rows (x, y) per
 // batch slice.  A row is served by L = 2^lshift lanes (L >= min(ext x, 32)), so a warp
 // covers 32/L short rows without any per-element division; 4 rows per thread in flight.
+template <bool V4>
 __global__ void __launch_bounds__(256) ce_rowcopy_kernel(const CePermDesc d, const float* __restrict__ A,
                                                          float* __restrict__ C, int lshift) {
+  // V4: rows are 16-B aligned multiples of 4 floats on both sides -> float4 traffic
   ce_pdl_enter();
-  const uint32_t ex = static_cast<uint32_t>(d.ext[d.vin]), ey = static_cast<uint32_t>(d.ext[d.vout]);
+  using T = typename std::conditional<V4, float4, float>::type;
+  constexpr int W = V4 ? 4 : 1;
+  const uint32_t ex = static_cast<uint32_t>(d.ext[d.vin]) / W, ey = static_cast<uint32_t>(d.ext[d.vout]);
   const int64_t sa_y = d.sa[d.vout], sc_y = d.sc[d.vout];
   const uint32_t L = 1u << lshift, lx = threadIdx.x & (L - 1), rows = 256u >> lshift;
   const uint32_t ly = threadIdx.x >> lshift;
@@ -1293,16 +1298,16 @@ __global__ void __launch_bounds__(256) ce_rowcopy_kernel(const CePermDesc d, con
     }
     for (uint32_t yb = blockIdx.x * rows * 4; yb < ey; yb += gridDim.x * rows * 4) {
       for (uint32_t x = lx; x < ex; x += L) {
-        float v[4];
+        T v[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint32_t y = yb + ly + j * rows;
-          v[j] = y < ey ? __ldg(A + bin + static_cast<int64_t>(y) * sa_y + x) : 0.f;
+          if (y < ey) v[j] = __ldg(reinterpret_cast<const T*>(A + bin + static_cast<int64_t>(y) * sa_y) + x);
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint32_t y = yb + ly + j * rows;
-          if (y < ey) C[bout + static_cast<int64_t>(y) * sc_y + x] = v[j];
+          if (y < ey) reinterpret_cast<T*>(C + bout + static_cast<int64_t>(y) * sc_y)[x] = v[j];
         }
       }
     }
@@ -1466,14 +1471,19 @@ cudaError_t ce_launch_permute(const CeProblem& p, const float* A, float* C, cuda
   CePermDesc d;
   if (!perm_desc(p, &d)) return cudaErrorInvalidValue;
   if (d.same) {
+    bool v4 = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
+              d.ext[d.vin] % 4 == 0 && d.sa[d.vout] % 4 == 0 && d.sc[d.vout] % 4 == 0;
+    for (int i = 0; i < d.nrest; ++i) v4 = v4 && d.sa[d.rest[i]] % 4 == 0 && d.sc[d.rest[i]] % 4 == 0;
+    const int64_t ex = d.ext[d.vin] / (v4 ? 4 : 1);
     int lshift = 0;
-    while (lshift < 5 && (1ll << lshift) < d.ext[d.vin]) ++lshift;
+    while (lshift < 5 && (1ll << lshift) < ex) ++lshift;
     const int64_t rows_per_cta = (256 >> lshift) * 4;
     const int64_t per_slice = (d.ext[d.vout] + rows_per_cta - 1) / rows_per_cta;
     const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(per_slice, (148 * 16 + d.nbatch - 1) / d.nbatch));
     const int64_t gy = std::min<int64_t>(d.nbatch, 65535);
-    return ce_launch(ce_rowcopy_kernel, dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), dim3(256), 0, s, d,
-                     A, C, lshift);
+    const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
+    if (v4) return ce_launch(ce_rowcopy_kernel<true>, grid, dim3(256), 0, s, d, A, C, lshift);
+    return ce_launch(ce_rowcopy_kernel<false>, grid, dim3(256), 0, s, d, A, C, lshift);
   }
   const int64_t ein = d.ext[d.vin] * (d.vin2 >= 0 ? d.ext[d.vin2] : 1);
   const int64_t eout = d.ext[d.vout] * (d.vout2 >= 0 ? d.ext[d.vout2] : 1);
