@@ -278,25 +278,33 @@ def main():
     def e2e_step():
         h2d_stream.wait_stream(stream)  # previous users of the device input buffers are done
         d2h_stream.wait_stream(stream)
-        uploaded = []
+        up_fwd, up_bwd = [], []
         with torch.cuda.stream(h2d_stream):
+            # per layer: the forward's inputs first, then dY (needed only by the backward)
             for (hin, hd, hout, hg, din, ddout) in pinned:
                 for d, h in zip(din, hin):
                     d.copy_(h, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d_stream)
+                up_fwd.append(ev)
                 ddout.copy_(hd, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d_stream)
-                uploaded.append(ev)
-        for l, (hin, hd, hout, hg, din, ddout), ev in zip(layers, pinned, uploaded):
-            stream.wait_event(ev)
+                up_bwd.append(ev)
+        for l, (hin, hd, hout, hg, din, ddout), ef, eb in zip(layers, pinned, up_fwd, up_bwd):
+            stream.wait_event(ef)
             with torch.cuda.stream(stream):
                 out = l["ex"].execute(din, l["out"])
+            d2h_stream.wait_stream(stream)
+            with torch.cuda.stream(d2h_stream):
+                hout.copy_(out, non_blocking=True)  # overlaps this layer's backward
+            stream.wait_event(eb)
+            with torch.cuda.stream(stream):
                 grads = l["ex"].backward(din, ddout)
                 if world > 1:
                     grads = allreduce_factor_grads(grads)
             d2h_stream.wait_stream(stream)
             with torch.cuda.stream(d2h_stream):
-                hout.copy_(out, non_blocking=True)
                 for h, g in zip(hg, grads):
                     h.copy_(g, non_blocking=True)
                     g.record_stream(d2h_stream)
