@@ -228,7 +228,8 @@ __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
                : "memory");
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
+// Named barrier of one epilogue warp group (ids 1 and 2).
+__device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(32 * kEpiWarps) : "memory"); }
 
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -378,12 +379,13 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  float* stage_out = reinterpret_cast<float*>(sB + STAGES * B_BYTES);  // [kEpiWarps][32][kStagePitch]
-  int64_t* col_off = reinterpret_cast<int64_t*>(stage_out + kEpiWarps * 32 * kStagePitch);  // [2][BN]
+  constexpr int EPI_GROUPS = BN == 64 ? 2 : 1;  // small tiles: a second epilogue warp group
+  float* stage_out = reinterpret_cast<float*>(sB + STAGES * B_BYTES);  // [EPI_GROUPS*kEpiWarps][32][kStagePitch]
+  int64_t* col_off = reinterpret_cast<int64_t*>(stage_out + EPI_GROUPS * kEpiWarps * 32 * kStagePitch);  // [2][BN]
   int64_t* grp_off = col_off + 2 * BN;                                  // [2][BN/4]: 16-B column groups
   int64_t* row_tab = grp_off + 2 * (BN / 4);                            // [2][128]: row offsets in C
-  Tile* tiles = reinterpret_cast<Tile*>(row_tab + 2 * TC_BM);           // [0] producer, [1] epilogue
-  uint64_t* full = reinterpret_cast<uint64_t*>(tiles + 2);
+  Tile* tiles = reinterpret_cast<Tile*>(row_tab + 2 * TC_BM);           // [0] producer, [1+g] epilogue group g
+  uint64_t* full = reinterpret_cast<uint64_t*>(tiles + 4);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;       // [2]
@@ -633,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       }
       stamp(P, 3);
     }
-  } else if (warp >= 2 + kEpiWarps) {
+  } else if (warp >= 2 + kEpiWarps && (xpose || EPI_GROUPS == 1)) {
     // ------------------------------------------------------------ transposer warps
     // MN-major operand boxes -> K-major layout in place, then hand the stage to the MMA.
     if (xpose) {
@@ -667,10 +669,14 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     // tables (overlapping the MMAs), then each warp drains its TMEM lane quarter 32 columns
     // at a time.  Columns that are contiguous and 16-B aligned in C (the padded channel-
     // last intermediates) go out as 128-bit stores; anything else element by element.
+    // BN=64 without MN-major operands: the transposer warps form a second group; group g
+    // drains accumulator g (alternate tiles), so two tiles' epilogues are in flight
+    const int ngrp = (EPI_GROUPS == 2 && !xpose) ? 2 : 1;
+    const int grp = warp >= 2 + kEpiWarps ? 1 : 0;
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;     // accumulator row owned by this thread
-    const int ew = warp - 2;           // 0..3
-    const int et = threadIdx.x - 64;   // 0..127
+    const int ew = warp - 2;           // 0..7
+    const int et = threadIdx.x - 64 - grp * 32 * kEpiWarps;  // 0..127 within the group
     float* stage = stage_out + ew * 32 * kStagePitch;
 
     const int dbg = Pg.dbg;
@@ -678,7 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     const bool tstore = P.transpose_store != 0;
     const bool c_al = (reinterpret_cast<uintptr_t>(C) & 15u) == 0;
     uint32_t local = 0;
-    Tile& T = tiles[1];
+    Tile& T = tiles[1 + grp];
     int cols_for[2] = {-1, -1};  // N tile whose column tables each accumulator buffer holds
     WorkIter wi;
     work_begin(P, group, ngroups, wi);
@@ -687,8 +693,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     bool atomic;
     for (; work_next(P, ngroups, wi, item, k0, k1, atomic); ++local) {
       const int acc = static_cast<int>(local & 1);
+      if (ngrp == 2 && acc != grp) continue;  // the other group's tile
       if (et == 0) decode_work(P, item, rank, csize, T);
-      epi_bar();  // decoded tile visible (and the previous tile's tables are no longer read)
+      epi_bar(1 + grp);  // decoded tile visible (and the previous tile's tables are no longer read)
       // address tables for this tile (overlaps the MMAs)
       int64_t* cols = col_off + acc * BN;
       int64_t* gcol = grp_off + acc * (BN / 4);
@@ -707,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       // are built once per accumulator buffer
       if (T.ntile != cols_for[acc]) {
         for (int c = et; c < BN; c += 32 * kEpiWarps) cols[c] = c < n_cols ? tile_offset(P, P.nt, P.nn, T.val, c) : -1;
-        epi_bar();
+        epi_bar(1 + grp);
         for (int g = et; g < BN / 4; g += 32 * kEpiWarps) {
           const int64_t c0 = cols[4 * g];
           const bool ok = c_al && c0 >= 0 && (c0 & 3) == 0 && cols[4 * g + 1] == c0 + 1 && cols[4 * g + 2] == c0 + 2 &&
@@ -719,7 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       const int64_t ro = row < m_rows ? tile_offset(P, P.mt, P.nm, T.val, row) : -1;
       const int64_t roff = ro < 0 ? -1 : base + ro;  // row offset in C, -1 outside the tile
       rtab[row] = roff;
-      epi_bar();  // tables visible to all epilogue warps
+      epi_bar(1 + grp);  // tables visible to all epilogue warps
       if ((dbg & 32) && et == 0 && local == 0) stamp(P, 10);
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       if ((dbg & 32) && et == 0 && local == 0) stamp(P, 4);
@@ -902,8 +909,8 @@ int sm_count() {
 template <int BN, int STAGES, bool PAIR>
 cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
   constexpr int smem =
-      STAGES * (TC_BM * 128 + (PAIR ? BN * 64 : BN * 128)) + kEpiWarps * 32 * kStagePitch * 4 +
-      (2 * BN + 2 * (BN / 4) + 2 * TC_BM) * 8 + 2 * static_cast<int>(sizeof(Tile)) + 8 * (3 * STAGES + 4) + 16 + 64 +
+      STAGES * (TC_BM * 128 + (PAIR ? BN * 64 : BN * 128)) + (BN == 64 ? 2 : 1) * kEpiWarps * 32 * kStagePitch * 4 +
+      (2 * BN + 2 * (BN / 4) + 2 * TC_BM) * 8 + 4 * static_cast<int>(sizeof(Tile)) + 8 * (3 * STAGES + 4) + 16 + 64 +
       static_cast<int>(sizeof(TcParams)) + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static bool configured = false;
@@ -994,13 +1001,13 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
   }
   if (P.mcast == 2) {
     switch (plan.bn) {
-      case 64: return launch<64, 10, true>(P, C, s);
+      case 64: return launch<64, 9, true>(P, C, s);
       case 128: return launch<128, 8, true>(P, C, s);
       default: return launch<256, 6, true>(P, C, s);
     }
   }
   switch (plan.bn) {
-    case 64: return launch<64, 8, false>(P, C, s);
+    case 64: return launch<64, 7, false>(P, C, s);
     case 128: return launch<128, 6, false>(P, C, s);
     default: return launch<256, 4, false>(P, C, s);
   }

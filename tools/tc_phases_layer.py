@@ -13,9 +13,10 @@ from paper_2401_03384_b200 import _lib  # noqa: E402
 from paper_2401_03384_b200.device import Context, Executor  # noqa: E402
 
 kind, cr = sys.argv[1], float(sys.argv[2])
+SL = {"cp": 1, "tk": 2, "tt": 3, "tr": 4}
 ctx = Context(0, "auto", graphs=False)
 torch.cuda.set_stream(ctx.torch_stream)
-slots = {"tk": 2, "tt": 3, "cp": 1, "tr": 4}[kind]
+slots = SL[kind]
 le = ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, 128, [1] * slots), cr)
 plan = ce.optimal(le.expr, le.dims, "same", "training")
 ex = Executor(ctx, plan, backward=True)
