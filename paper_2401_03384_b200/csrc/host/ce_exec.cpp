@@ -284,7 +284,17 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
   Step st;
   st.node = node;
   st.label = label;
-  if (cfg_.math == 0 && !p.unary) {
+  // Tiny contractions (K <= 8, e.g. ResNet conv1's 3 input channels) with a large output
+  // are output-bandwidth problems: the streaming SIMT kernel writes them with float4
+  // stores and no per-tile epilogue, where the TC path would pad K to 32 and pay a
+  // ~5 us epilogue for every 128-row tile.
+  const bool tiny_k = [&] {
+    int64_t k = 1, outs = 1;
+    for (int v = 0; v < p.nv; ++v) (p.cls[v] == CE_K ? k : outs) *= p.ext[v];
+    for (int g = 0; g < p.ng_a; ++g) k *= 1;  // gathered taps are K vars already counted
+    return k <= 8 && outs >= (1ll << 20);
+  }();
+  if (cfg_.math == 0 && !p.unary && !tiny_k) {
     bool ok = ce_tc_plan(p, &st.tc);
     if (!ok) {
       // tf32 tensor cores need both operands K-major over the same K unit: repack
