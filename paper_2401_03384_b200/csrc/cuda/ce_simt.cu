@@ -181,6 +181,7 @@ struct SvDesc {
   int32_t a_bcast;                          // VEC=4 with A independent of the lane var
   int32_t jrep, l1ext;                      // output slot 1 values per thread, slot 1 extent
   int32_t g_inv1, b_inv1, bfix1;            // gathers / B / B and its gathers independent of slot 1
+  int32_t stencil;                          // depthwise stencil path: taps (0 = off)
   int32_t oext[SV_O];
   TcDiv odiv[SV_O];
   int32_t osa[SV_O], osb[SV_O], osc[SV_O];
@@ -602,6 +603,105 @@ __global__ void __launch_bounds__(256) ce_stream_blk_kernel(const SvDesc d, cons
   }
 }
 
+
+// Depthwise 1-D stencil (CP's `bhwr,rh->bhwr` family and its input-gradient adjoint):
+// one gathered A axis x = gc + SA*p + SB*q over the conv output var p (slot 1) and the tap
+// q (the only K var), B = F[lane, q].  A thread owns 4 lanes x J consecutive p: the
+// J+KT-1 input rows of its window are loaded once into registers (float4) and reused by
+// every tap -- a register sliding window instead of KT loads per output.
+template <int KT, int J, int SA, int SB>
+__global__ void __launch_bounds__(256) ce_dw_kernel(const SvDesc d, const float* __restrict__ A,
+                                                    const float* __restrict__ B, float* __restrict__ C) {
+  ce_pdl_enter();
+  const uint32_t o = blockIdx.x * 256u + threadIdx.x;
+  if (o >= d.outs) return;
+  int32_t offA = 0, offB = 0, offC = 0, lane0 = 0, p0 = 0;
+  int32_t x00 = d.gc[0];
+  uint32_t rest = o;
+#pragma unroll
+  for (int i = 0; i < SV_O; ++i) {
+    if (i < d.nout) {
+      const uint32_t q = tc_quo(rest, d.odiv[i]);
+      int32_t v = static_cast<int32_t>(rest - q * static_cast<uint32_t>(d.oext[i]));
+      rest = q;
+      if (i == 0) {
+        v *= 4;
+        lane0 = v;
+      } else if (i == 1) {
+        v *= J;
+        p0 = v;
+      }
+      offA += v * d.osa[i];
+      offB += v * d.osb[i];
+      offC += v * d.osc[i];
+      x00 += v * d.go[0][i];
+    }
+  }
+  // taps of this thread's 4 lanes
+  float bq[KT][4];
+  const float* pb = B + offB;
+  const int32_t sb0 = d.osb[0], ksb = d.ksb[0];
+#pragma unroll
+  for (int q = 0; q < KT; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) bq[q][e] = lane0 + e < d.lext ? __ldg(pb + q * ksb + e * sb0) : 0.f;
+  // window rows t = SA*jj + SB*q in [TMIN, TMAX]
+  constexpr int TMIN = (SA > 0 ? 0 : -(J - 1)) + (SB > 0 ? 0 : -(KT - 1));
+  constexpr int NW = J + KT - 1;
+  float4 rw[NW];
+  const int32_t gext = d.gext[0], gstr = d.gstride[0];
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int32_t x = x00 + TMIN + w;
+    if (static_cast<uint32_t>(x) < static_cast<uint32_t>(gext)) {
+      const float* pa = A + offA + x * gstr;
+      if (d.a_bcast) {
+        const float v = __ldg(pa);
+        rw[w] = make_float4(v, v, v, v);
+      } else {
+        rw[w] = __ldg(reinterpret_cast<const float4*>(pa));
+      }
+    } else {
+      rw[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  const int32_t sc1 = d.osc[1], sc0 = d.osc[0];
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    if (p0 + jj >= d.l1ext) break;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+    for (int q = 0; q < KT; ++q) {
+      const float4 r = rw[SA * jj + SB * q - TMIN];
+      a0 += r.x * bq[q][0];
+      a1 += r.y * bq[q][1];
+      a2 += r.z * bq[q][2];
+      a3 += r.w * bq[q][3];
+    }
+    const int32_t pc = offC + jj * sc1;
+    if (d.vec_c) {
+      float4* cp = reinterpret_cast<float4*>(C + pc);
+      if (d.mode == 1) {
+        float4 c = *cp;
+        *cp = make_float4(c.x + a0, c.y + a1, c.z + a2, c.w + a3);
+      } else {
+        *cp = make_float4(a0, a1, a2, a3);
+      }
+    } else {
+      const float av[4] = {a0, a1, a2, a3};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (lane0 + e >= d.lext) break;
+        float* cp = C + pc + e * sc0;
+        if (d.mode == 1)
+          *cp += av[e];
+        else
+          *cp = av[e];
+      }
+    }
+  }
+}
+
 // K-lane mode: a warp per output, lanes striding the K range (for steps whose streamed
 // operand is contiguous along a K var, e.g. the input gradient of RTR's first node:
 // 900 contiguous terms per output), combined with a warp-shuffle tree.
@@ -865,10 +965,43 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
   const int64_t lim = (1ll << 31) - 1;
   if (outs > lim || K > lim || maxA > lim || maxB > lim || maxC > lim) return false;
   d.K = static_cast<uint32_t>(K);
+  // depthwise stencil: a single tap K var, one gather on A over (conv output var, tap)
+  // with unit coefficients, B = F[lane, tap]
+  d.stencil = 0;
+  if (!klane && d.vec && !p.unary && d.ng == 1 && d.gop[0] == 0 && !d.gwrap[0] && d.nk == 1 &&
+      (d.kext[0] == 3 || d.kext[0] == 5 || d.kext[0] == 7) && (d.gk[0][0] == 1 || d.gk[0][0] == -1) &&
+      !p.accumulate) {
+    int sstar = -1, nz = 0;
+    for (int i = 1; i < d.nout; ++i)
+      if (d.go[0][i] != 0) {
+        ++nz;
+        sstar = i;
+      }
+    bool bok = true;
+    for (int i = 1; i < d.nout; ++i) bok = bok && d.osb[i] == 0;
+    if (nz == 1 && (d.go[0][sstar] == 1 || d.go[0][sstar] == -1) && d.osa[sstar] == 0 && bok) {
+      // move the conv output var to slot 1 (blocked J per thread)
+      auto sw = [&](int32_t* a) { std::swap(a[1], a[sstar]); };
+      sw(d.oext);
+      sw(d.osa);
+      sw(d.osb);
+      sw(d.osc);
+      std::swap(d.odiv[1], d.odiv[sstar]);
+      for (int g = 0; g < 2 * SV_G; ++g) sw(d.go[g]);
+      d.stencil = d.kext[0];
+    }
+  }
   // several consecutive values of output slot 1 per thread when K is short: the index
   // decoding (~10 instructions per var) otherwise dominates a 3-term stencil
   d.jrep = 1;
   d.l1ext = d.nout > 1 ? d.oext[1] : 1;
+  if (d.stencil) {
+    const int jb = d.stencil <= 3 ? 8 : 4;
+    d.jrep = jb;
+    d.oext[1] = (d.l1ext + jb - 1) / jb;
+    d.odiv[1] = tc_div(static_cast<uint32_t>(d.oext[1]));
+    outs = outs / d.l1ext * d.oext[1];
+  } else
   if (!klane && d.vec && d.nout > 1 && K <= 32 && outs >= 148 * 256 * 8) {
     d.jrep = 4;
     d.oext[1] = (d.l1ext + 3) / 4;
@@ -909,6 +1042,18 @@ cudaError_t sv_launch(const SvDesc& d, int64_t span, bool zero_first, const floa
   }
   const unsigned gy = d.K ? (d.K + d.kper - 1) / d.kper : 1u;
   const dim3 gk((d.outs + 7u) / 8u, gy), g1((d.outs + 255u) / 256u, gy), blk(256);
+  if (d.stencil) {
+    const int sa = d.go[0][1], sb = d.gk[0][0];
+#define CE_DW(KT, J)                                                                                     \
+  if (sa > 0 && sb > 0) return ce_launch(ce_dw_kernel<KT, J, 1, 1>, g1, blk, 0, s, d, A, B, C);          \
+  if (sa > 0 && sb < 0) return ce_launch(ce_dw_kernel<KT, J, 1, -1>, g1, blk, 0, s, d, A, B, C);         \
+  if (sa < 0 && sb > 0) return ce_launch(ce_dw_kernel<KT, J, -1, 1>, g1, blk, 0, s, d, A, B, C);         \
+  return ce_launch(ce_dw_kernel<KT, J, -1, -1>, g1, blk, 0, s, d, A, B, C);
+    if (d.stencil == 3) { CE_DW(3, 8) }
+    if (d.stencil == 5) { CE_DW(5, 4) }
+    CE_DW(7, 4)
+#undef CE_DW
+  }
   if (d.vec && d.jrep == 4) {
     switch (d.ng) {
       case 0: return ce_launch(ce_stream_blk_kernel<0>, g1, blk, 0, s, d, A, B, C);
