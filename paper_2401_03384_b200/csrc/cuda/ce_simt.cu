@@ -182,6 +182,7 @@ struct SvDesc {
   int32_t jrep, l1ext;                      // output slot 1 values per thread, slot 1 extent
   int32_t g_inv1, b_inv1, bfix1;            // gathers / B / B and its gathers independent of slot 1
   int32_t stencil;                          // depthwise stencil path: taps (0 = off)
+  int32_t dwgrad;                           // depthwise filter-gradient path: taps (0 = off)
   int32_t oext[SV_O];
   TcDiv odiv[SV_O];
   int32_t osa[SV_O], osb[SV_O], osc[SV_O];
@@ -702,6 +703,151 @@ __global__ void __launch_bounds__(256) ce_dw_kernel(const SvDesc d, const float*
   }
 }
 
+
+// Depthwise filter gradient (the reduce adjoint of the stencil): dF[lane, q] =
+// sum_k A[.., x = gc + SA*p + SB*q, .., lane] * B[.., p, .., lane] with p (the gathered
+// K var) fastest.  A thread owns 4 lanes x all KT taps over a K slice; the KT rows of A
+// live in a register window that shifts by one row per p step (4 steps' loads issued
+// together), so a K step costs one float4 of A, one of B and 4*KT FMAs.  Threads map
+// lane groups fastest (coalesced) then K slices; slices add atomically.
+template <int KT, int SA, int SB>
+__global__ void __launch_bounds__(256) ce_dwgrad_kernel(const SvDesc d, const float* __restrict__ A,
+                                                        const float* __restrict__ B, float* __restrict__ C) {
+  ce_pdl_enter();
+  const uint32_t t = blockIdx.x * 256u + threadIdx.x;
+  const uint32_t nslices = (d.K + d.kper - 1) / d.kper;
+  if (t >= d.outs * nslices) return;
+  const uint32_t slice = tc_quo(t, d.odiv[0]);
+  const uint32_t o = t - slice * d.outs;
+  const int32_t lane0 = static_cast<int32_t>(o) * 4;
+  const uint32_t k0 = slice * d.kper;
+  const uint32_t k1 = min(d.K, k0 + d.kper);
+  int32_t kv[SV_K];
+  int32_t offAk = 0, offBk = 0;
+  uint32_t rest = k0;
+#pragma unroll
+  for (int j = 0; j < SV_K; ++j) {
+    kv[j] = 0;
+    if (j < d.nk) {
+      const uint32_t q = tc_quo(rest, d.kdiv[j]);
+      kv[j] = static_cast<int32_t>(rest - q * static_cast<uint32_t>(d.kext[j]));
+      rest = q;
+      if (j > 0) {
+        offAk += kv[j] * d.ksa[j];
+        offBk += kv[j] * d.ksb[j];
+      }
+    }
+  }
+  const int32_t gext = d.gext[0], gstr = d.gstride[0], gc = d.gc[0], ext0 = d.kext[0], ksb0 = d.ksb[0];
+  const float* Al = A + lane0 * d.osa[0];
+  const float* Bl = B + lane0 * d.osb[0];
+  const bool full4 = lane0 + 4 <= d.lext;
+  const int32_t sb0 = d.osb[0];
+  auto row = [&](int32_t x) -> float4 {
+    if (static_cast<uint32_t>(x) >= static_cast<uint32_t>(gext)) return make_float4(0.f, 0.f, 0.f, 0.f);
+    return __ldg(reinterpret_cast<const float4*>(Al + offAk + x * gstr));
+  };
+  auto brow = [&](int32_t pp) -> float4 {
+    const float* pb = Bl + offBk + pp * ksb0;
+    if (d.vec_b) return __ldg(reinterpret_cast<const float4*>(pb));
+    float4 b;
+    b.x = __ldg(pb);
+    b.y = full4 || lane0 + 1 < d.lext ? __ldg(pb + sb0) : 0.f;
+    b.z = full4 || lane0 + 2 < d.lext ? __ldg(pb + 2 * sb0) : 0.f;
+    b.w = full4 || lane0 + 3 < d.lext ? __ldg(pb + 3 * sb0) : 0.f;
+    return b;
+  };
+  // the row entering the window at step p (SA == SB: the last tap's row, else the first)
+  auto enter_x = [&](int32_t pp) { return SA == SB ? gc + SA * pp + SB * (KT - 1) : gc + SA * pp; };
+  float4 w[KT];
+  float acc[KT][4];
+#pragma unroll
+  for (int q = 0; q < KT; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[q][e] = 0.f;
+  auto fma_step = [&](const float4& b) {
+#pragma unroll
+    for (int q = 0; q < KT; ++q) {
+      acc[q][0] += w[q].x * b.x;
+      acc[q][1] += w[q].y * b.y;
+      acc[q][2] += w[q].z * b.z;
+      acc[q][3] += w[q].w * b.w;
+    }
+  };
+  auto shift_in = [&](const float4& nr) {
+    if (SA == SB) {
+#pragma unroll
+      for (int q = 0; q + 1 < KT; ++q) w[q] = w[q + 1];
+      w[KT - 1] = nr;
+    } else {
+#pragma unroll
+      for (int q = KT - 1; q > 0; --q) w[q] = w[q - 1];
+      w[0] = nr;
+    }
+  };
+  uint32_t k = k0;
+  while (k < k1) {
+    // a run of consecutive p without a carry into the other K vars
+    const int32_t p = kv[0];
+    const int32_t run = min(static_cast<int32_t>(k1 - k), ext0 - p);
+#pragma unroll
+    for (int q = 0; q < KT; ++q) w[q] = row(gc + SA * p + SB * q);
+    int32_t j = 0;
+    for (; j + 4 <= run; j += 4) {
+      float4 bb[4], nr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        bb[u] = brow(p + j + u);
+        nr[u] = row(enter_x(p + j + u + 1));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        fma_step(bb[u]);
+        shift_in(nr[u]);
+      }
+    }
+    for (; j < run; ++j) {
+      const float4 b = brow(p + j);
+      const float4 nr = row(enter_x(p + j + 1));
+      fma_step(b);
+      shift_in(nr);
+    }
+    k += static_cast<uint32_t>(run);
+    kv[0] = p + run;
+    if (kv[0] >= ext0) {
+      kv[0] = 0;
+#pragma unroll
+      for (int jj = 1; jj < SV_K; ++jj) {
+        if (jj < d.nk) {
+          if (++kv[jj] < d.kext[jj]) {
+            offAk += d.ksa[jj];
+            offBk += d.ksb[jj];
+            break;
+          }
+          const int32_t back = d.kext[jj] - 1;
+          offAk -= back * d.ksa[jj];
+          offBk -= back * d.ksb[jj];
+          kv[jj] = 0;
+        }
+      }
+    }
+  }
+  const int32_t offC = lane0 * d.osc[0], sc0 = d.osc[0], sc1 = d.osc[1];
+#pragma unroll
+  for (int q = 0; q < KT; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (lane0 + e >= d.lext) break;
+      float* cp = C + offC + q * sc1 + e * sc0;
+      if (d.mode == 2)
+        atomicAdd(cp, acc[q][e]);
+      else if (d.mode == 1)
+        *cp += acc[q][e];
+      else
+        *cp = acc[q][e];
+    }
+}
+
 // K-lane mode: a warp per output, lanes striding the K range (for steps whose streamed
 // operand is contiguous along a K var, e.g. the input gradient of RTR's first node:
 // 900 contiguous terms per output), combined with a warp-shuffle tree.
@@ -991,11 +1137,34 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
       d.stencil = d.kext[0];
     }
   }
+  // depthwise filter gradient: outputs (lane, tap), one gather on A over (K var p, tap)
+  d.dwgrad = 0;
+  if (!klane && !d.stencil && d.vec && !d.a_bcast && !p.unary && d.ng == 1 && d.gop[0] == 0 && !d.gwrap[0] &&
+      d.nout == 2 && (d.oext[1] == 3 || d.oext[1] == 5 || d.oext[1] == 7) &&
+      (d.go[0][1] == 1 || d.go[0][1] == -1) && d.osa[1] == 0 && d.osb[1] == 0) {
+    int pj = -1, nz = 0;
+    for (int j = 0; j < d.nk; ++j)
+      if (d.gk[0][j] != 0) {
+        ++nz;
+        pj = j;
+      }
+    if (nz == 1 && (d.gk[0][pj] == 1 || d.gk[0][pj] == -1) && d.ksa[pj] == 0) {
+      auto sw = [&](int32_t* a) { std::swap(a[0], a[pj]); };
+      sw(d.kext);
+      sw(d.ksa);
+      sw(d.ksb);
+      std::swap(d.kdiv[0], d.kdiv[pj]);
+      for (int g = 0; g < 2 * SV_G; ++g) sw(d.gk[g]);
+      d.dwgrad = d.oext[1];
+      outs = d.oext[0];  // one thread per 4 lanes and K slice, all taps
+    }
+  }
   // several consecutive values of output slot 1 per thread when K is short: the index
   // decoding (~10 instructions per var) otherwise dominates a 3-term stencil
   d.jrep = 1;
   d.l1ext = d.nout > 1 ? d.oext[1] : 1;
-  if (d.stencil) {
+  if (d.dwgrad) {
+  } else if (d.stencil) {
     const int jb = d.stencil <= 3 ? 8 : 4;
     d.jrep = jb;
     d.oext[1] = (d.l1ext + jb - 1) / jb;
@@ -1023,7 +1192,9 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
   // each thread keeping >= 32 K terms
   const int64_t blocks = klane ? (outs + 7) / 8 : (outs + 255) / 256;
   int64_t split = 1;
-  if (blocks < 148 * 8 && K >= 64)
+  if (d.dwgrad)  // ~4 waves of 256-thread CTAs, each thread >= 64 K steps
+    split = std::max<int64_t>(1, std::min<int64_t>((148 * 256 * 4 + outs - 1) / outs, K / 64));
+  else if (blocks < 148 * 8 && K >= 64)
     split = std::min<int64_t>((148 * 8 + blocks - 1) / blocks, K / (klane ? 1024 : 32));
   split = std::max<int64_t>(1, std::min<int64_t>(split, 65535));
   d.kper = static_cast<uint32_t>((K + split - 1) / split);
@@ -1042,6 +1213,19 @@ cudaError_t sv_launch(const SvDesc& d, int64_t span, bool zero_first, const floa
   }
   const unsigned gy = d.K ? (d.K + d.kper - 1) / d.kper : 1u;
   const dim3 gk((d.outs + 7u) / 8u, gy), g1((d.outs + 255u) / 256u, gy), blk(256);
+  if (d.dwgrad) {
+    const int sa = d.gk[0][0], sb = d.go[0][1];
+    const dim3 gd(static_cast<unsigned>((static_cast<uint64_t>(d.outs) * gy + 255u) / 256u));
+#define CE_DWG(KT)                                                                                       \
+  if (sa > 0 && sb > 0) return ce_launch(ce_dwgrad_kernel<KT, 1, 1>, gd, blk, 0, s, d, A, B, C);         \
+  if (sa > 0 && sb < 0) return ce_launch(ce_dwgrad_kernel<KT, 1, -1>, gd, blk, 0, s, d, A, B, C);        \
+  if (sa < 0 && sb > 0) return ce_launch(ce_dwgrad_kernel<KT, -1, 1>, gd, blk, 0, s, d, A, B, C);        \
+  return ce_launch(ce_dwgrad_kernel<KT, -1, -1>, gd, blk, 0, s, d, A, B, C);
+    if (d.dwgrad == 3) { CE_DWG(3) }
+    if (d.dwgrad == 5) { CE_DWG(5) }
+    CE_DWG(7)
+#undef CE_DWG
+  }
   if (d.stencil) {
     const int sa = d.go[0][1], sb = d.gk[0][0];
 #define CE_DW(KT, J)                                                                                     \
