@@ -297,11 +297,19 @@ __device__ __forceinline__ void decode_work(const TcParams& P, uint32_t w, uint3
 // then (stream-K) the group's contiguous share of the sk_r tail items' K iterations.
 struct WorkIter {
   uint32_t w;         // next whole item
+  uint32_t wend;      // contiguous mode: end of this group's items
   uint32_t pos, end;  // stream-K iteration range (relative to item sk_full, iteration 0)
+  bool seq;           // the item returned last was the previous item + 1 (contiguous mode)
 };
 
 __device__ __forceinline__ void work_begin(const TcParams& P, uint32_t group, uint32_t ngroups, WorkIter& it) {
   it.w = group;
+  it.wend = 0;
+  it.seq = false;
+  if (P.contig) {
+    it.w = group * P.ipg + min(group, P.irem);
+    it.wend = it.w + P.ipg + (group < P.irem ? 1u : 0u);
+  }
   it.pos = it.end = 0;
   if (P.sk_r > 0) {
     const uint32_t total = P.sk_r * static_cast<uint32_t>(P.k_iters);
@@ -311,9 +319,52 @@ __device__ __forceinline__ void work_begin(const TcParams& P, uint32_t group, ui
   }
 }
 
+// T <- the tile of the next item in decode_work's order (M units fastest, then N units,
+// then grid units; single CTA groups, no K split).
+__device__ __forceinline__ void advance_tile(const TcParams& P, Tile& T) {
+  for (int i = 0; i < P.nm; ++i) {
+    const TcUnit& u = P.u[P.mt[i]];
+    const int32_t v = T.val[P.mt[i]] + u.box;
+    if (v < u.ext) {
+      T.val[P.mt[i]] = v;
+      return;
+    }
+    T.val[P.mt[i]] = 0;
+  }
+  for (int i = 0; i < P.nn; ++i) {
+    const TcUnit& u = P.u[P.nt[i]];
+    const int32_t v = T.val[P.nt[i]] + u.box;
+    if (v < u.ext) {
+      T.val[P.nt[i]] = v;
+      T.ntile += 1;
+      return;
+    }
+    T.val[P.nt[i]] = 0;
+  }
+  T.ntile = 0;
+  for (int i = 0; i < P.ng; ++i) {
+    const TcUnit& u = P.u[P.gu[i]];
+    const int32_t v = T.val[P.gu[i]] + 1;
+    if (v < u.ext) {
+      T.val[P.gu[i]] = v;
+      return;
+    }
+    T.val[P.gu[i]] = 0;
+  }
+}
+
 // Next segment: item (full-decomposition index), K range [k0, k1), atomic epilogue flag.
 __device__ __forceinline__ bool work_next(const TcParams& P, uint32_t ngroups, WorkIter& it, uint32_t& item, int& k0,
                                           int& k1, bool& atomic) {
+  if (P.contig) {
+    if (it.w >= it.wend) return false;
+    it.seq = item == it.w - 1 && it.w != 0;
+    item = it.w++;
+    k0 = 0;
+    k1 = P.k_iters;
+    atomic = false;
+    return true;
+  }
   const uint32_t whole = P.sk_r > 0 ? P.sk_full : P.n_items;
   if (it.w < whole) {
     item = it.w;
@@ -479,8 +530,12 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       uint32_t item;
       int k0, k1;
       bool seg_atomic;
+      item = 0xffffffffu;
       while (work_next(P, ngroups, wi, item, k0, k1, seg_atomic)) {
-        decode_work(P, item, rank, csize, T);
+        if (wi.seq)
+          advance_tile(P, T);
+        else
+          decode_work(P, item, rank, csize, T);
         int ca[5], cb[5], dig[6];
         coords(P.oa, T.val, ca);
         coords(P.ob, T.val, cb);
@@ -581,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       uint32_t gi = 0, local = 0;
       WorkIter wi;
       work_begin(P, group, ngroups, wi);
-      uint32_t item;
+      uint32_t item = 0xffffffffu;
       int k0, k1;
       bool seg_atomic;
       for (; work_next(P, ngroups, wi, item, k0, k1, seg_atomic); ++local) {
@@ -643,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       uint32_t gi = 0;
       WorkIter wi;
       work_begin(P, group, ngroups, wi);
-      uint32_t item;
+      uint32_t item = 0xffffffffu;
       int k0, k1;
       bool seg_atomic;
       while (work_next(P, ngroups, wi, item, k0, k1, seg_atomic)) {
@@ -688,13 +743,18 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     int cols_for[2] = {-1, -1};  // N tile whose column tables each accumulator buffer holds
     WorkIter wi;
     work_begin(P, group, ngroups, wi);
-    uint32_t item;
+    uint32_t item = 0xffffffffu;
     int k0, k1;
     bool atomic;
     for (; work_next(P, ngroups, wi, item, k0, k1, atomic); ++local) {
       const int acc = static_cast<int>(local & 1);
+      if (et == 0) {  // (also for the other group's tiles: the incremental advance needs every item)
+        if (wi.seq)
+          advance_tile(P, T);
+        else
+          decode_work(P, item, rank, csize, T);
+      }
       if (ngrp == 2 && acc != grp) continue;  // the other group's tile
-      if (et == 0) decode_work(P, item, rank, csize, T);
       epi_bar(1 + grp);  // decoded tile visible (and the previous tile's tables are no longer read)
       // address tables for this tile (overlaps the MMAs)
       int64_t* cols = col_off + acc * BN;
@@ -975,6 +1035,16 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
     P.n_items = static_cast<uint32_t>(items);
     P.sk_full = 0;
     P.sk_r = 0;
+    P.contig = 0;
+    static const bool contig_on = [] {
+      const char* e = getenv("CE_TC_CONTIG");
+      return !(e && *e == '0');
+    }();
+    if (contig_on && csize == 1 && P.k_split == 1 && items >= 4 * ngroups) {
+      P.contig = 1;
+      P.ipg = static_cast<uint32_t>(items / ngroups);
+      P.irem = static_cast<uint32_t>(items % ngroups);
+    }
     P.dkit = tc_div(static_cast<uint32_t>(std::max(1, P.k_iters)));
     // off by default: the C memset it needs is a separate graph node that breaks the PDL
     // chain, which cost more than the shorter last round saved (measured on cfg2:
@@ -983,7 +1053,7 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
       const char* e = getenv("CE_TC_SK");
       return e && *e == '1';
     }();
-    if (sk_on && P.k_split == 1 && items > ngroups && items % ngroups != 0) {
+    if (sk_on && !P.contig && P.k_split == 1 && items > ngroups && items % ngroups != 0) {
       // gain: the last round shrinks from one item time to r/ngroups of it; cost: zeroing C
       // (and an atomic epilogue for those items).  Item time ~ 0.4 us per K stage.
       const int64_t r = items % ngroups;

@@ -113,6 +113,11 @@ struct TcParams {
   uint32_t sk_full;  // items handled whole (a multiple of ngroups)
   uint32_t sk_r;     // items handled stream-K
   TcDiv dkit;        // k_iters
+  // contiguous assignment (set per launch for many small tiles, no K split, no pairs):
+  // group g takes items [g*ipg + min(g, rem), ...) in order, so the tile origins advance
+  // incrementally instead of being re-decoded per tile
+  int32_t contig;
+  uint32_t ipg, irem;
   // 2-CTA cluster along M: each CTA TMA-loads mc_half rows of the B tile and multicasts
   // them to both CTAs (B is read from L2 once per CTA pair instead of once per CTA)
   int32_t mcast;           // 1: launched with cluster dims (2,1,1)
