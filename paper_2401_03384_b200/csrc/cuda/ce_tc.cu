@@ -37,7 +37,7 @@ __device__ unsigned long long g_tc_ts[160 * 16];
 // producer (after its empty wait), 1 MMA issuer (after its full wait).
 __device__ unsigned long long g_tc_it[3 * 256];
 __device__ __forceinline__ void stamp_it(const TcParams& P, int role, uint32_t gi) {
-  if ((P.dbg & 512) && blockIdx.x == 0 && gi < 256) {
+  if ((P.dbg & 512) && blockIdx.x == 0 && gi < 256) {  // role 2: epilogue, slot tile*4 + phase
     long long t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles (cheap; same SM for all roles)
     g_tc_it[role * 256 + gi] = static_cast<unsigned long long>(t);
@@ -755,6 +755,8 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
           decode_work(P, item, rank, csize, T);
       }
       if (ngrp == 2 && acc != grp) continue;  // the other group's tile
+      const bool est = (dbg & 512) && et == 0 && grp == 0 && local < 128;
+      if (est) stamp_it(P, 2, static_cast<uint32_t>(local / ngrp) * 4 + 0);
       epi_bar(1 + grp);  // decoded tile visible (and the previous tile's tables are no longer read)
       // address tables for this tile (overlaps the MMAs)
       int64_t* cols = col_off + acc * BN;
@@ -788,7 +790,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       rtab[row] = roff;
       epi_bar(1 + grp);  // tables visible to all epilogue warps
       if ((dbg & 32) && et == 0 && local == 0) stamp(P, 10);
+      if (est) stamp_it(P, 2, static_cast<uint32_t>(local / ngrp) * 4 + 1);
       mbar_wait(&tfull[acc], (local >> 1) & 1);
+      if (est) stamp_it(P, 2, static_cast<uint32_t>(local / ngrp) * 4 + 2);
       if ((dbg & 32) && et == 0 && local == 0) stamp(P, 4);
       if (dbg & 8) {  // timing experiment: skip the epilogue body
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -897,6 +901,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
           if (ch + 2 < nch) tmem_ld_wait(ra);
         }
       }
+      if (est) stamp_it(P, 2, static_cast<uint32_t>(local / ngrp) * 4 + 3);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       if (PAIR && !leader)
         mbar_arrive_cluster(mapa(&tempty[acc], 0));  // the even CTA's MMA owns the pair's TMEM writes

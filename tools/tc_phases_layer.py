@@ -41,7 +41,14 @@ _lib.lib().ce_debug_tc_iter_timestamps(it)
 a = np.array(it, dtype=np.float64).reshape(3, 256)
 if (a > 0).any():
     base = a[a > 0].min()
-    for role, nm in enumerate(["producer", "mma", "commit"]):
+    for role, nm in enumerate(["producer", "mma"]):
         v = a[role]
         v = (v[v > 0] - base) / 1.9e3
         print(nm, " ".join(f"{x:.2f}" for x in v[:60]))
+    e = a[2].reshape(64, 4)
+    e = e[e[:, 0] > 0]
+    if len(e):
+        e = (e - base) / 1.9e3
+        print("epi [start, tables, tfull, stored] per tile:")
+        for row in e[:16]:
+            print("   ", " ".join(f"{x:8.2f}" for x in row))
