@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
             // K-major: one box; MN-major: nsub boxes of [32 K rows][32 MN] at 4 KB steps
             if (!(dbg & 2048)) {
               tma_load(sA + s * A_BYTES, &Pg.ta, &full[s], ca);
-              for (int j = 1; j < nsub_a; ++j) {
+              for (int j = 1; j < nsub_a && !P.oa.wide; ++j) {
                 const int cj[5] = {ca[0] + 32 * j, ca[1], ca[2], ca[3], ca[4]};
                 tma_load(sA + s * A_BYTES + j * 4096, &Pg.ta, &full[s], cj);
               }
@@ -705,8 +705,27 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
         for (int it = k0; it < k1; ++it, ++gi) {
           const int s = static_cast<int>(gi % STAGES);
           mbar_wait(&full[s], (gi / STAGES) & 1);
-          if (P.oa.mn_major && !(P.dbg & 8192))
+          if (P.oa.mn_major && P.oa.wide) {
+            // [32 K][wbox MN] unswizzled: every warp reads its 32-MN slab first (the
+            // K-major blocks overwrite the whole stage), then writes block xw
+            const int wbox = P.oa.wbox;
+            const float* st = reinterpret_cast<const float*>(sA + s * A_BYTES);
+            float v[32];
+            if (32 * xw < wbox) {
+#pragma unroll
+              for (int k = 0; k < 32; ++k) v[k] = st[k * wbox + 32 * xw + lane];
+            }
+            asm volatile("bar.sync 3, %0;" ::"n"(32 * kXposeWarps) : "memory");
+            if (32 * xw < wbox) {
+              uint8_t* blk = sA + s * A_BYTES + xw * 4096;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<float4*>(blk + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+          } else if (P.oa.mn_major && !(P.dbg & 8192)) {
             for (int j = xw; j < P.oa.nsub; j += kXposeWarps) xpose_block(sA + s * A_BYTES + j * 4096, lane);
+          }
           if (P.ob.mn_major && !(P.dbg & 8192))
             for (int j = xw; j < P.ob.nsub; j += kXposeWarps) xpose_block(sB + s * B_BYTES + j * 4096, lane);
           // generic-proxy smem writes must be visible to the tensor core (async proxy)
@@ -938,7 +957,8 @@ EncodeTiledFn encoder() {
   return fn;
 }
 
-bool encode(CUtensorMap* map, const void* ptr, const uint64_t* gdim, const uint64_t* gstride, const uint32_t* box) {
+bool encode(CUtensorMap* map, const void* ptr, const uint64_t* gdim, const uint64_t* gstride, const uint32_t* box,
+            int swizzle) {
   EncodeTiledFn fn = encoder();
   if (!fn) return false;
   cuuint64_t dims[5], strides[4];
@@ -955,8 +975,8 @@ bool encode(CUtensorMap* map, const void* ptr, const uint64_t* gdim, const uint6
     last = s * dims[i];
   }
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void*>(ptr), dims, strides, boxes, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -1023,11 +1043,11 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
     if (at >= 0 && counter++ != at) P.dbg = 0;
   }
   if (plan.cached_a != A) {
-    if (!encode(&P.ta, A, plan.gdim_a, plan.gstride_a, plan.box_a)) return cudaErrorInvalidValue;
+    if (!encode(&P.ta, A, plan.gdim_a, plan.gstride_a, plan.box_a, plan.swz_a)) return cudaErrorInvalidValue;
     plan.cached_a = A;
   }
   if (plan.cached_b != B) {
-    if (!encode(&P.tb, B, plan.gdim_b, plan.gstride_b, plan.box_b)) return cudaErrorInvalidValue;
+    if (!encode(&P.tb, B, plan.gdim_b, plan.gstride_b, plan.box_b, plan.swz_b)) return cudaErrorInvalidValue;
     plan.cached_b = B;
   }
   if (static_cast<int64_t>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_split >= (1ll << 32))

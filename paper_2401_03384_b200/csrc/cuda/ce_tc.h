@@ -71,6 +71,8 @@ struct TcOperand {
   int32_t mn_major;   // 0: K-major (box = 32 K x rows), 1: MN-major (nsub boxes of 32 MN x 32 K)
   int32_t nsub;       // TMA issues per stage
   int32_t stage_bytes;
+  int32_t wide;       // MN-major loaded as ONE unswizzled [32 K rows][wbox MN] box (wbox <= 128)
+  int32_t wbox;
 };
 
 struct TcParams {
@@ -137,6 +139,7 @@ struct TcPlan {
   uint64_t gdim_a[5]{}, gdim_b[5]{};
   uint64_t gstride_a[5]{}, gstride_b[5]{};  // bytes, [0] unused
   uint32_t box_a[5]{}, box_b[5]{};
+  int swz_a = 1, swz_b = 1;   // 1: SWIZZLE_128B tensor map, 0: none (wide MN-major boxes)
   int64_t out_span = 0;       // elements of C to zero before a split-K launch
   const void* cached_a = nullptr;
   const void* cached_b = nullptr;

@@ -423,6 +423,21 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     return fail("A TMA dims");
   if (!dims_for(B, b_mn == 1, P.ob, plan->gdim_b, plan->gstride_b, plan->box_b, &plan->rank_b))
     return fail("B TMA dims");
+  // An MN-major A is fetched as one unswizzled [32 K][<=128 MN] box (512-B rows: one TMA
+  // per stage instead of nsub 4-KB boxes, 4x longer DRAM runs); the transposer warps then
+  // write the swizzled K-major blocks the MMA reads.
+  static const bool wide_on = [] {
+    const char* e = std::getenv("CE_TC_WIDE");
+    return !(e && *e == '0');
+  }();
+  P.oa.wide = 0;
+  P.ob.wide = 0;
+  if (wide_on && a_mn == 1 && P.oa.nsub >= 2 && P.oa.nsub <= 4) {
+    P.oa.wide = 1;
+    P.oa.wbox = P.oa.nsub * 32;
+    plan->box_a[0] = static_cast<uint32_t>(P.oa.wbox);
+    plan->swz_a = 0;
+  }
   if (a_mn == 0 && P.oa.stage_bytes != P.m_rows * 128) return fail("A rows");
   if (b_mn == 0 && P.ob.stage_bytes != P.n_cols * 128) return fail("B rows");
   if (P.ob.stage_bytes > plan->bn * 128) return fail("B tile too large");
