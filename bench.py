@@ -179,9 +179,17 @@ def main():
     from paper_2401_03384_b200.device import Context, Executor
     from paper_2401_03384_b200.parallel import allreduce_factor_grads, allreduce_factor_grads_async
 
+    # CE_BENCH_BACKEND=gloo + CE_BENCH_SHARE_GPU=1 exercise the multi-rank path of this
+    # script on a single GPU (test only; the measured path is NCCL, one GPU per rank)
+    if os.environ.get("CE_BENCH_SHARE_GPU") == "1":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("CE_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     ctx = Context(local, "auto")
     stream = ctx.torch_stream
     dev = torch.device(f"cuda:{local}")
