@@ -1212,6 +1212,15 @@ cudaError_t sv_launch(const SvDesc& d, int64_t span, bool zero_first, const floa
     if (e != cudaSuccess) return e;
   }
   const unsigned gy = d.K ? (d.K + d.kper - 1) / d.kper : 1u;
+  static const bool trace = [] {  // debug: CE_SV_TRACE=1 prints the variant of every launch
+    const char* e = std::getenv("CE_SV_TRACE");
+    return e && *e == '1';
+  }();
+  if (trace)
+    std::fprintf(stderr, "sv_launch %s outs=%u K=%u slices=%u\n",
+                 d.dwgrad ? "dwgrad" : d.stencil ? "stencil" : d.klane ? "klane" : (d.vec && d.jrep == 4) ? "blocked"
+                                                                               : d.vec ? "vec4" : "scalar",
+                 d.outs, d.K, gy);
   const dim3 gk((d.outs + 7u) / 8u, gy), g1((d.outs + 255u) / 256u, gy), blk(256);
   if (d.dwgrad) {
     const int sa = d.gk[0][0], sb = d.go[0][1];

@@ -350,3 +350,27 @@ def test_single_rank_nccl_allreduce(ctx):
     torch.cuda.synchronize()
     for a, b in zip(g, ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("conv_mode", ["same", "full", "valid"])
+@pytest.mark.parametrize("rank", [20, 24, 18])
+def test_depthwise_stencil_paths(any_ctx, conv_mode, rank):
+    """Depthwise convolutions in every linear mode: the register-window stencil (forward and
+    input gradient, all tap/position sign combinations) and the filter-gradient window kernel
+    when the channel pitch is a multiple of 4 (rank 20, 24), the scalar stream path otherwise
+    (18); every output and gradient against the FP64 oracle."""
+    c_, mode = any_ctx
+    rng = np.random.default_rng(31 + rank)
+    for expr, dims in [("bhwr,rh->bhwr|h", [[6, 13, 9, rank], [rank, 3]]),
+                       ("bhwr,rw->bhwr|w", [[5, 7, 11, rank], [rank, 5]]),
+                       ("bhwr,rh->bhwr|h", [[4, 16, 3, rank], [rank, 7]])]:
+        ins = [f32(rng.uniform(-1, 1, d)) for d in dims]
+        import paper_2401_03384_b200 as ce
+        plan = ce.optimal(expr, dims, conv_mode, "training")
+        dout = f32(rng.uniform(-1, 1, plan.out_dims))
+        plan, nodes, out, grads, _ = _run_plan(c_, expr, dims, conv_mode, ins, dout, "training")
+        ref, _ = npo.execute(expr, dims, nodes, ins, conv_mode)
+        ref_g = npo.backward(expr, dims, nodes, ins, dout, conv_mode)
+        assert nerr(out, ref) <= TOL[mode][0], (expr, conv_mode, rank)
+        for i, (g, r) in enumerate(zip(grads, ref_g)):
+            assert nerr(g.cpu().numpy(), r) <= TOL[mode][1], (expr, conv_mode, rank, i)
