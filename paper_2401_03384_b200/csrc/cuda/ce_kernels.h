@@ -15,5 +15,6 @@ cudaError_t ce_launch_tiled(const CeSimtDesc& d, const float* A, const float* B,
 // axes differ (smem-tiled transpose, coalesced on both sides).
 bool ce_permute_supported(const CeProblem& p);
 int ce_permute_describe(const CeProblem& p, char* buf, int n);  // diagnostics
+int ce_stream_describe(const CeSimtDesc& d, char* buf, int n);  // diagnostics
 cudaError_t ce_launch_permute(const CeProblem& p, const float* A, float* C, cudaStream_t s);
 cudaError_t ce_launch_fill(float* dst, int64_t n, uint64_t seed, cudaStream_t s);

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <vector>
 #include <cstdio>
+#include <cstring>
 
 #include "ce_device.h"
 #include "ce_kernels.h"
@@ -924,7 +925,12 @@ __global__ void __launch_bounds__(256) ce_stream_klane_kernel(const SvDesc d, co
 
 // Builds the stream descriptor; false when the problem exceeds its limits (then the
 // int64 reference kernels run).  *span = elements of C an atomic reduction must zero.
-bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float* C, SvDesc* out, int64_t* span) {
+bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float* C, SvDesc* out, int64_t* span,
+              const char** why = nullptr) {
+  auto fail = [&](const char* w) {
+    if (why) *why = w;
+    return false;
+  };
   // merge vars that are contiguous in every operand (same role, not gathered): fewer
   // index digits per thread and longer lane runs (e.g. RTR's (r3)(r0) output pair)
   CeProblem p = sd.p;
@@ -950,14 +956,14 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
       }
   }
   SvDesc d{};
-  if (p.ng_a > SV_G || p.ng_b > SV_G) return false;
+  if (p.ng_a > SV_G || p.ng_b > SV_G) return fail("too many gathers");
   // output vars: the lane var (unit stride in the operand that streams, else in C) first,
   // then by ascending out stride
   std::vector<int> ov(sd.ov, sd.ov + sd.nout);
   std::vector<int> kvars(sd.kv, sd.kv + sd.nk);
   ov.erase(std::remove_if(ov.begin(), ov.end(), [&](int v) { return p.ext[v] == 1; }), ov.end());
   kvars.erase(std::remove_if(kvars.begin(), kvars.end(), [&](int v) { return p.ext[v] == 1; }), kvars.end());
-  if (static_cast<int>(ov.size()) > SV_O || static_cast<int>(kvars.size()) > SV_K) return false;
+  if (static_cast<int>(ov.size()) > SV_O || static_cast<int>(kvars.size()) > SV_K) return fail("too many vars");
   auto astride = [&](int v) -> int64_t {
     if (p.sa[v]) return p.sa[v];
     for (int g = 0; g < p.ng_a; ++g)
@@ -1056,7 +1062,7 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
       const int slot = d.ng++;
       d.gop[slot] = side;
       const CeGather& G = gs[g];
-      if (G.extent >= (1ll << 30) || std::llabs(G.c) >= (1ll << 30)) return false;
+      if (G.extent >= (1ll << 30) || std::llabs(G.c) >= (1ll << 30)) return fail("gather extent");
       d.gc[slot] = static_cast<int32_t>(G.c);
       d.gext[slot] = static_cast<int32_t>(G.extent);
       d.gstride[slot] = static_cast<int32_t>(G.stride);
@@ -1109,7 +1115,9 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
     }
   }
   const int64_t lim = (1ll << 31) - 1;
-  if (outs > lim || K > lim || maxA > lim || maxB > lim || maxC > lim) return false;
+  if (outs > lim) return fail("outputs >= 2^31");
+  if (K > lim) return fail("K >= 2^31");
+  if (maxA > lim || maxB > lim || maxC > lim) return fail("operand span >= 2^31");
   d.K = static_cast<uint32_t>(K);
   // depthwise stencil: a single tap K var, one gather on A over (conv output var, tap)
   // with unit coefficients, B = F[lane, tap]
@@ -1455,6 +1463,7 @@ struct CePermDesc {
   // continues vin in the INPUT; y = y1 + ext[vout]*y2 where y2 = vout2 continues vout in
   // the OUTPUT (-1: none)
   int32_t vin2, vout2;
+  int32_t tile_ok;         // 0: grid limits of the tile kernels exceeded (block kernel only)
   int64_t ext[CE_MAX_VARS], sa[CE_MAX_VARS], sc[CE_MAX_VARS];
   int32_t rest[CE_MAX_VARS];
   int64_t nbatch;
@@ -1652,6 +1661,89 @@ __global__ void __launch_bounds__(256) ce_rowcopy_kernel(const CePermDesc d, con
   }
 }
 
+// Block permute for short axes (RTR's 4- and 10-wide factor axes, where the 2-axis tile
+// kernels above use a fraction of each tile and pay a 64-bit slice decode per few dozen
+// elements).  A block = whole (or divisor-split) axes covering >= 32 elements of both the
+// input and the output unit-stride runs, <= BP_MAX elements; the remaining axes are a
+// batch walked by a persistent grid.  Every thread's in-block offsets are batch-invariant,
+// so they are decoded once: per element one LDG + STS and one LDS + STG.  Shared memory
+// holds the block in output order (1 word of padding per 32), double-buffered so one
+// barrier per block suffices.
+constexpr int BP_MAX = 2048, BP_AX = 8;
+struct CeBlkPermDesc {
+  int32_t S, ni, no, nr;
+  int32_t iext[BP_AX], isa[BP_AX], ipos[BP_AX];  // block axes in input-stride order
+  TcDiv idiv[BP_AX];
+  int32_t oext[BP_AX], osc[BP_AX];               // block axes in output-stride order
+  TcDiv odiv[BP_AX];
+  uint32_t rext[CE_MAX_VARS];                    // batch axes
+  TcDiv rdiv[CE_MAX_VARS];
+  int64_t rsa[CE_MAX_VARS], rsc[CE_MAX_VARS];
+  uint32_t nbatch;
+};
+
+template <int NE>
+__global__ void __launch_bounds__(256, 4) ce_blockperm_kernel(const CeBlkPermDesc d, const float* __restrict__ A,
+                                                              float* __restrict__ C) {
+  ce_pdl_enter();
+  constexpr int SM = BP_MAX + BP_MAX / 32;
+  __shared__ float sm[2][SM];
+  int32_t ioff[NE], spos[NE], ooff[NE];
+#pragma unroll
+  for (int k = 0; k < NE; ++k) {
+    const uint32_t t = threadIdx.x + 256u * k;
+    uint32_t r = t;
+    int32_t a = 0, p = 0, c = 0;
+#pragma unroll
+    for (int i = 0; i < BP_AX; ++i)
+      if (i < d.ni) {
+        const uint32_t q = tc_quo(r, d.idiv[i]);
+        const int32_t v = static_cast<int32_t>(r - q * static_cast<uint32_t>(d.iext[i]));
+        r = q;
+        a += v * d.isa[i];
+        p += v * d.ipos[i];
+      }
+    r = t;
+#pragma unroll
+    for (int i = 0; i < BP_AX; ++i)
+      if (i < d.no) {
+        const uint32_t q = tc_quo(r, d.odiv[i]);
+        const int32_t v = static_cast<int32_t>(r - q * static_cast<uint32_t>(d.oext[i]));
+        r = q;
+        c += v * d.osc[i];
+      }
+    ioff[k] = a;
+    spos[k] = p + (p >> 5);
+    ooff[k] = c;
+  }
+  int buf = 0;
+  for (uint32_t bt = blockIdx.x; bt < d.nbatch; bt += gridDim.x) {
+    uint32_t r = bt;
+    int64_t bin = 0, bout = 0;
+    for (int i = 0; i < d.nr; ++i) {
+      const uint32_t q = tc_quo(r, d.rdiv[i]);
+      const int64_t v = static_cast<int64_t>(r - q * d.rext[i]);
+      r = q;
+      bin += v * d.rsa[i];
+      bout += v * d.rsc[i];
+    }
+    float v[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k)
+      if (threadIdx.x + 256 * k < static_cast<uint32_t>(d.S)) v[k] = __ldg(A + bin + ioff[k]);
+#pragma unroll
+    for (int k = 0; k < NE; ++k)
+      if (threadIdx.x + 256 * k < static_cast<uint32_t>(d.S)) sm[buf][spos[k]] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+      const uint32_t t = threadIdx.x + 256u * k;
+      if (t < static_cast<uint32_t>(d.S)) C[bout + ooff[k]] = sm[buf][t + (t >> 5)];
+    }
+    buf ^= 1;
+  }
+}
+
 // ----------------------------------------------------------------------------- fill
 __global__ void ce_fill_kernel(float* __restrict__ dst, int64_t n, uint64_t seed) {
   ce_pdl_enter();
@@ -1673,6 +1765,28 @@ int grid_for(int64_t work, int threads) {
 }
 
 }  // namespace
+
+int ce_stream_describe(const CeSimtDesc& d, char* buf, int n) {
+  // diagnostics: the streaming variant a launch with 16-B aligned operands would take
+  SvDesc sv;
+  int64_t span = 0;
+  const char* why = "?";
+  const float* al = reinterpret_cast<const float*>(uintptr_t{256});
+  if (!simt_stream_enabled()) return std::snprintf(buf, n, "stream off");
+  if (!sv_build(d, al, al, al, &sv, &span, &why)) return std::snprintf(buf, n, "no stream: %s", why);
+  return std::snprintf(buf, n, "stream %s vec_b=%d vec_c=%d nout=%d nk=%d ng=%d outs=%u K=%u kper=%u",
+                       sv.dwgrad ? "dwgrad" : sv.stencil ? "stencil" : sv.klane ? "klane" : (sv.vec && sv.jrep == 4) ? "blocked"
+                       : sv.vec ? "vec4" : "scalar",
+                       sv.vec_b, sv.vec_c, sv.nout, sv.nk, sv.ng, sv.outs, sv.K, sv.kper) +
+         [&] {
+           int k = 0;
+           if (std::getenv("CE_SV_DESCRIBE_VARS"))
+             for (int i = 0; i < sv.nout; ++i)
+               k += std::snprintf(buf + std::strlen(buf), n - std::strlen(buf), " o%d:%d/%d/%d/%d", i, sv.oext[i],
+                                  sv.osa[i], sv.osb[i], sv.osc[i]);
+           return k;
+         }();
+}
 
 cudaError_t ce_launch_direct(const CeSimtDesc& d, const float* A, const float* B, float* C, cudaStream_t s) {
   const int64_t total = d.Z * d.M * d.N;
@@ -1756,6 +1870,7 @@ bool perm_desc(const CeProblem& p, CePermDesc* out) {
   }
   if (d.vin < 0 || d.vout < 0) return false;
   d.vin2 = d.vout2 = -1;
+  d.tile_ok = 1;
   if (d.vin != d.vout) {
     // short unit-stride axes borrow the axis that continues them on their own side
     if (ext[d.vin] < 32)
@@ -1766,7 +1881,7 @@ bool perm_desc(const CeProblem& p, CePermDesc* out) {
         if (v != d.vin && v != d.vout && v != d.vin2 && sc[v] == ext[d.vout]) d.vout2 = v;
     const int64_t ein = ext[d.vin] * (d.vin2 >= 0 ? ext[d.vin2] : 1);
     const int64_t eout = ext[d.vout] * (d.vout2 >= 0 ? ext[d.vout2] : 1);
-    if (ein >= (1ll << 31) || eout >= (1ll << 31) || (eout + 31) / 32 > 65535) return false;
+    if (ein >= (1ll << 31) || eout >= (1ll << 31) || (eout + 31) / 32 > 65535) d.tile_ok = 0;
   }
   if (d.vin == d.vout) {
     // row copy: y = the axis with the smallest output stride among the others
@@ -1777,7 +1892,7 @@ bool perm_desc(const CeProblem& p, CePermDesc* out) {
     d.vout = vy;
     d.same = 1;
   }
-  if ((ext[d.vout] + 31) / 32 > 65535 || ext[d.vin] >= (1ll << 31) || ext[d.vout] >= (1ll << 31)) return false;
+  if ((ext[d.vout] + 31) / 32 > 65535 || ext[d.vin] >= (1ll << 31) || ext[d.vout] >= (1ll << 31)) d.tile_ok = 0;
   d.nbatch = 1;
   for (int v = 0; v < n; ++v)
     if (v != d.vin && v != d.vout && v != d.vin2 && v != d.vout2) {
@@ -1787,11 +1902,140 @@ bool perm_desc(const CeProblem& p, CePermDesc* out) {
   *out = d;
   return true;
 }
+
+// Block decomposition for ce_blockperm_kernel (see there); false when no block of
+// <= BP_MAX elements covers 32-element runs on both sides.
+bool blkperm_desc(const CePermDesc& pd, CeBlkPermDesc* out) {
+  struct Ax {
+    int64_t ext, sa, sc;
+    bool in;
+  };
+  std::vector<Ax> ax;
+  for (int v = 0; v < CE_MAX_VARS; ++v)
+    if (pd.ext[v] > 1) ax.push_back({pd.ext[v], pd.sa[v], pd.sc[v], false});
+  int64_t S = 1;
+  auto add = [&](std::size_t i, int64_t q) {  // take q (| ext) of axis i into the block
+    if (q < ax[i].ext) ax.push_back({ax[i].ext / q, ax[i].sa * q, ax[i].sc * q, false});
+    ax[i].ext = q;
+    ax[i].in = true;
+    S *= q;
+  };
+  auto sorted = [&](bool by_out) {
+    std::vector<std::size_t> o(ax.size());
+    for (std::size_t i = 0; i < o.size(); ++i) o[i] = i;
+    std::stable_sort(o.begin(), o.end(), [&](std::size_t x, std::size_t y) {
+      return by_out ? ax[x].sc < ax[y].sc : ax[x].sa < ax[y].sa;
+    });
+    return o;
+  };
+  // each side's stride-order prefix must cover >= 32 elements; an axis that overshoots is
+  // split at its smallest sufficient divisor (its outer part stays a separate axis)
+  for (bool by_out : {true, false}) {
+    bool done = false;
+    for (int guard = 0; guard < 2 * CE_MAX_VARS && !done; ++guard) {
+      int64_t prod = 1;
+      bool added = false;
+      for (std::size_t i : sorted(by_out)) {
+        if (prod >= 32) break;
+        if (ax[i].in) {
+          prod *= ax[i].ext;
+          continue;
+        }
+        int64_t q = 2;
+        while (q < ax[i].ext && (ax[i].ext % q || prod * q < 32)) ++q;
+        q = std::min(q, ax[i].ext);
+        if (S * q > BP_MAX) return false;
+        add(i, q);
+        added = true;
+        break;
+      }
+      if (!added) {
+        if (prod < 32) return false;
+        done = true;
+      }
+    }
+    if (!done) return false;
+  }
+  // grow along the output order to ~1024 elements (fewer batch iterations, longer store runs)
+  for (std::size_t i : sorted(true)) {
+    if (S >= 1024) break;
+    if (ax[i].in) continue;
+    if (S * ax[i].ext <= BP_MAX) {
+      add(i, ax[i].ext);
+      continue;
+    }
+    int64_t q = BP_MAX / S;
+    while (q >= 2 && ax[i].ext % q) --q;
+    if (q >= 2) add(i, q);
+    break;
+  }
+  CeBlkPermDesc d{};
+  d.S = static_cast<int32_t>(S);
+  int64_t span_a = 0, span_c = 0, nb = 1, pos = 1;
+  std::vector<int64_t> opos(ax.size(), 0);
+  for (std::size_t i : sorted(true)) {
+    if (!ax[i].in) continue;
+    if (d.no >= BP_AX) return false;
+    d.oext[d.no] = static_cast<int32_t>(ax[i].ext);
+    d.odiv[d.no] = tc_div(static_cast<uint32_t>(ax[i].ext));
+    d.osc[d.no] = static_cast<int32_t>(ax[i].sc);
+    ++d.no;
+    opos[i] = pos;
+    pos *= ax[i].ext;
+    span_c += (ax[i].ext - 1) * ax[i].sc;
+  }
+  for (std::size_t i : sorted(false)) {
+    if (!ax[i].in) {
+      if (d.nr >= CE_MAX_VARS) return false;
+      d.rext[d.nr] = static_cast<uint32_t>(ax[i].ext);
+      d.rdiv[d.nr] = tc_div(static_cast<uint32_t>(ax[i].ext));
+      d.rsa[d.nr] = ax[i].sa;
+      d.rsc[d.nr] = ax[i].sc;
+      ++d.nr;
+      nb *= ax[i].ext;
+      continue;
+    }
+    if (d.ni >= BP_AX) return false;
+    d.iext[d.ni] = static_cast<int32_t>(ax[i].ext);
+    d.idiv[d.ni] = tc_div(static_cast<uint32_t>(ax[i].ext));
+    d.isa[d.ni] = static_cast<int32_t>(ax[i].sa);
+    d.ipos[d.ni] = static_cast<int32_t>(opos[i]);
+    ++d.ni;
+    span_a += (ax[i].ext - 1) * ax[i].sa;
+  }
+  if (span_a >= (1ll << 31) || span_c >= (1ll << 31) || nb >= (1ll << 31)) return false;
+  d.nbatch = static_cast<uint32_t>(nb);
+  *out = d;
+  return true;
+}
+
+// auto: the block kernel where the 2-axis tile kernels leave most of a tile idle
+bool use_blkperm(const CePermDesc& d, CeBlkPermDesc* bp) {
+  static const int mode = [] {  // CE_PERM_BLOCK: 0 never, 1 whenever viable, unset = auto
+    const char* e = std::getenv("CE_PERM_BLOCK");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (!d.tile_ok) return blkperm_desc(d, bp);
+  if (mode == 0 || !blkperm_desc(d, bp)) return false;
+  if (mode == 1) return true;
+  if (d.same) return d.ext[d.vin] < 32 || d.ext[d.vin] * d.ext[d.vout] < 2048;
+  const int64_t ein = d.ext[d.vin] * (d.vin2 >= 0 ? d.ext[d.vin2] : 1);
+  const int64_t eout = d.ext[d.vout] * (d.vout2 >= 0 ? d.ext[d.vout2] : 1);
+  return ein < 32 || eout < 32;
+}
 }  // namespace
 
 int ce_permute_describe(const CeProblem& p, char* buf, int n) {
   CePermDesc d;
   if (!perm_desc(p, &d)) return std::snprintf(buf, n, "unsupported");
+  CeBlkPermDesc bp;
+  if (use_blkperm(d, &bp)) {
+    int k = std::snprintf(buf, n, "block S=%d ni=%d no=%d batch=%u |", bp.S, bp.ni, bp.no, bp.nbatch);
+    for (int v = 0; v < CE_MAX_VARS && k < n; ++v)
+      if (d.ext[v] > 0) k += std::snprintf(buf + k, n - k, " %lld:%lld/%lld", (long long)d.ext[v], (long long)d.sa[v],
+                                           (long long)d.sc[v]);
+    return k;
+  }
   int k = std::snprintf(buf, n, "%s vin=%d vout=%d vin2=%d vout2=%d |", d.same ? "rowcopy" : "transpose", d.vin, d.vout,
                         d.vin2, d.vout2);
   for (int v = 0; v < CE_MAX_VARS && k < n; ++v)
@@ -1802,12 +2046,22 @@ int ce_permute_describe(const CeProblem& p, char* buf, int n) {
 
 bool ce_permute_supported(const CeProblem& p) {
   CePermDesc d;
-  return perm_desc(p, &d);
+  CeBlkPermDesc bp;
+  return perm_desc(p, &d) && (d.tile_ok || blkperm_desc(d, &bp));
 }
 
 cudaError_t ce_launch_permute(const CeProblem& p, const float* A, float* C, cudaStream_t s) {
   CePermDesc d;
   if (!perm_desc(p, &d)) return cudaErrorInvalidValue;
+  CeBlkPermDesc bp;
+  if (use_blkperm(d, &bp)) {
+    if (bp.nbatch == 0) return cudaSuccess;
+    const dim3 grid(std::min<uint32_t>(bp.nbatch, 148 * 4));
+    if (bp.S <= 256) return ce_launch(ce_blockperm_kernel<1>, grid, dim3(256), 0, s, bp, A, C);
+    if (bp.S <= 512) return ce_launch(ce_blockperm_kernel<2>, grid, dim3(256), 0, s, bp, A, C);
+    if (bp.S <= 1024) return ce_launch(ce_blockperm_kernel<4>, grid, dim3(256), 0, s, bp, A, C);
+    return ce_launch(ce_blockperm_kernel<8>, grid, dim3(256), 0, s, bp, A, C);
+  }
   if (d.same) {
     bool v4 = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
               d.ext[d.vin] % 4 == 0 && d.sa[d.vout] % 4 == 0 && d.sc[d.vout] % 4 == 0;

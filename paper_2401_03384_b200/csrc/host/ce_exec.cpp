@@ -247,7 +247,69 @@ CeProblem repack(CeProblem& p, bool side_b, const std::vector<int>& inner_order,
   return pk;
 }
 
-// Layout signature of a pack (a unary permute): (extent, input stride, output stride) of
+// Explicit tap expansion ("im2col") of one operand: every gathered axis (p, q) of that
+// side becomes two plain axes p and q of a new buffer E (out-of-range taps written as
+// zeros, circular ones wrapped), so the step itself has no gather on that side and the
+// tensor cores can take it.  Used when the gather sits on the operand's unit-stride axis
+// (RTR's X[b,s,h+i,w+j] contracted over the taps only), which neither TMA boxes nor a
+// repack can express.  `inner_order` vars become E's innermost axes as in repack().
+// Returns the unary gather problem that writes E and patches p in place.
+CeProblem expand(CeProblem& p, bool side_b, const std::vector<int>& inner_order, int64_t* span) {
+  int64_t* s = side_b ? p.sb : p.sa;
+  CeGather* g = side_b ? p.gb : p.ga;
+  int& ng = side_b ? p.ng_b : p.ng_a;
+  struct Ax { int64_t key; int var, rank; };
+  std::vector<Ax> ax;
+  auto rank_of = [&](int v) {
+    for (std::size_t i = 0; i < inner_order.size(); ++i)
+      if (inner_order[i] == v) return static_cast<int>(i);
+    return 1 << 20;
+  };
+  std::vector<int> seen(static_cast<std::size_t>(p.nv), 0);
+  for (int v = 0; v < p.nv; ++v)
+    if (s[v]) {
+      ax.push_back({s[v], v, rank_of(v)});
+      seen[static_cast<std::size_t>(v)] = 1;
+    }
+  for (int i = 0; i < ng; ++i)
+    for (int v : {g[i].qv, g[i].pv})
+      if (!seen[static_cast<std::size_t>(v)]) {
+        ax.push_back({g[i].stride, v, rank_of(v)});
+        seen[static_cast<std::size_t>(v)] = 1;
+      }
+  std::stable_sort(ax.begin(), ax.end(), [](const Ax& x, const Ax& y) {
+    if (x.rank != y.rank) return x.rank < y.rank;
+    return x.key < y.key;
+  });
+  CeProblem pk{};
+  pk.unary = 1;
+  std::vector<int> pvar(static_cast<std::size_t>(p.nv), -1);
+  int64_t acc = 1;
+  std::vector<int64_t> ns(static_cast<std::size_t>(p.nv), 0);
+  for (std::size_t i = 0; i < ax.size(); ++i) {
+    if (i > 0 && ax[i].rank >= (1 << 20) && ax[i - 1].rank < (1 << 20)) acc = (acc + 3) / 4 * 4;
+    const int v = pk.nv++;
+    pvar[static_cast<std::size_t>(ax[i].var)] = v;
+    pk.ext[v] = p.ext[ax[i].var];
+    pk.cls[v] = CE_M;
+    pk.sa[v] = s[ax[i].var];  // 0 for the gathered vars
+    pk.sc[v] = acc;
+    ns[static_cast<std::size_t>(ax[i].var)] = acc;
+    acc *= p.ext[ax[i].var];
+  }
+  for (int i = 0; i < ng; ++i) {
+    CeGather G = g[i];
+    G.pv = pvar[static_cast<std::size_t>(g[i].pv)];
+    G.qv = pvar[static_cast<std::size_t>(g[i].qv)];
+    pk.ga[pk.ng_a++] = G;
+  }
+  for (std::size_t i = 0; i < ax.size(); ++i) s[ax[i].var] = ns[static_cast<std::size_t>(ax[i].var)];
+  ng = 0;
+  *span = acc;
+  return pk;
+}
+
+// Layout signature of a pack (a unary permute):(extent, input stride, output stride) of
 // every axis with extent > 1, in input-stride order.  Two packs with equal signatures
 // of the same buffer produce identical bytes.
 std::vector<int64_t> pack_signature(const CeProblem& pk) {
@@ -355,6 +417,74 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
             (side ? b : a) = ps.c;
             if (&list == &fwd_) packs_.push_back({src, pks[side], ps.c});
             list.push_back(ps);
+          }
+          p = q;
+          st.tc = t;
+          ok = true;
+        }
+      }
+    }
+    static const bool expand_on = [] {  // CE_EXPAND=0: no tap expansion
+      const char* e = std::getenv("CE_EXPAND");
+      return !(e && *e == '0');
+    }();
+    for (int side = 0; side < 2 && !ok && expand_on; ++side) {
+      // the operand's unit-stride axis is a convolution gather: expand its taps
+      const int ngs = side ? p.ng_b : p.ng_a;
+      const CeGather* gs = side ? p.gb : p.ga;
+      const int64_t* ss = side ? p.sb : p.sa;
+      const int64_t* ps = side ? p.sa : p.sb;
+      bool inner_gather = false;
+      for (int i = 0; i < ngs; ++i) inner_gather |= gs[i].stride == 1;
+      if (!inner_gather || inner_var(p, side == 1) >= 0) continue;
+      std::vector<int> in_op(static_cast<std::size_t>(p.nv), 0);
+      double e_elems = 1, outs = 1, partner = 1;
+      for (int v = 0; v < p.nv; ++v) {
+        bool g = false;
+        for (int i = 0; i < ngs; ++i) g |= gs[i].pv == v || gs[i].qv == v;
+        in_op[static_cast<std::size_t>(v)] = ss[v] != 0 || g;
+        if (in_op[static_cast<std::size_t>(v)]) e_elems *= static_cast<double>(p.ext[v]);
+        if (p.cls[v] != CE_K) outs *= static_cast<double>(p.ext[v]);
+        if (ps[v]) partner *= static_cast<double>(p.ext[v]);
+      }
+      if (e_elems >= 2147483647.0 || (e_elems > 2.0 * std::max(outs, partner) && e_elems > 536870912.0)) continue;
+      // E's innermost axes: the K vars it shares with the partner, in the partner's order
+      std::vector<int> korder;
+      for (int v = 0; v < p.nv; ++v)
+        if (p.cls[v] == CE_K && ps[v] && in_op[static_cast<std::size_t>(v)]) korder.push_back(v);
+      std::stable_sort(korder.begin(), korder.end(), [&](int x, int y) { return ps[x] < ps[y]; });
+      for (const auto& order : {korder, std::vector<int>{}}) {
+        if (ok) break;
+        for (int pack_partner = 0; pack_partner < 2 && !ok; ++pack_partner) {
+          if (pack_partner && order.empty()) continue;
+          CeProblem q = p;
+          int64_t span = 0, pspan = 0;
+          const CeProblem pk = expand(q, side == 1, order, &span);
+          CeProblem ppk{};
+          if (pack_partner) ppk = repack(q, side == 0, order, &pspan, nullptr);
+          TcPlan t;
+          if (!ce_tc_plan(q, &t)) continue;
+          Step es;
+          es.kind = Step::kDirect;
+          es.desc = simt_desc(pk);
+          es.a = side ? b : a;
+          es.c = {BufRef::kWork, alloc(span)};
+          es.node = node;
+          es.label = label + (side ? ":expandB" : ":expandA");
+          es.bytes = 4.0 * static_cast<double>(span) + 4.0 * operand_elems(pk, 0);
+          (side ? b : a) = es.c;
+          list.push_back(es);
+          if (pack_partner) {
+            Step ps2;
+            ps2.kind = ce_permute_supported(ppk) ? Step::kPermute : Step::kDirect;
+            ps2.desc = simt_desc(ppk);
+            ps2.a = side ? a : b;
+            ps2.c = {BufRef::kWork, alloc(pspan)};
+            ps2.node = node;
+            ps2.label = label + (side ? ":packA" : ":packB");
+            ps2.bytes = 8.0 * operand_elems(ppk, 0);
+            (side ? a : b) = ps2.c;
+            list.push_back(ps2);
           }
           p = q;
           st.tc = t;
@@ -623,9 +753,11 @@ std::string Executor::describe() const {
         static const char* bk[] = {"none", "in", "out", "ws", "dout", "din"};
         std::snprintf(line + n, sizeof line - n, " %s src=%s:%lld\n", pd, bk[st.a.kind], (long long)st.a.index);
       } else {
-        std::snprintf(line + n, sizeof line - n, " Z=%lld M=%lld N=%lld K=%lld (tc: %s)\n", (long long)st.desc.Z,
+        char sd[256] = "";
+        if (st.kind == Step::kDirect || st.kind == Step::kReduce) ce_stream_describe(st.desc, sd, sizeof sd);
+        std::snprintf(line + n, sizeof line - n, " Z=%lld M=%lld N=%lld K=%lld (tc: %s) %s\n", (long long)st.desc.Z,
                       (long long)st.desc.M, (long long)st.desc.N, (long long)st.desc.K,
-                      st.desc.p.unary ? "unary" : st.tc.why);
+                      st.desc.p.unary ? "unary" : st.tc.why, sd);
       }
       out += line;
     }

@@ -1,6 +1,7 @@
 // Lowering.  The forward index maps restate feature_index()
 // (/root/reference/proj/src/kernels.cpp:298-315); the adjoint maps are the
 // exact Jacobian transposes listed in SURVEY §8 row A11.
+#include <cstdlib>
 #include "ce_lower.hpp"
 
 #include <algorithm>
@@ -14,10 +15,20 @@ View dense_view(const Subscripts& subs, const std::vector<int64_t>& dims) {
 
 View padded_view(const Subscripts& subs, const std::vector<int64_t>& dims, int64_t align) {
   View v{subs, dims, std::vector<int64_t>(dims.size())};
+  // The innermost axis is padded to `align` elements (16-B row pitch for TMA), except a
+  // short one whose product with its neighbour is already aligned (RTR's 10x10 rank
+  // pairs): left dense, the pair stays one contiguous run that merges into one unit.
+  static const bool pair = [] {
+    const char* e = std::getenv("CE_PAD_PAIR");
+    return !(e && *e == '0');
+  }();
+  const std::size_t n = dims.size();
+  const bool dense_pair = pair && n >= 2 && dims[n - 1] % align != 0 && dims[n - 1] < 32 &&
+                          (dims[n - 1] * dims[n - 2]) % align == 0;
   int64_t acc = 1;
-  for (std::size_t i = dims.size(); i-- > 0;) {
+  for (std::size_t i = n; i-- > 0;) {
     v.strides[i] = acc;
-    acc *= (i + 1 == dims.size()) ? (dims[i] + align - 1) / align * align : dims[i];
+    acc *= (i + 1 == n && !dense_pair) ? (dims[i] + align - 1) / align * align : dims[i];
   }
   return v;
 }

@@ -328,7 +328,17 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   }();
   int ncap = ncap_env;
   P.n_cols = tile(B, b_mn == 1, CE_N, ncap, P.nt, &P.nn, TC_SRC_NTILE);
-  if (P.nm == 0 || P.nn == 0) return fail("no M or N tile unit");
+  if (P.nm == 0) return fail("no M tile unit");
+  if (P.nn == 0) {
+    // N = 1 (e.g. an input gradient contracting every factor index: dX = sum dZ * F): one
+    // B row per stage; the MMA's other 15 columns read stale shared memory and are never
+    // stored.  An N var that merely failed to tile still fails.
+    for (int v = 0; v < p.nv; ++v)
+      if (p.cls[v] == CE_N && p.ext[v] > 1) return fail("no N tile unit");
+    // memory-bound: worth it only when the 32-wide K boxes are mostly useful data
+    if (kblock.empty() || U[static_cast<std::size_t>(kblock.front().first)].ext < 16)
+      return fail("N = 1 with a short K unit");
+  }
   P.n_mma = static_cast<int32_t>((P.n_cols + 15) / 16 * 16);
   plan->bn = P.n_mma <= 64 ? 64 : P.n_mma <= 128 ? 128 : 256;
   if (b_mn == 1 && P.n_cols % 32) return fail("MN-major B tile must be a multiple of 32");

@@ -374,3 +374,64 @@ def test_depthwise_stencil_paths(any_ctx, conv_mode, rank):
         assert nerr(out, ref) <= TOL[mode][0], (expr, conv_mode, rank)
         for i, (g, r) in enumerate(zip(grads, ref_g)):
             assert nerr(g.cpu().numpy(), r) <= TOL[mode][1], (expr, conv_mode, rank, i)
+
+
+PERMUTE_CASES = [
+    # (expr, dims, expected kernel in describe)
+    ("abcdef->dabcef", [4, 4, 4, 4, 28, 28], None),
+    ("abcde->cbdae", [3, 4, 10, 10, 12], "block"),       # RTR pack: 4-wide unit axis out, 10-wide in
+    ("abcde->abdce", [10, 12, 10, 16, 4], "block"),      # rowcopy with 10-wide rows
+    ("ab->ba", [4, 3136], "block"),                      # split axis: 3136 = 64 x 49
+    ("abc->cab", [3, 4, 257], None),                     # prime extent: no block split, tile kernel
+    ("abcd->dabc", [7, 9, 11, 13], None),
+    ("pqx->xqp", [784, 2, 10], "block"),                 # RTR-like grad pack: 784 split 49 x 16
+    ("ab->ba", [256, 1000], None),                       # 64x64 tile path
+]
+
+
+@pytest.mark.parametrize("case", PERMUTE_CASES, ids=[c[0] + "_" + "x".join(map(str, c[1])) for c in PERMUTE_CASES])
+def test_permute_paths(ctx, case):
+    """Unary permutes through every permute kernel, bit-exact against numpy."""
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import Executor
+    expr, dims, kind = case
+    plan = ce.optimal(expr, [dims], "same", "inference")
+    if kind:
+        assert kind in plan.describe_steps(False), plan.describe_steps(False)
+    x = ctx.fill_random(dims, 77)
+    ex = Executor(ctx, plan)
+    out = ex.execute([x])
+    torch.cuda.synchronize()
+    lhs, rhs = expr.split("->")
+    ref = np.transpose(x.cpu().numpy(), [lhs.index(c) for c in rhs])
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+RTR_X_FIRST = [  # (T factors, S factors, k, H, batch, tree): the path contracts X with the conv factor first
+    ([4, 4, 8], [4, 4, 4], 3, 28, 1, "(((0 4) 1) (2 3))"),  # cfg3 64->128
+    ([4, 4, 4], [1, 1, 3], 7, 56, 2, "(((0 4) 3) (1 2))"),  # cfg3 conv1 (7x7 taps), reduced
+]
+
+
+@pytest.mark.parametrize("case", RTR_X_FIRST, ids=["64to128_28", "conv1_56"])
+def test_rtr_x_first_layers(any_ctx, case):
+    """cfg3 RTR layers whose path starts with X * conv factor (tap expansion + TC, N=1 TC
+    input gradient, block permutes of the 5-GB-class intermediates at full batch): fwd +
+    all grads against the oracle at reduced batch."""
+    import paper_2401_03384_b200 as ce
+    c_, mode = any_ctx
+    tf, sf, k, hp, batch, tree = case
+    le = ce.expression(ce.LayerSpec("rtr", tf, sf, k, k, hp, hp, batch, [1, 1, 1, 1]), 0.1)
+    rng = np.random.default_rng(29)
+    ins = [f32(rng.uniform(-1, 1, d)) for d in le.dims]
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    assert plan.tree_encoding() == tree
+    if mode == "auto":
+        assert "expandA" in plan.describe_steps(True)
+    dout = f32(rng.uniform(-1, 1, plan.out_dims))
+    plan, nodes, out, grads, _ = _run_plan(c_, le.expr, le.dims, "same", ins, dout, "training")
+    ref, _ = npo.execute(le.expr, le.dims, nodes, ins)
+    ref_g = npo.backward(le.expr, le.dims, nodes, ins, dout)
+    assert nerr(out, ref) <= TOL[mode][0]
+    for i, (g, r) in enumerate(zip(grads, ref_g)):
+        assert nerr(g.cpu().numpy(), r) <= TOL[mode][1], i

@@ -16,6 +16,9 @@ CASES = [
     ("abcdhwxy->bcdhwxya", [[256, 4, 4, 4, 28, 28, 10, 10]]),
     ("abcdhwxy->yabcdhwx", [[64, 4, 4, 4, 28, 28, 10, 10]]),
     ("bthw->btwh", [[128, 256, 14, 14]]),
+    ("abcde->eabcd", [[256, 3136, 10, 10, 4]]),        # RTR pack: 4-wide in, 10-wide out
+    ("abcdef->abdcfe", [[256, 784, 4, 16, 10, 10]]),  # 10x10 transposes under a batch
+    ("ab->ba", [[3211264, 4]]),                        # 4-wide output unit axis
 ]
 ctx = Context(0, "auto")
 torch.cuda.set_stream(ctx.torch_stream)
