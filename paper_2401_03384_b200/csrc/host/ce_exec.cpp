@@ -381,47 +381,77 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
         }
         attempts.push_back({true, true, order});
       }
-      for (const Attempt& at : attempts) {
-        if (ok || at.order.empty()) continue;
-        const bool pack_a = at.pack_a, pack_b = at.pack_b;
+      // every layout that the tensor cores accept is scored (stages at ~0.25 us per SM plus
+      // pack traffic at ~3 TB/s; a pack the forward pass already made is free): the first
+      // legal layout can leave a 4-wide K unit padded to 32 where packing both operands
+      // merges the K vars into one 40-wide unit (RTR)
+      static const bool first_legal = [] {
+        const char* e = std::getenv("CE_PACK_FIRST");
+        return e && *e == '1';
+      }();
+      auto reusable = [&](BufRef src, const CeProblem& pk) -> const PackRecord* {
+        for (const PackRecord& r : packs_)
+          if (r.src.kind == src.kind && r.src.index == src.index && pack_signature(r.pk) == pack_signature(pk))
+            return &r;
+        return nullptr;
+      };
+      double best_us = 1e300;
+      int best = -1;
+      CeProblem best_q{}, best_pks[2];
+      int64_t best_spans[2] = {0, 0};
+      TcPlan best_t;
+      for (std::size_t ai = 0; ai < attempts.size(); ++ai) {
+        const Attempt& at = attempts[ai];
+        if (at.order.empty() || (first_legal && best >= 0)) continue;
         CeProblem q = p;
         CeProblem pks[2];
         int64_t spans[2] = {0, 0};
-        if (pack_a) pks[0] = repack(q, false, at.order, &spans[0], pack_b ? nullptr : p.sb);
-        if (pack_b) pks[1] = repack(q, true, at.order, &spans[1], pack_a ? nullptr : p.sa);
+        if (at.pack_a) pks[0] = repack(q, false, at.order, &spans[0], at.pack_b ? nullptr : p.sb);
+        if (at.pack_b) pks[1] = repack(q, true, at.order, &spans[1], at.pack_a ? nullptr : p.sa);
         TcPlan t;
-        if (ce_tc_plan(q, &t)) {
-          for (int side = 0; side < 2; ++side) {
-            if (!(side ? pack_b : pack_a)) continue;
-            // an identical repack of the same buffer done by the forward pass is reused
-            // (forward always runs before backward on the same inputs)
-            const BufRef src = side ? b : a;
-            bool reused = false;
-            for (const PackRecord& r : packs_) {
-              if (r.src.kind != src.kind || r.src.index != src.index) continue;
-              if (pack_signature(r.pk) == pack_signature(pks[side])) {
-                (side ? b : a) = r.dst;
-                reused = true;
-                break;
-              }
-            }
-            if (reused) continue;
-            Step ps;
-            ps.kind = ce_permute_supported(pks[side]) ? Step::kPermute : Step::kDirect;
-            ps.desc = simt_desc(pks[side]);
-            ps.a = side ? b : a;
-            ps.c = {BufRef::kWork, alloc(spans[side])};
-            ps.node = node;
-            ps.label = label + (side ? ":packB" : ":packA");
-            ps.bytes = 8.0 * operand_elems(pks[side], 0);
-            (side ? b : a) = ps.c;
-            if (&list == &fwd_) packs_.push_back({src, pks[side], ps.c});
-            list.push_back(ps);
-          }
-          p = q;
-          st.tc = t;
-          ok = true;
+        if (!ce_tc_plan(q, &t)) continue;
+        const TcParams& P = t.params;
+        double us = static_cast<double>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_iters * 0.25 / 148.0;
+        for (int side = 0; side < 2; ++side)
+          if ((side ? at.pack_b : at.pack_a) && !reusable(side ? b : a, pks[side]))
+            us += 8.0 * operand_elems(pks[side], 0) / 3.0e6;
+        if (us < best_us) {
+          best_us = us;
+          best = static_cast<int>(ai);
+          best_q = q;
+          best_pks[0] = pks[0];
+          best_pks[1] = pks[1];
+          best_spans[0] = spans[0];
+          best_spans[1] = spans[1];
+          best_t = t;
         }
+      }
+      if (best >= 0) {
+        const Attempt& at = attempts[static_cast<std::size_t>(best)];
+        for (int side = 0; side < 2; ++side) {
+          if (!(side ? at.pack_b : at.pack_a)) continue;
+          // an identical repack of the same buffer done by the forward pass is reused
+          // (forward always runs before backward on the same inputs)
+          const BufRef src = side ? b : a;
+          if (const PackRecord* r = reusable(src, best_pks[side])) {
+            (side ? b : a) = r->dst;
+            continue;
+          }
+          Step ps;
+          ps.kind = ce_permute_supported(best_pks[side]) ? Step::kPermute : Step::kDirect;
+          ps.desc = simt_desc(best_pks[side]);
+          ps.a = src;
+          ps.c = {BufRef::kWork, alloc(best_spans[side])};
+          ps.node = node;
+          ps.label = label + (side ? ":packB" : ":packA");
+          ps.bytes = 8.0 * operand_elems(best_pks[side], 0);
+          (side ? b : a) = ps.c;
+          if (&list == &fwd_) packs_.push_back({src, best_pks[side], ps.c});
+          list.push_back(ps);
+        }
+        p = best_q;
+        st.tc = best_t;
+        ok = true;
       }
     }
     static const bool expand_on = [] {  // CE_EXPAND=0: no tap expansion
