@@ -2018,7 +2018,9 @@ bool use_blkperm(const CePermDesc& d, CeBlkPermDesc* bp) {
   if (!d.tile_ok) return blkperm_desc(d, bp);
   if (mode == 0 || !blkperm_desc(d, bp)) return false;
   if (mode == 1) return true;
-  if (d.same) return d.ext[d.vin] < 32 || d.ext[d.vin] * d.ext[d.vout] < 2048;
+  // small packs (factor matrices, a few MB) run as fast on the tile kernels' wider grids
+  if (static_cast<int64_t>(bp->S) * bp->nbatch < (int64_t{1} << 22)) return false;
+  if (d.same) return d.ext[d.vin] < 12 || d.ext[d.vin] * d.ext[d.vout] < 1024;
   const int64_t ein = d.ext[d.vin] * (d.vin2 >= 0 ? d.ext[d.vin2] : 1);
   const int64_t eout = d.ext[d.vout] * (d.vout2 >= 0 ? d.ext[d.vout2] : 1);
   return ein < 32 || eout < 32;

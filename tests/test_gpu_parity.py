@@ -379,19 +379,20 @@ def test_depthwise_stencil_paths(any_ctx, conv_mode, rank):
 PERMUTE_CASES = [
     # (expr, dims, expected kernel in describe)
     ("abcdef->dabcef", [4, 4, 4, 4, 28, 28], None),
-    ("abcde->cbdae", [3, 4, 10, 10, 12], "block"),       # RTR pack: 4-wide unit axis out, 10-wide in
-    ("abcde->abdce", [10, 12, 10, 16, 4], "block"),      # rowcopy with 10-wide rows
-    ("ab->ba", [4, 3136], "block"),                      # split axis: 3136 = 64 x 49
+    ("abcde->cbdae", [60, 60, 10, 10, 12], "block"),       # RTR pack: 4-wide unit axis out, 10-wide in
+    ("abcde->abdce", [100, 120, 10, 16, 4], "block"),      # rowcopy with 10-wide rows
+    ("ab->ba", [4, 1254400], "block"),                   # split axis: 1254400 = 448 x 2800
     ("abc->cab", [3, 4, 257], None),                     # prime extent: no block split, tile kernel
     ("abcd->dabc", [7, 9, 11, 13], None),
-    ("pqx->xqp", [784, 2, 10], "block"),                 # RTR-like grad pack: 784 split 49 x 16
+    ("bpqx->bxqp", [300, 784, 2, 10], "block"),          # RTR-like grad pack: 784 split 49 x 16
     ("ab->ba", [256, 1000], None),                       # 64x64 tile path
 ]
 
 
 @pytest.mark.parametrize("case", PERMUTE_CASES, ids=[c[0] + "_" + "x".join(map(str, c[1])) for c in PERMUTE_CASES])
 def test_permute_paths(ctx, case):
-    """Unary permutes through every permute kernel, bit-exact against numpy."""
+    """Unary permutes through every permute kernel, bit-exact against numpy (the block
+    kernel is auto-selected from 4M elements on)."""
     import paper_2401_03384_b200 as ce
     from paper_2401_03384_b200.device import Executor
     expr, dims, kind = case
