@@ -12,6 +12,8 @@
 #include <array>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <string>
 #include <stdexcept>
 
 #include "../cuda/ce_kernels.h"
@@ -777,6 +779,22 @@ std::string Executor::describe() const {
                       " bn=%d rows=%d cols=%d mma_n=%d tiles=%dx%dx%d split=%d kit=%d amn=%d bmn=%d tr=%d mc=%d\n", st.tc.bn,
                       P.m_rows, P.n_cols, P.n_mma, P.tiles_m, P.tiles_n, P.grid_z, P.k_split, P.k_iters, P.oa.mn_major,
                       P.ob.mn_major, P.transpose_store, P.mcast);
+        if (std::getenv("CE_DESCRIBE_UNITS")) {
+          std::string u = " ";
+          n = static_cast<int>(std::strlen(line)) - 1;  // before the newline
+          for (int pass = 0; pass < 2; ++pass) {
+            u += pass ? " nt=[" : "mt=[";
+            const int32_t* list = pass ? P.nt : P.mt;
+            for (int i = 0; i < (pass ? P.nn : P.nm); ++i) {
+              const TcUnit& U = P.u[list[i]];
+              u += std::to_string(U.box) + "/" + std::to_string(U.ext) + ":";
+              for (int k = 0; k < U.nv; ++k) u += std::to_string(U.vext[k]) + "@" + std::to_string(U.sc[k]) + (k + 1 < U.nv ? "," : "");
+              u += " ";
+            }
+            u += "]";
+          }
+          std::snprintf(line + n, sizeof line - n, "%s\n", u.c_str());
+        }
       } else if (st.kind == Step::kPermute) {
         char pd[256];
         ce_permute_describe(st.desc.p, pd, sizeof pd);
