@@ -255,6 +255,10 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   TcParams& P = plan->params;
   std::memset(&P, 0, sizeof(P));
   // M tile from A, N tile from B
+  static const bool balance_n = [] {  // CE_TC_BALANCE_N=0: widest N boxes (previous tiling)
+    const char* e = std::getenv("CE_TC_BALANCE_N");
+    return !(e && *e == '0');
+  }();
   auto tile = [&](const std::vector<Axis>& ops, bool mn_major, int cls, int cap, int32_t* list, int32_t* n,
                   int src) -> int {
     int rows = 1;
@@ -283,8 +287,9 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     // of the rows useful) instead of [14 w][9 h] (77%).
     std::vector<int64_t> ext;
     for (int u : cand) ext.push_back(U[static_cast<std::size_t>(u)].ext);
+    const bool minbox = cls == CE_N && balance_n;
     std::vector<int> best(cand.size(), 1);
-    int64_t best_tiles = INT64_MAX, best_rows = 0;
+    int64_t best_tiles = INT64_MAX, best_rows = minbox ? INT64_MAX : 0;
     std::vector<int> b(cand.size(), 1);
     std::function<void(std::size_t, int)> search = [&](std::size_t i, int room) {
       if (i == cand.size()) {
@@ -293,7 +298,9 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
           tiles *= (ext[j] + b[j] - 1) / b[j];
           r *= b[j];
         }
-        if (tiles < best_tiles || (tiles == best_tiles && r > best_rows)) {
+        // M: the MMA is always 128 rows, so use as many as fit; N: the MMA width follows the
+        // tile, so among equal tile counts the narrowest box pads least (273 -> 2 x 137)
+        if (tiles < best_tiles || (tiles == best_tiles && (minbox ? r < best_rows : r > best_rows))) {
           best_tiles = tiles;
           best_rows = r;
           best = b;
@@ -303,7 +310,8 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
       const int hi = static_cast<int>(std::min<int64_t>(ext[i], room));
       for (int x = hi; x >= 1; --x) {
         // only boxes that are the full extent or change the tile count are worth trying
-        if (x < hi && (ext[i] + x - 1) / x == (ext[i] + x) / (x + 1)) continue;
+        if (!minbox && x < hi && (ext[i] + x - 1) / x == (ext[i] + x) / (x + 1)) continue;
+        if (minbox && x < hi && x > 1 && (ext[i] + x - 1) / x == (ext[i] + x - 2) / (x - 1)) continue;
         b[i] = x;
         search(i + 1, room / x);
       }
@@ -327,6 +335,19 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     return e ? std::atoi(e) : 256;
   }();
   int ncap = ncap_env;
+  if (balance_n && ncap == 256 && b_mn == 0) {
+    // a launch with fewer work items than half the SMs: narrower N tiles double them
+    const std::vector<TcUnit> U0 = U;
+    int32_t nt0[TC_MAX_UNITS];
+    int32_t nn0 = 0;
+    const int cols = tile(B, false, CE_N, 256, nt0, &nn0, TC_SRC_NTILE);
+    U = U0;
+    double out_elems = 1, k_elems = 1;
+    for (int v = 0; v < p.nv; ++v) (p.cls[v] != CE_K ? out_elems : k_elems) *= static_cast<double>(p.ext[v]);
+    // (a long K loop is split across CTAs instead: split-K fills the machine)
+    if (cols >= 128 && k_elems <= 64.0 * TC_BK && out_elems / (static_cast<double>(P.m_rows) * cols) < 74)
+      ncap = 128;
+  }
   P.n_cols = tile(B, b_mn == 1, CE_N, ncap, P.nt, &P.nn, TC_SRC_NTILE);
   if (P.nm == 0) return fail("no M tile unit");
   if (P.nn == 0) {
