@@ -1680,20 +1680,31 @@ struct CeBlkPermDesc {
   TcDiv rdiv[CE_MAX_VARS];
   int64_t rsa[CE_MAX_VARS], rsc[CE_MAX_VARS];
   uint32_t nbatch;
+  // gathered input axes (tap expansion, see ce_exec.cpp expand()): index x_g = gc + sum of
+  // coef * axis value over block and batch axes, valid in [0, gext), else the element is 0
+  int32_t ng;
+  int32_t gext[2], gc[2];
+  int64_t gstride[2];
+  int32_t icoef[2][BP_AX];
+  int32_t rcoef[2][CE_MAX_VARS];
 };
 
-template <int NE>
+template <int NE, int NG>
 __global__ void __launch_bounds__(256, 4) ce_blockperm_kernel(const CeBlkPermDesc d, const float* __restrict__ A,
                                                               float* __restrict__ C) {
   ce_pdl_enter();
   constexpr int SM = BP_MAX + BP_MAX / 32;
   __shared__ float sm[2][SM];
   int32_t ioff[NE], spos[NE], ooff[NE];
+  int32_t gin[NE][NG > 0 ? NG : 1];
 #pragma unroll
   for (int k = 0; k < NE; ++k) {
     const uint32_t t = threadIdx.x + 256u * k;
     uint32_t r = t;
     int32_t a = 0, p = 0, c = 0;
+    int32_t g[NG > 0 ? NG : 1];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) g[j] = 0;
 #pragma unroll
     for (int i = 0; i < BP_AX; ++i)
       if (i < d.ni) {
@@ -1702,6 +1713,8 @@ __global__ void __launch_bounds__(256, 4) ce_blockperm_kernel(const CeBlkPermDes
         r = q;
         a += v * d.isa[i];
         p += v * d.ipos[i];
+#pragma unroll
+        for (int j = 0; j < NG; ++j) g[j] += v * d.icoef[j][i];
       }
     r = t;
 #pragma unroll
@@ -1712,6 +1725,11 @@ __global__ void __launch_bounds__(256, 4) ce_blockperm_kernel(const CeBlkPermDes
         r = q;
         c += v * d.osc[i];
       }
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      gin[k][j] = g[j];
+      a += g[j] * static_cast<int32_t>(d.gstride[j]);
+    }
     ioff[k] = a;
     spos[k] = p + (p >> 5);
     ooff[k] = c;
@@ -1720,17 +1738,28 @@ __global__ void __launch_bounds__(256, 4) ce_blockperm_kernel(const CeBlkPermDes
   for (uint32_t bt = blockIdx.x; bt < d.nbatch; bt += gridDim.x) {
     uint32_t r = bt;
     int64_t bin = 0, bout = 0;
+    int32_t gb[NG > 0 ? NG : 1];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) gb[j] = d.gc[j];
     for (int i = 0; i < d.nr; ++i) {
       const uint32_t q = tc_quo(r, d.rdiv[i]);
       const int64_t v = static_cast<int64_t>(r - q * d.rext[i]);
       r = q;
       bin += v * d.rsa[i];
       bout += v * d.rsc[i];
+#pragma unroll
+      for (int j = 0; j < NG; ++j) gb[j] += static_cast<int32_t>(v) * d.rcoef[j][i];
     }
+#pragma unroll
+    for (int j = 0; j < NG; ++j) bin += static_cast<int64_t>(gb[j]) * d.gstride[j];
     float v[NE];
 #pragma unroll
-    for (int k = 0; k < NE; ++k)
-      if (threadIdx.x + 256 * k < static_cast<uint32_t>(d.S)) v[k] = __ldg(A + bin + ioff[k]);
+    for (int k = 0; k < NE; ++k) {
+      bool ok = threadIdx.x + 256 * k < static_cast<uint32_t>(d.S);
+#pragma unroll
+      for (int j = 0; j < NG; ++j) ok = ok && static_cast<uint32_t>(gb[j] + gin[k][j]) < static_cast<uint32_t>(d.gext[j]);
+      v[k] = ok ? __ldg(A + bin + ioff[k]) : 0.f;
+    }
 #pragma unroll
     for (int k = 0; k < NE; ++k)
       if (threadIdx.x + 256 * k < static_cast<uint32_t>(d.S)) sm[buf][spos[k]] = v[k];
@@ -1764,6 +1793,9 @@ int grid_for(int64_t work, int threads) {
   return blocks < 1 ? 1 : (int)blocks;
 }
 
+// block permute with gathered axes (defined with the permute host code below)
+bool blkgather_desc(const CeProblem& p, CeBlkPermDesc* out);
+cudaError_t blk_launch(const CeBlkPermDesc& bp, const float* A, float* C, cudaStream_t s);
 }  // namespace
 
 int ce_stream_describe(const CeSimtDesc& d, char* buf, int n) {
@@ -1772,6 +1804,19 @@ int ce_stream_describe(const CeSimtDesc& d, char* buf, int n) {
   int64_t span = 0;
   const char* why = "?";
   const float* al = reinterpret_cast<const float*>(uintptr_t{256});
+  CeBlkPermDesc bp;
+  if (!d.p.accumulate && blkgather_desc(d.p, &bp)) {
+    int k = std::snprintf(buf, n, "block-gather S=%d ni=%d no=%d batch=%u ng=%d", bp.S, bp.ni, bp.no, bp.nbatch, bp.ng);
+    if (std::getenv("CE_SV_DESCRIBE_VARS")) {
+      for (int i = 0; i < bp.ni && k < n; ++i)
+        k += std::snprintf(buf + k, n - k, " i%d:%d/sa%d/pos%d/c%d,%d", i, bp.iext[i], bp.isa[i], bp.ipos[i],
+                           bp.icoef[0][i], bp.icoef[1][i]);
+      for (int i = 0; i < bp.no && k < n; ++i) k += std::snprintf(buf + k, n - k, " o%d:%d/sc%d", i, bp.oext[i], bp.osc[i]);
+      for (int g = 0; g < bp.ng && k < n; ++g)
+        k += std::snprintf(buf + k, n - k, " g%d:c%d/ext%d/st%lld", g, bp.gc[g], bp.gext[g], (long long)bp.gstride[g]);
+    }
+    return k;
+  }
   if (!simt_stream_enabled()) return std::snprintf(buf, n, "stream off");
   if (!sv_build(d, al, al, al, &sv, &span, &why)) return std::snprintf(buf, n, "no stream: %s", why);
   return std::snprintf(buf, n, "stream %s vec_b=%d vec_c=%d nout=%d nk=%d ng=%d outs=%u K=%u kper=%u",
@@ -1793,6 +1838,8 @@ cudaError_t ce_launch_direct(const CeSimtDesc& d, const float* A, const float* B
   if (total == 0) return cudaSuccess;
   SvDesc sv;
   int64_t span = 0;
+  CeBlkPermDesc bp;
+  if (!d.p.accumulate && blkgather_desc(d.p, &bp)) return blk_launch(bp, A, C, s);
   if (simt_stream_enabled() && sv_build(d, A, B, C, &sv, &span))
     return sv_launch(sv, span, sv.mode == 2 && !d.p.accumulate, A, B, C, s);
   return ce_launch(ce_direct_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, d, A, B, C);
@@ -1905,17 +1952,22 @@ bool perm_desc(const CeProblem& p, CePermDesc* out) {
 
 // Block decomposition for ce_blockperm_kernel (see there); false when no block of
 // <= BP_MAX elements covers 32-element runs on both sides.
-bool blkperm_desc(const CePermDesc& pd, CeBlkPermDesc* out) {
-  struct Ax {
-    int64_t ext, sa, sc;
-    bool in;
-  };
-  std::vector<Ax> ax;
-  for (int v = 0; v < CE_MAX_VARS; ++v)
-    if (pd.ext[v] > 1) ax.push_back({pd.ext[v], pd.sa[v], pd.sc[v], false});
+struct BpAx {
+  int64_t ext, sa, sc;
+  int64_t coef[2];  // gather coefficients
+  bool in;
+};
+
+bool blk_build(std::vector<BpAx> ax, int ng, const int64_t* gstride, CeBlkPermDesc* out) {
   int64_t S = 1;
+  auto key_in = [&](const BpAx& a) {  // input-side stride (gathered axes: through the gather)
+    int64_t k = a.sa;
+    for (int g = 0; g < ng; ++g) k += std::llabs(a.coef[g]) * gstride[g];
+    return k;
+  };
   auto add = [&](std::size_t i, int64_t q) {  // take q (| ext) of axis i into the block
-    if (q < ax[i].ext) ax.push_back({ax[i].ext / q, ax[i].sa * q, ax[i].sc * q, false});
+    if (q < ax[i].ext)
+      ax.push_back({ax[i].ext / q, ax[i].sa * q, ax[i].sc * q, {ax[i].coef[0] * q, ax[i].coef[1] * q}, false});
     ax[i].ext = q;
     ax[i].in = true;
     S *= q;
@@ -1924,7 +1976,7 @@ bool blkperm_desc(const CePermDesc& pd, CeBlkPermDesc* out) {
     std::vector<std::size_t> o(ax.size());
     for (std::size_t i = 0; i < o.size(); ++i) o[i] = i;
     std::stable_sort(o.begin(), o.end(), [&](std::size_t x, std::size_t y) {
-      return by_out ? ax[x].sc < ax[y].sc : ax[x].sa < ax[y].sa;
+      return by_out ? ax[x].sc < ax[y].sc : key_in(ax[x]) < key_in(ax[y]);
     });
     return o;
   };
@@ -1991,6 +2043,10 @@ bool blkperm_desc(const CePermDesc& pd, CeBlkPermDesc* out) {
       d.rdiv[d.nr] = tc_div(static_cast<uint32_t>(ax[i].ext));
       d.rsa[d.nr] = ax[i].sa;
       d.rsc[d.nr] = ax[i].sc;
+      for (int g = 0; g < ng; ++g) {
+        if (std::llabs(ax[i].coef[g]) * ax[i].ext >= (1ll << 30)) return false;
+        d.rcoef[g][d.nr] = static_cast<int32_t>(ax[i].coef[g]);
+      }
       ++d.nr;
       nb *= ax[i].ext;
       continue;
@@ -2000,13 +2056,23 @@ bool blkperm_desc(const CePermDesc& pd, CeBlkPermDesc* out) {
     d.idiv[d.ni] = tc_div(static_cast<uint32_t>(ax[i].ext));
     d.isa[d.ni] = static_cast<int32_t>(ax[i].sa);
     d.ipos[d.ni] = static_cast<int32_t>(opos[i]);
+    for (int g = 0; g < ng; ++g) d.icoef[g][d.ni] = static_cast<int32_t>(ax[i].coef[g]);
     ++d.ni;
-    span_a += (ax[i].ext - 1) * ax[i].sa;
+    span_a += (ax[i].ext - 1) * key_in(ax[i]);
   }
+  d.ng = ng;
   if (span_a >= (1ll << 31) || span_c >= (1ll << 31) || nb >= (1ll << 31)) return false;
   d.nbatch = static_cast<uint32_t>(nb);
   *out = d;
   return true;
+}
+
+
+bool blkperm_desc(const CePermDesc& pd, CeBlkPermDesc* out) {
+  std::vector<BpAx> ax;
+  for (int v = 0; v < CE_MAX_VARS; ++v)
+    if (pd.ext[v] > 1) ax.push_back({pd.ext[v], pd.sa[v], pd.sc[v], {0, 0}, false});
+  return blk_build(ax, 0, nullptr, out);
 }
 
 // auto: the block kernel where the 2-axis tile kernels leave most of a tile idle
@@ -2024,6 +2090,58 @@ bool use_blkperm(const CePermDesc& d, CeBlkPermDesc* bp) {
   const int64_t ein = d.ext[d.vin] * (d.vin2 >= 0 ? d.ext[d.vin2] : 1);
   const int64_t eout = d.ext[d.vout] * (d.vout2 >= 0 ? d.ext[d.vout2] : 1);
   return ein < 32 || eout < 32;
+}
+}  // namespace
+
+namespace {
+template <int NG>
+cudaError_t blk_launch_ng(const CeBlkPermDesc& bp, const float* A, float* C, cudaStream_t s) {
+  const dim3 grid(std::min<uint32_t>(bp.nbatch, 148 * 4));
+  if (bp.S <= 256) return ce_launch(ce_blockperm_kernel<1, NG>, grid, dim3(256), 0, s, bp, A, C);
+  if (bp.S <= 512) return ce_launch(ce_blockperm_kernel<2, NG>, grid, dim3(256), 0, s, bp, A, C);
+  if (bp.S <= 1024) return ce_launch(ce_blockperm_kernel<4, NG>, grid, dim3(256), 0, s, bp, A, C);
+  return ce_launch(ce_blockperm_kernel<8, NG>, grid, dim3(256), 0, s, bp, A, C);
+}
+cudaError_t blk_launch(const CeBlkPermDesc& bp, const float* A, float* C, cudaStream_t s) {
+  if (bp.nbatch == 0) return cudaSuccess;
+  switch (bp.ng) {
+    case 0: return blk_launch_ng<0>(bp, A, C, s);
+    case 1: return blk_launch_ng<1>(bp, A, C, s);
+    default: return blk_launch_ng<2>(bp, A, C, s);
+  }
+}
+
+// Tap expansion (a unary step whose input is gathered, ce_exec.cpp expand()) as a block
+// permute with gathered input axes; false if the problem is not of that form.
+bool blkgather_desc(const CeProblem& p, CeBlkPermDesc* out) {
+  static const bool on = [] {
+    const char* e = std::getenv("CE_BLK_GATHER");
+    return !(e && *e == '0');
+  }();
+  if (!on || !p.unary || p.ng_a < 1 || p.ng_a > 2 || p.ng_b) return false;
+  int64_t gstride[2] = {0, 0};
+  for (int g = 0; g < p.ng_a; ++g) {
+    if (p.ga[g].wrap || p.ga[g].extent >= (1ll << 30) || std::llabs(p.ga[g].c) >= (1ll << 30)) return false;
+    gstride[g] = p.ga[g].stride;
+  }
+  std::vector<BpAx> ax;
+  for (int v = 0; v < p.nv; ++v) {
+    if (p.ext[v] <= 1) continue;
+    if (p.cls[v] == CE_K || p.sc[v] == 0) return false;
+    BpAx a{p.ext[v], p.sa[v], p.sc[v], {0, 0}, false};
+    for (int g = 0; g < p.ng_a; ++g)
+      a.coef[g] = (p.ga[g].pv == v ? p.ga[g].sp : 0) + (p.ga[g].qv == v ? p.ga[g].sq : 0);
+    ax.push_back(a);
+  }
+  CeBlkPermDesc d;
+  if (!blk_build(ax, p.ng_a, gstride, &d)) return false;
+  for (int g = 0; g < p.ng_a; ++g) {
+    d.gc[g] = static_cast<int32_t>(p.ga[g].c);
+    d.gext[g] = static_cast<int32_t>(p.ga[g].extent);
+    d.gstride[g] = gstride[g];
+  }
+  *out = d;
+  return true;
 }
 }  // namespace
 
@@ -2059,10 +2177,7 @@ cudaError_t ce_launch_permute(const CeProblem& p, const float* A, float* C, cuda
   if (use_blkperm(d, &bp)) {
     if (bp.nbatch == 0) return cudaSuccess;
     const dim3 grid(std::min<uint32_t>(bp.nbatch, 148 * 4));
-    if (bp.S <= 256) return ce_launch(ce_blockperm_kernel<1>, grid, dim3(256), 0, s, bp, A, C);
-    if (bp.S <= 512) return ce_launch(ce_blockperm_kernel<2>, grid, dim3(256), 0, s, bp, A, C);
-    if (bp.S <= 1024) return ce_launch(ce_blockperm_kernel<4>, grid, dim3(256), 0, s, bp, A, C);
-    return ce_launch(ce_blockperm_kernel<8>, grid, dim3(256), 0, s, bp, A, C);
+    return blk_launch(bp, A, C, s);
   }
   if (d.same) {
     bool v4 = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
