@@ -358,7 +358,130 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
     for (int g = 0; g < p.ng_a; ++g) k *= 1;  // gathered taps are K vars already counted
     return k <= 8 && outs >= (1ll << 20);
   }();
+  auto try_col2im = [&]() -> bool {
+    static const bool col2im_on = [] {  // CE_COL2IM=0: no col2im split
+      const char* e = std::getenv("CE_COL2IM");
+      return !(e && *e == '0');
+    }();
+    for (int side = 0; side < 2 && col2im_on && !p.unary; ++side) {
+      // col2im split of a convolution whose taps are contracted together with plain K vars
+      // (RTR conv1's dX = sum_{r,i,j} dZ[b,c,h-i,w-j,r] F[r,i,j]: the SIMT K-lane kernel
+      // re-walks all 441 terms per output):  T[b,c,u_h,u_w,i,j] = sum_r dZ[b,c,u_h,u_w,r] F[r,i,j]
+      // on the tensor cores (u = the gathered feature index as a plain axis, taps outermost
+      // in T), then C = sum_{i,j} T[b,c,h-i,w-j,i,j], a 49-term gather-sum.
+      const int ng = side ? p.ng_b : p.ng_a;
+      if (ng == 0 || ng > 2 || (side ? p.ng_a : p.ng_b)) continue;
+      const CeGather* gs = side ? p.gb : p.ga;
+      const int64_t* ss = side ? p.sb : p.sa;
+      const int64_t* os = side ? p.sa : p.sb;
+      bool fits = true;
+      double taps = 1, plain_k = 1, t_elems = 1, g_elems = 1;
+      for (int g = 0; g < ng; ++g) {
+        const int pv = gs[g].pv, qv = gs[g].qv;
+        // (p: an output position, q: a filter tap -- a gather whose "taps" outnumber its
+        // positions is a filter gradient, which the stream kernel's dwgrad path handles)
+        if (gs[g].wrap || p.cls[pv] == CE_K || ss[pv] || os[pv] || p.cls[qv] != CE_K || ss[qv] || !os[qv] ||
+            p.ext[pv] < p.ext[qv])
+          fits = false;
+        for (int h = 0; h < ng; ++h)
+          if (h != g && (gs[h].pv == pv || gs[h].qv == qv || gs[h].pv == qv || gs[h].qv == pv)) fits = false;
+        taps *= static_cast<double>(p.ext[qv]);
+        t_elems *= static_cast<double>(gs[g].extent) * static_cast<double>(p.ext[qv]);
+        g_elems *= static_cast<double>(gs[g].extent);
+      }
+      if (!fits) continue;
+      std::vector<char> is_p(static_cast<std::size_t>(p.nv), 0);
+      for (int g = 0; g < ng; ++g) is_p[static_cast<std::size_t>(gs[g].pv)] = 1;
+      for (int v = 0; v < p.nv; ++v) {
+        if (p.cls[v] == CE_K && ss[v] && os[v]) plain_k *= static_cast<double>(p.ext[v]);
+        if (p.cls[v] != CE_K && !is_p[static_cast<std::size_t>(v)]) t_elems *= static_cast<double>(p.ext[v]);
+        if (ss[v]) g_elems *= static_cast<double>(p.ext[v]);
+      }
+      if (taps < 9 || plain_k < 2 || t_elems >= 2147483647.0 || t_elems > std::max(536870912.0, 8.0 * g_elems))
+        continue;
+      // step 1: gathers replaced by plain feature axes u; p vars vanish; taps become outputs
+      CeProblem q1 = p;
+      int64_t* s1 = side ? q1.sb : q1.sa;
+      int uvar[2] = {-1, -1};
+      for (int g = 0; g < ng; ++g) {
+        if (q1.nv >= CE_MAX_VARS) fits = false;
+        if (!fits) break;
+        const int u = q1.nv++;
+        uvar[g] = u;
+        q1.ext[u] = gs[g].extent;
+        q1.cls[u] = side ? CE_N : CE_M;
+        q1.sa[u] = q1.sb[u] = q1.sc[u] = 0;
+        s1[u] = gs[g].stride;
+        const int pv = gs[g].pv, qv = gs[g].qv;
+        q1.ext[pv] = 1;
+        q1.sa[pv] = q1.sb[pv] = q1.sc[pv] = 0;
+        q1.cls[qv] = side ? CE_M : CE_N;
+      }
+      if (!fits) continue;
+      (side ? q1.ng_b : q1.ng_a) = 0;
+      q1.accumulate = 0;
+      // T layout: the gathered operand's non-K axes in its stride order (innermost first,
+      // pitch padded to 16 B), then the partner's, then the taps outermost (so the gather-sum
+      // reads T along the gathered operand's unit-stride axis)
+      std::vector<int> lay;
+      for (int pass = 0; pass < 3; ++pass) {
+        std::vector<int> vs;
+        for (int v = 0; v < q1.nv; ++v) {
+          if (q1.ext[v] <= 1 || q1.cls[v] == CE_K) continue;
+          bool tap = false;
+          for (int g = 0; g < ng; ++g) tap |= v == gs[g].qv;
+          const int64_t* s1o = side ? q1.sa : q1.sb;
+          const bool mine = s1[v] != 0 && !tap, theirs = s1o[v] != 0 && !tap;
+          if ((pass == 0 && mine) || (pass == 1 && theirs && !mine) || (pass == 2 && tap)) vs.push_back(v);
+        }
+        const int64_t* key = pass == 1 ? (side ? q1.sa : q1.sb) : s1;
+        std::stable_sort(vs.begin(), vs.end(), [&](int x, int y) { return pass == 2 ? x < y : key[x] < key[y]; });
+        lay.insert(lay.end(), vs.begin(), vs.end());
+      }
+      int64_t acc = 1;
+      std::vector<int64_t> tstr(static_cast<std::size_t>(q1.nv), 0);
+      for (std::size_t i = 0; i < lay.size(); ++i) {
+        tstr[static_cast<std::size_t>(lay[i])] = acc;
+        acc *= i == 0 ? (q1.ext[lay[i]] + 3) / 4 * 4 : q1.ext[lay[i]];
+      }
+      for (int v = 0; v < q1.nv; ++v) q1.sc[v] = q1.cls[v] == CE_K ? 0 : tstr[static_cast<std::size_t>(v)];
+      // step 2: C[...] (+)= sum_taps T[..., u = sp*p + sq*q + c, ..., q]
+      CeProblem q2 = p;
+      q2.unary = 1;
+      q2.ng_a = ng;
+      q2.ng_b = 0;
+      for (int v = 0; v < q2.nv; ++v) {
+        q2.sb[v] = 0;
+        bool tap = false;
+        for (int g = 0; g < ng; ++g) tap |= v == gs[g].qv;
+        if (p.cls[v] == CE_K && !tap) {
+          q2.ext[v] = 1;  // contracted in step 1
+          q2.sa[v] = q2.sc[v] = 0;
+          continue;
+        }
+        q2.sa[v] = is_p[static_cast<std::size_t>(v)] ? 0 : tstr[static_cast<std::size_t>(v)];
+      }
+      for (int g = 0; g < ng; ++g) {
+        q2.ga[g] = gs[g];
+        q2.ga[g].stride = tstr[static_cast<std::size_t>(uvar[g])];
+      }
+      const BufRef tref{BufRef::kWork, alloc(acc)};
+      add_problem(list, q1, a, b, tref, node, label + ":col2im-gemm");
+      add_problem(list, q2, tref, BufRef{}, c, node, label + ":col2im-sum");
+      return true;
+    }
+    return false;
+  };
   if (cfg_.math == 0 && !p.unary && !tiny_k) {
+    {
+      // an N = 1 convolution (input gradient over every factor index) is memory-bound on the
+      // tensor cores with the taps as shifted boxes (each dZ element read once per tap):
+      // the col2im split reads it once
+      double n_ext = 1;
+      for (int v = 0; v < p.nv; ++v)
+        if (p.cls[v] == CE_N) n_ext *= static_cast<double>(p.ext[v]);
+      if (n_ext == 1 && p.ng_a + p.ng_b > 0 && try_col2im()) return;
+    }
     bool ok = ce_tc_plan(p, &st.tc);
     if (!ok) {
       // tf32 tensor cores need both operands K-major over the same K unit: repack
@@ -524,117 +647,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
         }
       }
     }
-    static const bool col2im_on = [] {  // CE_COL2IM=0: no col2im split
-      const char* e = std::getenv("CE_COL2IM");
-      return !(e && *e == '0');
-    }();
-    for (int side = 0; side < 2 && !ok && col2im_on && !p.unary; ++side) {
-      // col2im split of a convolution whose taps are contracted together with plain K vars
-      // (RTR conv1's dX = sum_{r,i,j} dZ[b,c,h-i,w-j,r] F[r,i,j]: the SIMT K-lane kernel
-      // re-walks all 441 terms per output):  T[b,c,u_h,u_w,i,j] = sum_r dZ[b,c,u_h,u_w,r] F[r,i,j]
-      // on the tensor cores (u = the gathered feature index as a plain axis, taps outermost
-      // in T), then C = sum_{i,j} T[b,c,h-i,w-j,i,j], a 49-term gather-sum.
-      const int ng = side ? p.ng_b : p.ng_a;
-      if (ng == 0 || ng > 2 || (side ? p.ng_a : p.ng_b)) continue;
-      const CeGather* gs = side ? p.gb : p.ga;
-      const int64_t* ss = side ? p.sb : p.sa;
-      const int64_t* os = side ? p.sa : p.sb;
-      bool fits = true;
-      double taps = 1, plain_k = 1, t_elems = 1, g_elems = 1;
-      for (int g = 0; g < ng; ++g) {
-        const int pv = gs[g].pv, qv = gs[g].qv;
-        // (p: an output position, q: a filter tap -- a gather whose "taps" outnumber its
-        // positions is a filter gradient, which the stream kernel's dwgrad path handles)
-        if (gs[g].wrap || p.cls[pv] == CE_K || ss[pv] || os[pv] || p.cls[qv] != CE_K || ss[qv] || !os[qv] ||
-            p.ext[pv] < p.ext[qv])
-          fits = false;
-        for (int h = 0; h < ng; ++h)
-          if (h != g && (gs[h].pv == pv || gs[h].qv == qv || gs[h].pv == qv || gs[h].qv == pv)) fits = false;
-        taps *= static_cast<double>(p.ext[qv]);
-        t_elems *= static_cast<double>(gs[g].extent) * static_cast<double>(p.ext[qv]);
-        g_elems *= static_cast<double>(gs[g].extent);
-      }
-      if (!fits) continue;
-      std::vector<char> is_p(static_cast<std::size_t>(p.nv), 0);
-      for (int g = 0; g < ng; ++g) is_p[static_cast<std::size_t>(gs[g].pv)] = 1;
-      for (int v = 0; v < p.nv; ++v) {
-        if (p.cls[v] == CE_K && ss[v] && os[v]) plain_k *= static_cast<double>(p.ext[v]);
-        if (p.cls[v] != CE_K && !is_p[static_cast<std::size_t>(v)]) t_elems *= static_cast<double>(p.ext[v]);
-        if (ss[v]) g_elems *= static_cast<double>(p.ext[v]);
-      }
-      if (taps < 9 || plain_k < 2 || t_elems >= 2147483647.0 || t_elems > std::max(536870912.0, 8.0 * g_elems))
-        continue;
-      // step 1: gathers replaced by plain feature axes u; p vars vanish; taps become outputs
-      CeProblem q1 = p;
-      int64_t* s1 = side ? q1.sb : q1.sa;
-      int uvar[2] = {-1, -1};
-      for (int g = 0; g < ng; ++g) {
-        if (q1.nv >= CE_MAX_VARS) fits = false;
-        if (!fits) break;
-        const int u = q1.nv++;
-        uvar[g] = u;
-        q1.ext[u] = gs[g].extent;
-        q1.cls[u] = side ? CE_N : CE_M;
-        q1.sa[u] = q1.sb[u] = q1.sc[u] = 0;
-        s1[u] = gs[g].stride;
-        const int pv = gs[g].pv, qv = gs[g].qv;
-        q1.ext[pv] = 1;
-        q1.sa[pv] = q1.sb[pv] = q1.sc[pv] = 0;
-        q1.cls[qv] = side ? CE_M : CE_N;
-      }
-      if (!fits) continue;
-      (side ? q1.ng_b : q1.ng_a) = 0;
-      q1.accumulate = 0;
-      // T layout: the gathered operand's non-K axes in its stride order (innermost first,
-      // pitch padded to 16 B), then the partner's, then the taps outermost (so the gather-sum
-      // reads T along the gathered operand's unit-stride axis)
-      std::vector<int> lay;
-      for (int pass = 0; pass < 3; ++pass) {
-        std::vector<int> vs;
-        for (int v = 0; v < q1.nv; ++v) {
-          if (q1.ext[v] <= 1 || q1.cls[v] == CE_K) continue;
-          bool tap = false;
-          for (int g = 0; g < ng; ++g) tap |= v == gs[g].qv;
-          const int64_t* s1o = side ? q1.sa : q1.sb;
-          const bool mine = s1[v] != 0 && !tap, theirs = s1o[v] != 0 && !tap;
-          if ((pass == 0 && mine) || (pass == 1 && theirs && !mine) || (pass == 2 && tap)) vs.push_back(v);
-        }
-        const int64_t* key = pass == 1 ? (side ? q1.sa : q1.sb) : s1;
-        std::stable_sort(vs.begin(), vs.end(), [&](int x, int y) { return pass == 2 ? x < y : key[x] < key[y]; });
-        lay.insert(lay.end(), vs.begin(), vs.end());
-      }
-      int64_t acc = 1;
-      std::vector<int64_t> tstr(static_cast<std::size_t>(q1.nv), 0);
-      for (std::size_t i = 0; i < lay.size(); ++i) {
-        tstr[static_cast<std::size_t>(lay[i])] = acc;
-        acc *= i == 0 ? (q1.ext[lay[i]] + 3) / 4 * 4 : q1.ext[lay[i]];
-      }
-      for (int v = 0; v < q1.nv; ++v) q1.sc[v] = q1.cls[v] == CE_K ? 0 : tstr[static_cast<std::size_t>(v)];
-      // step 2: C[...] (+)= sum_taps T[..., u = sp*p + sq*q + c, ..., q]
-      CeProblem q2 = p;
-      q2.unary = 1;
-      q2.ng_a = ng;
-      q2.ng_b = 0;
-      for (int v = 0; v < q2.nv; ++v) {
-        q2.sb[v] = 0;
-        bool tap = false;
-        for (int g = 0; g < ng; ++g) tap |= v == gs[g].qv;
-        if (p.cls[v] == CE_K && !tap) {
-          q2.ext[v] = 1;  // contracted in step 1
-          q2.sa[v] = q2.sc[v] = 0;
-          continue;
-        }
-        q2.sa[v] = is_p[static_cast<std::size_t>(v)] ? 0 : tstr[static_cast<std::size_t>(v)];
-      }
-      for (int g = 0; g < ng; ++g) {
-        q2.ga[g] = gs[g];
-        q2.ga[g].stride = tstr[static_cast<std::size_t>(uvar[g])];
-      }
-      const BufRef tref{BufRef::kWork, alloc(acc)};
-      add_problem(list, q1, a, b, tref, node, label + ":col2im-gemm");
-      add_problem(list, q2, tref, BufRef{}, c, node, label + ":col2im-sum");
-      return;
-    }
+    if (!ok && try_col2im()) return;
     if (ok && st.tc.params.oa.mn_major && st.tc.params.ob.mn_major && st.tc.params.k_iters > 64) {
       // Both operands would be transposed in shared memory every stage: over a long K
       // loop that is smem-bandwidth bound (measured 2.2x slower than the MMA).  Repack B
