@@ -226,6 +226,26 @@ CeProblem repack(CeProblem& p, bool side_b, const std::vector<int>& inner_order,
     if (x.rank != y.rank) return x.rank < y.rank;
     return x.stride < y.stride;
   });
+  // the output vars among the rest take their slots in C's stride order: the tile units they
+  // form then enumerate columns / rows in C order, so the epilogue's 4-column groups are
+  // contiguous in C (float4 stores) -- K vars keep their slots (same K units)
+  // Opt-in (CE_PACK_CORDER=1): RTR 64->128 layer 64.3 -> 60.9 ms, but conv1 17.0 -> 17.4 ms
+  // and the cfg2 step +0.3% (3 A/B pairs), so not the default.
+  static const bool c_order = [] {
+    const char* e = std::getenv("CE_PACK_CORDER");
+    return e && *e == '1';
+  }();
+  if (c_order) {
+    std::vector<std::size_t> slots;
+    std::vector<Ax> outs;
+    for (std::size_t i = 0; i < ax.size(); ++i)
+      if (ax[i].rank >= (1 << 20) && ax[i].var >= 0 && p.cls[ax[i].var] != CE_K && p.sc[ax[i].var]) {
+        slots.push_back(i);
+        outs.push_back(ax[i]);
+      }
+    std::stable_sort(outs.begin(), outs.end(), [&](const Ax& x, const Ax& y) { return p.sc[x.var] < p.sc[y.var]; });
+    for (std::size_t k = 0; k < slots.size(); ++k) ax[slots[k]] = outs[k];
+  }
   CeProblem pk{};
   pk.unary = 1;
   int64_t acc = 1;
