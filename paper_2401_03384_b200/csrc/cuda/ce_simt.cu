@@ -1200,8 +1200,18 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
   // each thread keeping >= 32 K terms
   const int64_t blocks = klane ? (outs + 7) / 8 : (outs + 255) / 256;
   int64_t split = 1;
-  if (d.dwgrad)  // ~4 waves of 256-thread CTAs, each thread >= 64 K steps
+  if (d.dwgrad) {  // ~4 waves of 256-thread CTAs, each thread >= 64 K steps
+    // few outputs (a 7x7 filter over 11 ranks: 3 lane quads) with a long K: tens of
+    // thousands of slices would all red.add into the same 21 float4s; capping the slices
+    // at ~16K / outs (measured sweep 4K..64K) trades that contention for longer threads
+    // (CP conv1 filter gradients 1.15 -> 0.37 ms, CP 64->64 @56 cr0.1 266 -> 147 us)
+    static const int64_t cap = [] {
+      const char* e = std::getenv("CE_DWG_SLICES");
+      return e ? std::atoll(e) : int64_t{16384};
+    }();
     split = std::max<int64_t>(1, std::min<int64_t>((148 * 256 * 4 + outs - 1) / outs, K / 64));
+    if (cap > 0 && outs < 16) split = std::min<int64_t>(split, std::max<int64_t>(1, cap / outs));
+  }
   else if (blocks < 148 * 8 && K >= 64)
     split = std::min<int64_t>((148 * 8 + blocks - 1) / blocks, K / (klane ? 1024 : 32));
   split = std::max<int64_t>(1, std::min<int64_t>(split, 65535));

@@ -16,15 +16,17 @@ View dense_view(const Subscripts& subs, const std::vector<int64_t>& dims) {
 View padded_view(const Subscripts& subs, const std::vector<int64_t>& dims, int64_t align) {
   View v{subs, dims, std::vector<int64_t>(dims.size())};
   // The innermost axis is padded to `align` elements (16-B row pitch for TMA), except a
-  // short one whose product with its neighbour is already aligned (RTR's 10x10 rank
+  // short one whose product with its short neighbour is already aligned (RTR's 10x10 rank
   // pairs): left dense, the pair stays one contiguous run that merges into one unit.
-  static const bool pair = [] {
+  static const int pair = [] {  // CE_PAD_PAIR: 0 off, 2 any neighbour (experiment)
     const char* e = std::getenv("CE_PAD_PAIR");
-    return !(e && *e == '0');
+    return e ? std::atoi(e) : 1;
   }();
   const std::size_t n = dims.size();
+  // (both axes short: a CP `bhwr` with r = 27 keeps its padded pitch, which the stencil
+  // and filter-gradient kernels need for float4 rows)
   const bool dense_pair = pair && n >= 2 && dims[n - 1] % align != 0 && dims[n - 1] < 32 &&
-                          (dims[n - 1] * dims[n - 2]) % align == 0;
+                          (dims[n - 2] < 32 || pair == 2) && (dims[n - 1] * dims[n - 2]) % align == 0;
   int64_t acc = 1;
   for (std::size_t i = n; i-- > 0;) {
     v.strides[i] = acc;
