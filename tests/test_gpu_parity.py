@@ -157,6 +157,8 @@ LAYER_CASES = [
     ("cfg5 dense", "standard", 256, 256, 14, 128, []),
     # cfg4 CP stack first layer (7x7 at 112x112, 3->64), reduced batch
     ("cfg4 CP conv1 cr1.0", "cp", 64, 3, 112, 8, 1.0),
+    # R = 11: 3 lane quads, filter-gradient K slices capped (same-address atomics)
+    ("cfg4 CP conv1 cr0.1 B32", "cp", 64, 3, 112, 32, 0.1),
 ]
 
 
