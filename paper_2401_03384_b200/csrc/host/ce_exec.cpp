@@ -207,7 +207,7 @@ namespace {
 // pitch padded to 16 B) and every other axis keeps its relative order.  Returns
 // the pack problem and patches p's strides for that operand in place.
 CeProblem repack(CeProblem& p, bool side_b, const std::vector<int>& inner_order, int64_t* span,
-                 const int64_t* partner = nullptr) {
+                 const int64_t* partner = nullptr, bool out_c_order = false) {
   int64_t* s = side_b ? p.sb : p.sa;
   CeGather* g = side_b ? p.gb : p.ga;
   const int ng = side_b ? p.ng_b : p.ng_a;
@@ -235,7 +235,7 @@ CeProblem repack(CeProblem& p, bool side_b, const std::vector<int>& inner_order,
     const char* e = std::getenv("CE_PACK_CORDER");
     return e && *e == '1';
   }();
-  if (c_order) {
+  if (c_order || out_c_order) {
     std::vector<std::size_t> slots;
     std::vector<Ax> outs;
     for (std::size_t i = 0; i < ax.size(); ++i)
@@ -636,7 +636,9 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
           int64_t span = 0, pspan = 0;
           const CeProblem pk = expand(q, side == 1, order, &span);
           CeProblem ppk{};
-          if (pack_partner) ppk = repack(q, side == 0, order, &pspan, nullptr);
+          // (output vars in C order: the expanded step's tile columns then match C, e.g. RTR
+          // X*F writing 10x10 rank pairs as contiguous 100-float rows)
+          if (pack_partner) ppk = repack(q, side == 0, order, &pspan, nullptr, true);
           TcPlan t;
           if (!ce_tc_plan(q, &t)) continue;
           Step es;
