@@ -928,10 +928,10 @@ std::string Executor::describe() const {
         if (std::getenv("CE_DESCRIBE_UNITS")) {
           std::string u = " ";
           n = static_cast<int>(std::strlen(line)) - 1;  // before the newline
-          for (int pass = 0; pass < 2; ++pass) {
-            u += pass ? " nt=[" : "mt=[";
-            const int32_t* list = pass ? P.nt : P.mt;
-            for (int i = 0; i < (pass ? P.nn : P.nm); ++i) {
+          for (int pass = 0; pass < 3; ++pass) {
+            u += pass == 2 ? " gu=[" : pass ? " nt=[" : "mt=[";
+            const int32_t* list = pass == 2 ? P.gu : pass ? P.nt : P.mt;
+            for (int i = 0; i < (pass == 2 ? P.ng : pass ? P.nn : P.nm); ++i) {
               const TcUnit& U = P.u[list[i]];
               u += std::to_string(U.box) + "/" + std::to_string(U.ext) + ":";
               for (int k = 0; k < U.nv; ++k) u += std::to_string(U.vext[k]) + "@" + std::to_string(U.sc[k]) + (k + 1 < U.nv ? "," : "");

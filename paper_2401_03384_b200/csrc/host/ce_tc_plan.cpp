@@ -255,6 +255,10 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   TcParams& P = plan->params;
   std::memset(&P, 0, sizeof(P));
   // M tile from A, N tile from B
+  static const bool cinner = [] {  // CE_TC_CINNER=0: tile search ignores C's unit-stride axis
+    const char* e = std::getenv("CE_TC_CINNER");
+    return !(e && *e == '0');
+  }();
   static const bool balance_n = [] {  // CE_TC_BALANCE_N=0: widest N boxes (previous tiling)
     const char* e = std::getenv("CE_TC_BALANCE_N");
     return !(e && *e == '0');
@@ -294,10 +298,18 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     std::function<void(std::size_t, int)> search = [&](std::size_t i, int room) {
       if (i == cand.size()) {
         int64_t tiles = 1, r = 1;
+        bool split_cinner = false;
         for (std::size_t j = 0; j < cand.size(); ++j) {
           tiles *= (ext[j] + b[j] - 1) / b[j];
           r *= b[j];
+          // an M unit that is C's unit-stride axis, cut into boxes of < 4: every tile row
+          // then writes runs shorter than 16 B (RTR dZ rows: 2 of a 10-float run; tt1.0's
+          // NCHW output 2 of 14 w).  Measured: cfg2 step -1.2%, tt1.0 711 -> 688 us, RTR
+          // 64->128 61.6 -> 58.6 ms; a box of 4 (RTR @56) is better left alone (5.10 vs 5.27 ms)
+          const TcUnit& uu = U[static_cast<std::size_t>(cand[j])];
+          split_cinner |= cinner && cls == CE_M && uu.nv >= 1 && uu.sc[0] == 1 && b[j] < ext[j] && b[j] < 4;
         }
+        if (split_cinner) tiles = tiles * 3 / 2;
         // M: the MMA is always 128 rows, so use as many as fit; N: the MMA width follows the
         // tile, so among equal tile counts the narrowest box pads least (273 -> 2 x 137)
         if (tiles < best_tiles || (tiles == best_tiles && (minbox ? r < best_rows : r > best_rows))) {
