@@ -581,17 +581,19 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     return !(e && *e == '0');
   }();
   P.mcast = 0;
-  if (mcast_enabled && b_mn == 0 && P.nn == 1 && P.tiles_m >= 2 && P.n_cols >= 64 &&
+  static const bool pair_enabled = [] {
+    const char* e = std::getenv("CE_TC_PAIR");
+    return !(e && *e == '0');
+  }();
+  // (CE_TC_PAIR=0 now means no cluster at all: the older single-CTA multicast variant
+  // (mcast 1) hung on a CP 64->64 @56 layer's split-K launch and is no longer planned)
+  if (mcast_enabled && pair_enabled && b_mn == 0 && P.nn == 1 && P.tiles_m >= 2 && P.n_cols >= 64 &&
       P.ob.dim[1].u0 == P.nt[0]) {
     const int half = ((P.n_cols + 1) / 2 + 7) / 8 * 8;
     if (2 * half <= plan->bn) {
       P.mc_half = half;
       P.mc_ndim = 1;
       plan->box_b[1] = static_cast<uint32_t>(half);
-      static const bool pair_enabled = [] {
-        const char* e = std::getenv("CE_TC_PAIR");
-        return !(e && *e == '0');
-      }();
       if (pair_enabled) {
         // CTA pair, M=256 cta_group::2 MMAs: each CTA stages its own half of the B columns
         P.mcast = 2;
