@@ -259,6 +259,10 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     const char* e = std::getenv("CE_TC_CINNER");
     return !(e && *e == '0');
   }();
+  static const bool nalign = [] {  // CE_TC_NALIGN=0: balanced N boxes not kept 16-B aligned
+    const char* e = std::getenv("CE_TC_NALIGN");
+    return !(e && *e == '0');
+  }();
   static const bool balance_n = [] {  // CE_TC_BALANCE_N=0: widest N boxes (previous tiling)
     const char* e = std::getenv("CE_TC_BALANCE_N");
     return !(e && *e == '0');
@@ -323,7 +327,13 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
       for (int x = hi; x >= 1; --x) {
         // only boxes that are the full extent or change the tile count are worth trying
         if (!minbox && x < hi && (ext[i] + x - 1) / x == (ext[i] + x) / (x + 1)) continue;
-        if (minbox && x < hi && x > 1 && (ext[i] + x - 1) / x == (ext[i] + x - 2) / (x - 1)) continue;
+        // (balanced N boxes stay multiples of 4 so every N tile starts 16-B aligned in C and
+        // the epilogue keeps its float4 column groups: 275 = 140 + 135, not 138 + 137)
+        if (minbox && nalign && x < hi && ext[i] >= 8) {
+          if (x % 4 || (x > 4 && (ext[i] + x - 1) / x == (ext[i] + x - 5) / (x - 4))) continue;
+        } else if (minbox && x < hi && x > 1 && (ext[i] + x - 1) / x == (ext[i] + x - 2) / (x - 1)) {
+          continue;
+        }
         b[i] = x;
         search(i + 1, room / x);
       }
