@@ -50,6 +50,10 @@ struct CeProblem {
   int64_t sc[CE_MAX_VARS];   // stride of var v in out (Z/M/N vars only)
   CeGather ga[CE_MAX_GATHER];
   CeGather gb[CE_MAX_GATHER];
+  // 1: that operand is a caller-owned buffer with no slack past its logical span (set per
+  // launch), so no float4 access may run past a row whose extent is not a multiple of 4
+  // (workspace buffers are allocated in 256-B units and padded per row)
+  int32_t exact_a, exact_b, exact_c;
 };
 
 // Compact per-class var lists the SIMT kernels iterate over (built on host).

@@ -1099,13 +1099,15 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
     };
     // A along the lane var: unit stride (float4) or independent of it (one scalar, broadcast)
     const bool a_b = d.nout >= 1 && d.osa[0] == 0;
-    bool ok = d.nout >= 1 && (a_b || (al(A) && d.osa[0] == 1 && padded(d.osa, d.ksa, 0)));
+    // a caller-owned operand ends exactly at its last row: no float4 past a ragged row end
+    const bool ragged = ext0 % 4 != 0;
+    bool ok = d.nout >= 1 && (a_b || (al(A) && d.osa[0] == 1 && padded(d.osa, d.ksa, 0) && !(ragged && p.exact_a)));
     for (int g = 0; g < 2 * SV_G && ok; ++g) ok = d.go[g][0] == 0;
     d.a_bcast = a_b ? 1 : 0;
     d.vec = ok ? 1 : 0;
     if (ok) {
-      const bool vb = !p.unary && al(B) && d.osb[0] == 1 && padded(d.osb, d.ksb, 1);
-      const bool vc = al(C) && d.osc[0] == 1 && padded(d.osc, nullptr, 2);
+      const bool vb = !p.unary && al(B) && d.osb[0] == 1 && padded(d.osb, d.ksb, 1) && !(ragged && p.exact_b);
+      const bool vc = al(C) && d.osc[0] == 1 && padded(d.osc, nullptr, 2) && !(ragged && p.exact_c);
       d.vec_b = vb ? 1 : 0;
       d.vec_c = vc ? 1 : 0;
       d.lext = ext0;

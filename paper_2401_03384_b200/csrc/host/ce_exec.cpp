@@ -1045,6 +1045,18 @@ void Executor::run_concurrent(std::vector<Step>& steps, const std::vector<char>*
     }
 }
 
+namespace {
+// the step's SIMT descriptor with the caller-owned-buffer flags of its operands
+CeSimtDesc exact(const Step& st) {
+  auto user = [](const BufRef& r) { return r.kind != BufRef::kWork && r.kind != BufRef::kNone ? 1 : 0; };
+  CeSimtDesc d = st.desc;
+  d.p.exact_a = user(st.a);
+  d.p.exact_b = user(st.b);
+  d.p.exact_c = user(st.c);
+  return d;
+}
+}  // namespace
+
 void Executor::launch_step(Step& st, cudaStream_t s) {
   const float* A = resolve(st.a);
   const float* B = resolve(st.b);
@@ -1060,11 +1072,11 @@ void Executor::launch_step(Step& st, cudaStream_t s) {
     }
     cudaError_t e = cudaSuccess;
     switch (st.kind) {
-      case Step::kDirect: e = ce_launch_direct(st.desc, A, B, C, s); break;
+      case Step::kDirect: e = ce_launch_direct(exact(st), A, B, C, s); break;
       case Step::kTiled: e = ce_launch_tiled(st.desc, A, B, C, st.a_kfast, st.b_kfast, s); break;
       case Step::kTc: e = ce_launch_tc(st.tc, A, B, C, s); break;
       case Step::kZero: e = cudaMemsetAsync(C, 0, static_cast<size_t>(st.zero_elems) * 4, s); break;
-      case Step::kReduce: e = ce_launch_reduce(st.desc, A, B, C, st.zero_elems, s); break;
+      case Step::kReduce: e = ce_launch_reduce(exact(st), A, B, C, st.zero_elems, s); break;
       case Step::kPermute: e = ce_launch_permute(st.desc.p, A, C, s); break;
     }
     cuda_check(e, st.label.c_str());
