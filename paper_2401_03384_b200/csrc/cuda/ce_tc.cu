@@ -36,14 +36,7 @@ __device__ unsigned long long g_tc_ts[160 * 16];
 // Debug-only per-iteration timestamps of CTA 0 (P.dbg & 512): [role][iteration], role 0
 // producer (after its empty wait), 1 MMA issuer (after its full wait).
 __device__ unsigned long long g_tc_it[3 * 256];
-// grid barriers of the in-kernel C zeroing (TcParams::zero_c): {arrivals, generation}
-__device__ unsigned int g_tc_zbar[256][2];
 
-__device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned int* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ void stamp_it(const TcParams& P, int role, uint32_t gi) {
   if ((P.dbg & 512) && blockIdx.x == 0 && gi < 256) {  // role 2: epilogue, slot tile*4 + phase
     long long t;
@@ -768,35 +761,6 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     uint32_t local = 0;
     Tile& T = tiles[1 + grp];
     int cols_for[2] = {-1, -1};  // N tile whose column tables each accumulator buffer holds
-    bool zero_wait = P.zero_c != 0;
-    uint32_t zgen = 0;
-    if (zero_wait) {
-      // zero C (every CTA a grid-strided share), then arrive at the launch's grid barrier;
-      // the atomic stores wait for it below.  After the PDL wait: earlier kernels may read C.
-      ce_pdl_wait();
-      unsigned int* zb = g_tc_zbar[P.zslot];
-      if (et == 0) zgen = ld_acquire_u32(zb + 1);
-      if (grp == 0) {
-        const int64_t n = P.zspan, nthr = static_cast<int64_t>(gridDim.x) * (32 * kEpiWarps);
-        const int64_t t0 = static_cast<int64_t>(blockIdx.x) * (32 * kEpiWarps) + et;
-        int64_t tail = 0;
-        if (c_al) {
-          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int64_t i = t0; i < n / 4; i += nthr) reinterpret_cast<float4*>(C)[i] = z;
-          tail = n / 4 * 4;
-        }
-        for (int64_t i = tail + t0; i < n; i += nthr) C[i] = 0.f;
-        epi_bar(1);
-        if (et == 0) {
-          __threadfence();
-          if (atomicAdd(zb, 1u) == gridDim.x - 1) {
-            zb[0] = 0;
-            __threadfence();
-            atomicAdd(zb + 1, 1u);
-          }
-        }
-      }
-    }
     WorkIter wi;
     work_begin(P, group, ngroups, wi);
     uint32_t item = 0xffffffffu;
@@ -860,12 +824,6 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (local == 0) ce_pdl_wait();  // (long complete: the producer waited before its loads)
-      if (zero_wait) {  // C zeroed by every CTA
-        if (et == 0)
-          while (ld_acquire_u32(g_tc_zbar[P.zslot] + 1) == zgen) __nanosleep(100);
-        epi_bar(1 + grp);
-        zero_wait = false;
-      }
       const bool empty_k = k1 <= k0;
       const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
       // TMEM loads double-buffered against the stores: chunk c+1 is read while chunk c drains
@@ -1133,8 +1091,7 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
       }
     }
   }
-  P.zspan = plan.out_span;
-  if ((P.k_split > 1 || P.sk_r > 0) && !P.zero_c) {
+  if (P.k_split > 1 || P.sk_r > 0) {
     cudaError_t e = cudaMemsetAsync(C, 0, static_cast<size_t>(plan.out_span) * 4, s);
     if (e != cudaSuccess) return e;
   }

@@ -127,12 +127,6 @@ struct TcParams {
   int32_t mc_ndim;         // TMA dim of B that carries the N tile
   int32_t mn_lbo, mn_sbo;  // MN-major descriptor strides (bytes)
   int32_t dbg;             // debug: bit0 skip MMAs, bit1 skip TMA loads (timing experiments only)
-  // Quantisation split-K (k_split == 2 on a launch whose tiles fill 1.x waves): C is zeroed
-  // inside the kernel by the epilogue warps of every CTA, then a grid barrier (slot zslot of
-  // g_tc_zbar) precedes the first atomic store -- no memset node breaking the PDL chain.
-  int32_t zero_c;
-  uint32_t zslot;
-  int64_t zspan;           // floats of C to zero
 };
 
 // Host-side plan: everything except the pointer-dependent tensor maps.

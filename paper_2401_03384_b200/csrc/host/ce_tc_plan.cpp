@@ -624,26 +624,6 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     const int64_t ctas = (tm + csize - 1) / csize * csize * tn * gz;
     int split = 1;
     if (ctas < 148 && ki >= 16) split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 / ctas, ki / 8)));
-    // tiles filling 1.x waves (196 conv tiles on 148 SMs: 2 rounds for 1.32 rounds of work):
-    // two K halves make 3 rounds of half-length items, with C zeroed inside the kernel
-    // Off by default (CE_TC_QSPLIT=1 enables): tk1.0's two conv launches drop 70 -> 66 and
-    // 74 -> 68 us, but the cfg2 step does not move (1.4537 vs 1.4568 ms over 4 A/B pairs)
-    static const bool qsplit_on = [] {
-      const char* e = std::getenv("CE_TC_QSPLIT");
-      return e && *e == '1';
-    }();
-    P.zero_c = 0;
-    // (transposed-store launches only: their atomic epilogue is red.v4; the row-store
-    // path's scalar atomics cost more than the shorter last round saves, measured)
-    if (qsplit_on && split == 1 && ctas > 148 && ki >= 24 && P.transpose_store) {
-      const int64_t cost1 = (ctas + 147) / 148 * ki, cost2 = (2 * ctas + 147) / 148 * ((ki + 1) / 2);
-      if (5 * cost2 <= 4 * cost1) {
-        static uint32_t next_slot = 0;
-        split = 2;
-        P.zero_c = 1;
-        P.zslot = next_slot++ % 256u;
-      }
-    }
     if (gz * split > 65535) return fail("grid z too large");
     P.k_split = split;
   }
