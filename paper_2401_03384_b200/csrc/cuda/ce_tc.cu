@@ -31,6 +31,14 @@ constexpr int kXposeWarps = 4;
 constexpr int kThreads = 64 + 32 * kEpiWarps + 32 * kXposeWarps;
 constexpr int kStagePitch = 36;  // floats per staged row: 16-B aligned, conflict-free float4 phases
 
+// Debug flags (timing experiments, phase stamps) are compiled in only with -DCE_TC_DEBUG=1
+// (`make TC_DEBUG=1`): their branches cost registers, and the kernel already runs at the
+// register cap (spills raise the cfg2 step time measurably).
+#ifndef CE_TC_DEBUG
+#define CE_TC_DEBUG 0
+#endif
+#define TC_DBG(p) (CE_TC_DEBUG ? (p).dbg : 0)
+
 // Debug-only phase timestamps (P.dbg & 32): [cta][slot] = %globaltimer (ns).
 __device__ unsigned long long g_tc_ts[160 * 16];
 // Debug-only per-iteration timestamps of CTA 0 (P.dbg & 512): [role][iteration], role 0
@@ -38,14 +46,14 @@ __device__ unsigned long long g_tc_ts[160 * 16];
 __device__ unsigned long long g_tc_it[3 * 256];
 
 __device__ __forceinline__ void stamp_it(const TcParams& P, int role, uint32_t gi) {
-  if ((P.dbg & 512) && blockIdx.x == 0 && gi < 256) {  // role 2: epilogue, slot tile*4 + phase
+  if ((TC_DBG(P) & 512) && blockIdx.x == 0 && gi < 256) {  // role 2: epilogue, slot tile*4 + phase
     long long t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles (cheap; same SM for all roles)
     g_tc_it[role * 256 + gi] = static_cast<unsigned long long>(t);
   }
 }
 __device__ __forceinline__ void stamp(const TcParams& P, int slot) {
-  if (P.dbg & 32) {
+  if (TC_DBG(P) & 32) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (blockIdx.x < 160) g_tc_ts[blockIdx.x * 16 + slot] = t;
@@ -453,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     for (int i = threadIdx.x; i < static_cast<int>(sizeof(TcParams) / 16); i += kThreads) dst[i] = src[i];
   }
   const TcParams& P = *sP;
-  if (Pg.dbg & 128) return;  // timing experiment: launch cost only
+  if (TC_DBG(Pg) & 128) return;  // timing experiment: launch cost only
   const bool xpose = Pg.oa.mn_major || Pg.ob.mn_major;
   const bool mc = !PAIR && Pg.mcast != 0;
   const uint32_t csize = (mc || PAIR) ? 2u : 1u;
@@ -503,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   // above and the first tile's decoding / address tables overlap the predecessor's tail.
   ce_pdl_trigger();
 
-  if (P.dbg & 64) {
+  if (TC_DBG(P) & 64) {
     // timing experiment: set-up and tear-down only
   } else if (warp == 0) {
     if (lane == 0) {
@@ -512,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       // (the loop period is this thread's instruction latency when the ring is not full).
       const uint32_t bytes = static_cast<uint32_t>(P.oa.stage_bytes + P.ob.stage_bytes);
       const uint32_t full_lead = PAIR ? mapa(&full[0], 0) : 0u;
-      const int dbg = Pg.dbg;
+      const int dbg = TC_DBG(Pg);
       const int nsub_a = P.oa.nsub, nsub_b = P.ob.nsub;
       const int mc_ndim = P.mc_ndim, mc_half = P.mc_half;
       // digit-0 deltas live in registers; carries (rare) and per-tile set-up read shared memory
@@ -628,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ---------------------------------------------------------- MMA issuer
-      const int dbg = Pg.dbg;
+      const int dbg = TC_DBG(Pg);
       const uint32_t idesc = P.idesc;
       const int kc0 = P.kcount[0], ktail = P.ktail_kk;
       // descriptors of stage 0; stage s and K step kk add (s * bytes + kk * 32) >> 4 to the
@@ -724,13 +732,13 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
                 *reinterpret_cast<float4*>(blk + lane * 128 + ((j ^ (lane & 7)) << 4)) =
                     make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
-          } else if (P.oa.mn_major && !(P.dbg & 8192)) {
+          } else if (P.oa.mn_major && !(TC_DBG(P) & 8192)) {
             for (int j = xw; j < P.oa.nsub; j += kXposeWarps) xpose_block(sA + s * A_BYTES + j * 4096, lane);
           }
-          if (P.ob.mn_major && !(P.dbg & 8192))
+          if (P.ob.mn_major && !(TC_DBG(P) & 8192))
             for (int j = xw; j < P.ob.nsub; j += kXposeWarps) xpose_block(sB + s * B_BYTES + j * 4096, lane);
           // generic-proxy smem writes must be visible to the tensor core (async proxy)
-          if (!(P.dbg & 16384)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (!(TC_DBG(P) & 16384)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (PAIR && !leader)
             mbar_arrive_cluster(mapa(&ready[s], 0));  // the even CTA issues the pair's MMAs
           else
@@ -754,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
     const int et = threadIdx.x - 64 - grp * 32 * kEpiWarps;  // 0..127 within the group
     float* stage = stage_out + ew * 32 * kStagePitch;
 
-    const int dbg = Pg.dbg;
+    const int dbg = TC_DBG(Pg);
     const int n_cols = P.n_cols, m_rows = P.m_rows;
     const bool tstore = P.transpose_store != 0;
     const bool c_al = (reinterpret_cast<uintptr_t>(C) & 15u) == 0;
