@@ -1,5 +1,8 @@
 """Per-step device times of single pairwise problems (TC kernel experiments).
-usage: CE_TC_DBG=<flags> python tools/tc_micro.py  [cases from CASES env, python literal list of (expr, dims)]"""
+usage: CE_TC_DBG=<flags> python tools/tc_micro.py  [cases from CASES env, python literal list of (expr, dims)]
+Needs the debug build of the TC kernel (flags and stamps are compiled out otherwise):
+  rm -rf build && make -C paper_2401_03384_b200/csrc TC_DEBUG=1   (rebuild normally afterwards)
+"""
 import os
 import sys
 

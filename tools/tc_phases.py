@@ -1,4 +1,7 @@
-"""Phase timestamps of one TC launch (CE_TC_DBG=32): python tools/tc_phases.py tk 0.1 <step-label>"""
+"""Phase timestamps of one TC launch (CE_TC_DBG=32): python tools/tc_phases.py tk 0.1 <step-label>
+Needs the debug build of the TC kernel (flags and stamps are compiled out otherwise):
+  rm -rf build && make -C paper_2401_03384_b200/csrc TC_DEBUG=1   (rebuild normally afterwards)
+"""
 import ctypes
 import os
 import sys

@@ -1,5 +1,8 @@
 """Phase + per-iteration timestamps of the factor-gradient (dB) TC launch of one pairwise node.
-EXPR/DIMS env as in tc_phases.py; CE_TC_DBG = 32 | EXTRA_DBG."""
+EXPR/DIMS env as in tc_phases.py; CE_TC_DBG = 32 | EXTRA_DBG.
+Needs the debug build of the TC kernel (flags and stamps are compiled out otherwise):
+  rm -rf build && make -C paper_2401_03384_b200/csrc TC_DEBUG=1   (rebuild normally afterwards)
+"""
 import ctypes
 import os
 import sys

@@ -1,5 +1,8 @@
 """Phase + per-iteration stamps of ONE TC launch inside a cfg2 layer's fwd+bwd (graphs off).
-usage: CE_TC_DBG=544 CE_TC_DBG_AT=<n-th TC launch> python tools/tc_phases_layer.py tk 1.0"""
+usage: CE_TC_DBG=544 CE_TC_DBG_AT=<n-th TC launch> python tools/tc_phases_layer.py tk 1.0
+Needs the debug build of the TC kernel (flags and stamps are compiled out otherwise):
+  rm -rf build && make -C paper_2401_03384_b200/csrc TC_DEBUG=1   (rebuild normally afterwards)
+"""
 import ctypes
 import os
 import sys
