@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libce.so")
+# CE_LIB_PATH: an alternate build of the same library for same-box A/B experiments
+LIB_PATH = os.environ.get("CE_LIB_PATH") or os.path.join(_HERE, "libce.so")
 
 c_i64p = ctypes.POINTER(ctypes.c_int64)
 c_intp = ctypes.POINTER(ctypes.c_int)
