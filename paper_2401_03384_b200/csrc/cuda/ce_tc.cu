@@ -463,7 +463,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   const TcParams& P = *sP;
   if (TC_DBG(Pg) & 128) return;  // timing experiment: launch cost only
   const bool xpose = Pg.oa.mn_major || Pg.ob.mn_major;
-  const bool mc = !PAIR && Pg.mcast != 0;
+  // (the single-CTA B multicast, mcast 1, is no longer planned -- see ce_tc_plan.cpp;
+  // compiled out so the non-pair instances carry no multicast code)
+  constexpr bool mc = false;
   const uint32_t csize = (mc || PAIR) ? 2u : 1u;
   uint32_t rank = 0;
   if (csize == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
