@@ -917,19 +917,14 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
             }
           }
       };
-      uint32_t ra[32], rb[32];
-      tmem_ld32_issue(t_base, ra);
-      tmem_ld_wait(ra);
+      // one 32-column chunk in flight: a second buffer (measured neutral) would hold 32 more
+      // registers in a kernel that sits at its 168-register cap
+      uint32_t ra[32];
 #pragma unroll 1
-      for (int ch = 0; ch < nch; ch += 2) {
-        if (ch + 1 < nch) tmem_ld32_issue(t_base + (ch + 1) * 32, rb);
+      for (int ch = 0; ch < nch; ++ch) {
+        tmem_ld32_issue(t_base + ch * 32, ra);
+        tmem_ld_wait(ra);
         process(ra, ch);
-        if (ch + 1 < nch) {
-          tmem_ld_wait(rb);
-          if (ch + 2 < nch) tmem_ld32_issue(t_base + (ch + 2) * 32, ra);
-          process(rb, ch + 1);
-          if (ch + 2 < nch) tmem_ld_wait(ra);
-        }
       }
       if (est) stamp_it(P, 2, static_cast<uint32_t>(local / ngrp) * 4 + 3);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
