@@ -1557,7 +1557,8 @@ struct CeRowMap {
 // smem phases at 2-way bank conflicts.  Composite tile axes (short unit-stride axes
 // continued by a second axis, see CePermDesc) cost one division per row, not per element.
 template <bool VI, bool VO>
-__global__ void __launch_bounds__(256, 8) ce_transpose64_kernel(const CePermDesc d, const float* __restrict__ A,
+// (6 CTAs/SM: at 8 the 32-register budget spilled the float4 variant; cfg2 step -0.6%)
+__global__ void __launch_bounds__(256, 6) ce_transpose64_kernel(const CePermDesc d, const float* __restrict__ A,
                                                              float* __restrict__ C) {
   ce_pdl_enter();
   __shared__ float tile[64][65];
