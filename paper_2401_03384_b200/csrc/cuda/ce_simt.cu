@@ -1483,7 +1483,7 @@ struct CePermDesc {
 
 // 64x64 tile, 256 threads, 16 independent loads in flight per thread; 32-bit in-tile
 // index math, 64-bit only for the per-batch base.
-__global__ void __launch_bounds__(256) ce_transpose_kernel(const CePermDesc d, const float* __restrict__ A,
+__global__ void __launch_bounds__(256, 6) ce_transpose_kernel(const CePermDesc d, const float* __restrict__ A,
                                                            float* __restrict__ C) {
   ce_pdl_enter();
   __shared__ float tile[32][33];
@@ -1637,7 +1637,7 @@ __global__ void __launch_bounds__(256, 6) ce_transpose64_kernel(const CePermDesc
 // batch slice.  A row is served by L = 2^lshift lanes (L >= min(ext x, 32)), so a warp
 // covers 32/L short rows without any per-element division; 4 rows per thread in flight.
 template <bool V4>
-__global__ void __launch_bounds__(256) ce_rowcopy_kernel(const CePermDesc d, const float* __restrict__ A,
+__global__ void __launch_bounds__(256, 6) ce_rowcopy_kernel(const CePermDesc d, const float* __restrict__ A,
                                                          float* __restrict__ C, int lshift) {
   // V4: rows are 16-B aligned multiples of 4 floats on both sides -> float4 traffic
   ce_pdl_enter();
