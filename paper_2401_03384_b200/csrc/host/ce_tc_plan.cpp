@@ -591,9 +591,12 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     return !(e && *e == '0');
   }();
   P.mcast = 0;
+  // CTA pairs (cta_group::2 + B multicast) are opt-in (CE_TC_PAIR=1): once the kernel ran
+  // below its register cap, single-CTA launches measured faster on the cfg2 step (1.195 vs
+  // 1.216 ms, same-box A/B x3) and equal or better on every layer profiled
   static const bool pair_enabled = [] {
     const char* e = std::getenv("CE_TC_PAIR");
-    return !(e && *e == '0');
+    return e && *e == '1';
   }();
   // (CE_TC_PAIR=0 now means no cluster at all: the older single-CTA multicast variant
   // (mcast 1) hung on a CP 64->64 @56 layer's split-K launch and is no longer planned)
