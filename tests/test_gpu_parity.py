@@ -438,3 +438,41 @@ def test_rtr_x_first_layers(any_ctx, case):
     assert nerr(out, ref) <= TOL[mode][0]
     for i, (g, r) in enumerate(zip(grads, ref_g)):
         assert nerr(g.cpu().numpy(), r) <= TOL[mode][1], i
+
+
+_PAIR_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2401_03384_b200 as ce
+from paper_2401_03384_b200.device import Context, Executor
+ctx = Context(0, "auto")
+le = ce.expression(ce.LayerSpec("tk", [256], [256], 3, 3, 14, 14, 128, [1, 1]), 1.0)
+plan = ce.optimal(le.expr, le.dims, "same", "training")
+print(plan.describe_steps(True), file=sys.stderr)
+ex = Executor(ctx, plan, backward=True)
+xs = [ctx.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
+dout = ctx.fill_random(plan.out_dims, 2000)
+out = ex.execute(xs)
+grads = ex.backward(xs, dout)
+torch.cuda.synchronize()
+np.savez(sys.argv[2], out=out.cpu().numpy(), *[g.cpu().numpy() for g in grads])
+"""
+
+
+def test_cta_pair_path_opt_in(tmp_path):
+    """CE_TC_PAIR=1 (cta_group::2 M=256 MMAs, B multicast, 2-CTA clusters) agrees with the
+    default single-CTA path on the full cfg2 TK cr1.0 layer."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for flag in ("0", "1"):
+        f = tmp_path / f"p{flag}.npz"
+        env = dict(os.environ, CE_TC_PAIR=flag)
+        r = subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, str(f)], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert ("mc=2" in r.stderr) == (flag == "1"), r.stderr[-3000:]
+        outs[flag] = np.load(f)
+    for k in outs["0"].files:
+        assert nerr(outs["1"][k], outs["0"][k]) <= 2e-3, k
