@@ -149,6 +149,18 @@ __device__ __forceinline__ uint64_t kmajor_desc(uint32_t addr) {
          (1ull << 46) | (2ull << 61);
 }
 
+// SM100 UMMA shared-memory descriptor for an MN-major tf32 operand.  32-bit MN-major
+// operands use the SWIZZLE_128B_BASE32B layout (type 1; CUTLASS Layout_MN_SW128_32B_Atom:
+// 32-B chunks of a 128-B row XOR-swizzled, 4-row atoms), which TMA writes with
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B: 32 MN floats per 128-B row, one row per K index,
+// LBO = 4096 B to the next 32-MN box, SBO = 512 B to the next 4-row K atom.  A K=8 step
+// advances the start address by 8 rows (1024 B).  The upper word (SBO, version, layout)
+// and LBO come from the host (TcParams::mn_desc_hi / mn_lbo16).
+__device__ __forceinline__ uint64_t mnmajor_desc(uint32_t addr, uint32_t lbo16, uint32_t hi) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFF) | (static_cast<uint64_t>(lbo16 & 0x3FFF) << 16) |
+         (static_cast<uint64_t>(hi) << 32);
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -462,7 +474,9 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   }
   const TcParams& P = *sP;
   if (TC_DBG(Pg) & 128) return;  // timing experiment: launch cost only
-  const bool xpose = Pg.oa.mn_major || Pg.ob.mn_major;
+  // MN-major operands are either read by the MMA directly (native: transpose bits in the
+  // instruction descriptor, MN-major smem descriptors) or transposed in smem by warps 6..9
+  const bool xpose = !Pg.native_mn && (Pg.oa.mn_major || Pg.ob.mn_major);
   // (the single-CTA B multicast, mcast 1, is no longer planned -- see ce_tc_plan.cpp;
   // compiled out so the non-pair instances carry no multicast code)
   constexpr bool mc = false;
@@ -580,6 +594,10 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
             // both halves complete on the even CTA's barrier, which expects the pair's bytes
             if (leader) mbar_expect_tx(&full[s], 2 * bytes);
             tma_load_pair(sA + s * A_BYTES, &Pg.ta, full_lead + 8u * s, ca);
+            for (int j = 1; j < nsub_a; ++j) {  // native MN-major A: [32 K][32 MN] boxes at 4 KB steps
+              const int cj[5] = {ca[0] + 32 * j, ca[1], ca[2], ca[3], ca[4]};
+              tma_load_pair(sA + s * A_BYTES + j * 4096, &Pg.ta, full_lead + 8u * s, cj);
+            }
             tma_load_pair(sB + s * B_BYTES, &Pg.tb, full_lead + 8u * s, cb);
           } else {
             // timing experiments: 2048 skips the A loads, 4096 the B loads
@@ -643,7 +661,11 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
       const int kc0 = P.kcount[0], ktail = P.ktail_kk;
       // descriptors of stage 0; stage s and K step kk add (s * bytes + kk * 32) >> 4 to the
       // 14-bit start-address field (smem < 256 KB, so the add never carries out of it)
-      const uint64_t adesc0 = kmajor_desc(smem_u32(sA)), bdesc0 = kmajor_desc(smem_u32(sB));
+      const bool a_nat = P.native_mn && P.oa.mn_major, b_nat = P.native_mn && P.ob.mn_major;
+      const uint64_t adesc0 = a_nat ? mnmajor_desc(smem_u32(sA), P.mn_lbo16, P.mn_desc_hi) : kmajor_desc(smem_u32(sA));
+      const uint64_t bdesc0 = b_nat ? mnmajor_desc(smem_u32(sB), P.mn_lbo16, P.mn_desc_hi) : kmajor_desc(smem_u32(sB));
+      // per K=8 step: +32 B inside a K-major 128-B row, +1024 B (one 8-row atom) MN-major
+      const uint64_t astep = a_nat ? P.mn_kstep16 : 2, bstep = b_nat ? P.mn_kstep16 : 2;
       uint32_t gi = 0, local = 0;
       WorkIter wi;
       work_begin(P, group, ngroups, wi);
@@ -676,12 +698,12 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
           if (++d0 == kc0) d0 = 0;
           if (!(dbg & 1)) {
 #pragma unroll
-            for (int kk = 0; kk < TC_BK / 8; ++kk) {  // K=8 per tf32 MMA: +32 B inside the 128-B row
+            for (int kk = 0; kk < TC_BK / 8; ++kk) {  // K=8 per tf32 MMA
               if (kk < nkk) {
                 if (PAIR)
-                  mma_tf32_pair(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (it > k0 || kk > 0) ? 1u : 0u);
+                  mma_tf32_pair(d_tmem, ad + astep * kk, bd + bstep * kk, idesc, (it > k0 || kk > 0) ? 1u : 0u);
                 else
-                  mma_tf32(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (it > k0 || kk > 0) ? 1u : 0u);
+                  mma_tf32(d_tmem, ad + astep * kk, bd + bstep * kk, idesc, (it > k0 || kk > 0) ? 1u : 0u);
               }
             }
           }
@@ -963,6 +985,7 @@ EncodeTiledFn encoder() {
   return fn;
 }
 
+// swizzle: a CUtensorMapSwizzle value (0 none, 3 128B, 4 128B with 32-B atoms)
 bool encode(CUtensorMap* map, const void* ptr, const uint64_t* gdim, const uint64_t* gstride, const uint32_t* box,
             int swizzle) {
   EncodeTiledFn fn = encoder();
@@ -981,7 +1004,7 @@ bool encode(CUtensorMap* map, const void* ptr, const uint64_t* gdim, const uint6
     last = s * dims[i];
   }
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void*>(ptr), dims, strides, boxes, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, static_cast<CUtensorMapSwizzle>(swizzle),
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

@@ -125,7 +125,10 @@ struct TcParams {
   int32_t mcast;           // 1: launched with cluster dims (2,1,1)
   int32_t mc_half;         // B rows loaded per CTA (multiple of 8)
   int32_t mc_ndim;         // TMA dim of B that carries the N tile
-  int32_t mn_lbo, mn_sbo;  // MN-major descriptor strides (bytes)
+  int32_t native_mn;       // MN-major operands read by the MMA directly (no smem transpose)
+  uint32_t mn_lbo16;       // MN-major smem descriptor: LBO >> 4 (next 32-MN box)
+  uint32_t mn_desc_hi;     //   bits 32..63: SBO >> 4, version 1, layout type
+  uint32_t mn_kstep16;     //   start-address advance per K=8 MMA, >> 4
   int32_t dbg;             // debug: bit0 skip MMAs, bit1 skip TMA loads (timing experiments only)
 };
 
@@ -139,7 +142,7 @@ struct TcPlan {
   uint64_t gdim_a[5]{}, gdim_b[5]{};
   uint64_t gstride_a[5]{}, gstride_b[5]{};  // bytes, [0] unused
   uint32_t box_a[5]{}, box_b[5]{};
-  int swz_a = 1, swz_b = 1;   // 1: SWIZZLE_128B tensor map, 0: none (wide MN-major boxes)
+  int swz_a = 3, swz_b = 3;   // CUtensorMapSwizzle: 3 128B (K-major), 4 128B_ATOM_32B (native MN-major), 0 none (wide)
   int64_t out_span = 0;       // elements of C to zero before a split-K launch
   const void* cached_a = nullptr;
   const void* cached_b = nullptr;

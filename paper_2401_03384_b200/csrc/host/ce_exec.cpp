@@ -670,7 +670,13 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       }
     }
     if (!ok && try_col2im()) return;
-    if (ok && st.tc.params.oa.mn_major && st.tc.params.ob.mn_major && st.tc.params.k_iters > 64) {
+    // CE_MN_REPACK: 1 (default) both long-K repack rules below, 2 only the double-MN-major one,
+    // 0 none (native MN-major operands are read by the MMA directly; A/B knob)
+    static const int mn_repack = [] {
+      const char* e = std::getenv("CE_MN_REPACK");
+      return e ? std::atoi(e) : 1;
+    }();
+    if (ok && mn_repack >= 1 && st.tc.params.oa.mn_major && st.tc.params.ob.mn_major && st.tc.params.k_iters > 64) {
       // Both operands would be transposed in shared memory every stage: over a long K
       // loop that is smem-bandwidth bound (measured 2.2x slower than the MMA).  Repack B
       // once with its largest shared K var innermost so only A is transposed in-kernel.
@@ -703,7 +709,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       return e ? std::atoi(e) : 0;
     }();
     if (ok && (st.tc.params.oa.mn_major || st.tc.params.ob.mn_major) &&
-        (st.tc.params.k_iters > 64 || repack_mn == 1)) {
+        ((st.tc.params.k_iters > 64 && mn_repack == 1) || repack_mn == 1)) {
       // One MN-major operand over a long K loop (factor gradients: K = every b,h,w): its
       // 4 KB [32 K][32 MN] boxes plus the in-smem transpose make the TMA producer, not the
       // MMA, the bottleneck (measured 1.4 us per stage against 0.39 us K-major).  A single

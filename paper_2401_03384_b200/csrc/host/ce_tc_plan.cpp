@@ -175,10 +175,10 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   auto uid = [&](int v) { return unit_of[static_cast<std::size_t>(v)]; };
   const int innerA = A.front().v0, innerB = B.front().v0;
   const int ia_cls = ucls(innerA), ib_cls = ucls(innerB);
-  // tcgen05 kind::tf32 with the MN-major (transpose) descriptor bits set returns zeros on
-  // sm_100a (measured: tests/tc_probe2.py).  MN-major operands are therefore loaded by
-  // TMA as [K rows][32 MN] boxes and transposed in shared memory to the K-major layout
-  // by the kernel's transposer warps; the MMA always sees K-major operands.
+  // MN-major operands (the tile unit innermost in memory) are TMA-loaded as [32 K rows][32 MN]
+  // SWIZZLE_128B boxes -- exactly the UMMA MN-major SW128 canonical layout -- and read by the
+  // MMA with the transpose bits of the instruction descriptor (native_mn, the default), or
+  // (CE_TC_NATIVE_MN=0) transposed to K-major in shared memory by the transposer warps.
   int a_mn = -1, b_mn = -1;
   std::vector<std::pair<int, int>> kblock;  // (unit, box)
   auto has_plain = [&](const std::vector<Axis>& ops, int u) {
@@ -483,9 +483,33 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     const char* e = std::getenv("CE_TC_WIDE");
     return !(e && *e == '0');
   }();
+  static const bool native_on = [] {
+    const char* e = std::getenv("CE_TC_NATIVE_MN");
+    return !(e && *e == '0');
+  }();
+  P.native_mn = native_on ? 1 : 0;
+  {
+    // MN-major tf32 smem layout (probe knobs while the layout is being pinned on hardware):
+    // CE_TC_MN_LAYOUT (UMMA layout type, default 1 = SWIZZLE_128B_BASE32B), CE_TC_MN_TMASWZ
+    // (CUtensorMapSwizzle of the MN-major boxes, default 4 = 128B_ATOM_32B), CE_TC_MN_SBO /
+    // CE_TC_MN_LBO (bytes), CE_TC_MN_KSTEP (bytes per K=8 step)
+    auto env = [](const char* k, int d) {
+      const char* e = std::getenv(k);
+      return e ? std::atoi(e) : d;
+    };
+    static const int layout = env("CE_TC_MN_LAYOUT", 1), tmaswz = env("CE_TC_MN_TMASWZ", 4),
+                     sbo = env("CE_TC_MN_SBO", 512), lbo = env("CE_TC_MN_LBO", 4096), kstep = env("CE_TC_MN_KSTEP", 1024);
+    P.mn_lbo16 = static_cast<uint32_t>(lbo >> 4);
+    P.mn_desc_hi = static_cast<uint32_t>(sbo >> 4) | (1u << 14) | (static_cast<uint32_t>(layout) << 29);
+    P.mn_kstep16 = static_cast<uint32_t>(kstep >> 4);
+    if (P.native_mn) {
+      if (a_mn == 1) plan->swz_a = tmaswz;
+      if (b_mn == 1) plan->swz_b = tmaswz;
+    }
+  }
   P.oa.wide = 0;
   P.ob.wide = 0;
-  if (wide_on && a_mn == 1 && P.oa.nsub >= 2 && P.oa.nsub <= 4) {
+  if (wide_on && !P.native_mn && a_mn == 1 && P.oa.nsub >= 2 && P.oa.nsub <= 4) {
     P.oa.wide = 1;
     P.oa.wbox = P.oa.nsub * 32;
     plan->box_a[0] = static_cast<uint32_t>(P.oa.wbox);
@@ -582,8 +606,12 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     const int cols_sec = sectors(offsets(P.nt, P.nn, std::min(32, P.n_cols)));
     P.transpose_store = cols_sec < rows_sec ? 1 : 0;
   }
-  // both operands reach the MMA K-major (MN-major ones after the in-smem transpose)
-  P.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(P.n_mma >> 3) << 17) |
+  // instruction descriptor: D f32, A/B tf32, A/B major (bits 15/16: 1 = MN-major, read
+  // natively), N >> 3, M >> 4
+  const uint32_t major_bits = P.native_mn ? (static_cast<uint32_t>(a_mn == 1) << 15) |
+                                                (static_cast<uint32_t>(b_mn == 1) << 16)
+                                          : 0u;
+  P.idesc = (1u << 4) | (2u << 7) | (2u << 10) | major_bits | (static_cast<uint32_t>(P.n_mma >> 3) << 17) |
             (static_cast<uint32_t>(TC_BM >> 4) << 24);
   // 2-CTA cluster with B multicast: K-major B whose N tile is one unit (TMA dim 1)
   static const bool mcast_enabled = [] {
@@ -612,7 +640,7 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
         P.mcast = 2;
         P.ob.stage_bytes = half * 128;
         P.n_mma = 2 * half;
-        P.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(P.n_mma >> 3) << 17) |
+        P.idesc = (1u << 4) | (2u << 7) | (2u << 10) | major_bits | (static_cast<uint32_t>(P.n_mma >> 3) << 17) |
                   (static_cast<uint32_t>((2 * TC_BM) >> 4) << 24);
       } else {
         P.mcast = 1;  // B halves multicast to both CTAs, M=128 MMAs per CTA

@@ -94,24 +94,39 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def _device_f32(ctx: Context, what: str, t: torch.Tensor) -> torch.Tensor:
+    """A contiguous float32 tensor on the context's device (a copy when `t` is strided).
+    The caller keeps the returned tensor alive until the library call that reads it returns
+    and orders ctx.torch_stream after the caller's stream (where a copy is produced)."""
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float32:
+        raise TypeError(f"{what} must be a float32 torch tensor")
+    if not t.is_cuda or (t.device.index or 0) != ctx.device:
+        raise TypeError(f"{what} must live on cuda:{ctx.device}")
+    return t.contiguous()
+
+
 def conv_einsum_forward(ctx: Context, expr: str, *tensors: torch.Tensor, mode: str = "same",
                         cost_mode: str = "inference") -> torch.Tensor:
     """ce_conv_einsum: plan + executor cached in the context by (expr, shapes, mode, cost_mode)."""
     from .api import Plan as _P
-    dims = [list(t.shape) for t in tensors]
+    # contiguous copies are made on the caller's stream and kept alive until the call returns
+    ts = [_device_f32(ctx, f"input {i}", t) for i, t in enumerate(tensors)]
+    dims = [list(t.shape) for t in ts]
     key = (expr, tuple(map(tuple, dims)), mode, cost_mode)
     shapes = ctx.__dict__.setdefault("_out_shapes", {})
     if key not in shapes:
         shapes[key] = _P.optimal(expr, dims, mode, cost_mode).out_dims
     ctx.torch_stream.wait_stream(torch.cuda.current_stream(ctx.device))
-    out = torch.empty(shapes[key], dtype=torch.float32, device=tensors[0].device)
+    out = torch.empty(shapes[key], dtype=torch.float32, device=ts[0].device)
     d, r, _ = _dims_arg(dims)
-    ptrs = (ctypes.c_void_p * len(tensors))(*[ctypes.c_void_p(t.contiguous().data_ptr()) for t in tensors])
-    check(lib().ce_conv_einsum(ctx.handle, expr.encode(), d, r, len(tensors), mode.encode(), cost_mode.encode(),
+    ptrs = (ctypes.c_void_p * len(ts))(*[ctypes.c_void_p(t.data_ptr()) for t in ts])
+    check(lib().ce_conv_einsum(ctx.handle, expr.encode(), d, r, len(ts), mode.encode(), cost_mode.encode(),
                                ctypes.cast(ptrs, _lib.c_fpp), ctypes.c_void_p(out.data_ptr())))
     cur = torch.cuda.current_stream(ctx.device)
     if cur.cuda_stream != ctx.torch_stream.cuda_stream:
         cur.wait_stream(ctx.torch_stream)
+        for t in ts:
+            t.record_stream(ctx.torch_stream)
     return out
 
 
@@ -217,6 +232,7 @@ class Executor:
 def pairwise_eval(ctx: Context, expr: str, a: torch.Tensor, b: torch.Tensor, mode: str = "same") -> torch.Tensor:
     """pairwise_eval (kernels.cpp:425-470) for expr "L,R->RES|convs" (keep = RES, order RES)."""
     from .api import Plan as _P  # result shape via a one-node plan
+    a, b = _device_f32(ctx, "a", a), _device_f32(ctx, "b", b)
     shape = _P.optimal(expr, [list(a.shape), list(b.shape)], mode).out_dims
     ctx.torch_stream.wait_stream(torch.cuda.current_stream(ctx.device))  # ce_pairwise_* syncs its own stream
     out = torch.empty(shape, dtype=torch.float32, device=a.device)
@@ -227,11 +243,17 @@ def pairwise_eval(ctx: Context, expr: str, a: torch.Tensor, b: torch.Tensor, mod
 
 
 def pairwise_grad(ctx: Context, expr: str, a, b, dout, mode: str = "same"):
+    """Adjoints (dA, dB) of <dout, pairwise_eval(a, b)> (ce_pairwise_grad)."""
+    from .api import Plan as _P
+    a, b, dout = _device_f32(ctx, "a", a), _device_f32(ctx, "b", b), _device_f32(ctx, "dout", dout)
+    shape = _P.optimal(expr, [list(a.shape), list(b.shape)], mode).out_dims
+    if list(dout.shape) != list(shape):
+        raise _lib.ShapeError(3, f"pairwise_grad: dout shape {list(dout.shape)} != result shape {list(shape)}")
     ctx.torch_stream.wait_stream(torch.cuda.current_stream(ctx.device))
     da, db = torch.empty_like(a), torch.empty_like(b)
     d, r, _ = _dims_arg([list(a.shape), list(b.shape)])
     check(lib().ce_pairwise_grad(ctx.handle, expr.encode(), d, r, mode.encode(), ctypes.c_void_p(a.data_ptr()),
-                                 ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(dout.contiguous().data_ptr()),
+                                 ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(dout.data_ptr()),
                                  ctypes.c_void_p(da.data_ptr()), ctypes.c_void_p(db.data_ptr())))
     return da, db
 
