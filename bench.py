@@ -9,16 +9,23 @@ cost mode).  `value` = algorithmic TFLOP/s over all GPUs = sum over nodes of
 device time of the step (CUDA events on the executor stream, max over ranks).
 L2 is flushed (256 MiB write) between timed steps, outside the events.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--no-cfg3]
 
-Multi-GPU: one process per GPU (torchrun), batch sharded (128 per GPU, weak
+Multi-GPU: one process per GPU (torchrun; `--gpus N` without RANK in the environment
+re-launches itself under torch.distributed.run), batch sharded (128 per GPU, weak
 scaling), factors replicated, factor gradients all-reduced with NCCL.
+
+`--impl reference` times the reference's own CPU executor (the unmodified convexpr
+sources compiled by oracle/Makefile into oracle/_ref, FP64, OpenMP on every host core)
+on a bounded batch sample of the same four layers; everything it reports (expression,
+ranks, plan, executed multiplications) comes from that library, not from libce.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -29,8 +36,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 LAYERS = [("tk", 0.1), ("tk", 1.0), ("tt", 0.1), ("tt", 1.0)]
+SLOTS = {"tk": 2, "tt": 3}
 METRIC = "TFLOP/s & layer fwd+bwd latency, tensorized ResNet-34 convs, 1/2/4/8 B200 vs CPU"
 PER_GPU_BATCH = 128
+CPU_SAMPLE_BATCH = 4
+WORKLOAD = "cfg2: Tucker + TT 3x3 conv layers, 256->256 ch, 14x14, fwd+bwd (all grads)"
 
 
 def load_peaks():
@@ -44,8 +54,7 @@ def load_peaks():
 
 def layer_expr(kind, cr, batch):
     import paper_2401_03384_b200 as ce
-    slots = {"tk": 2, "tt": 3}[kind]
-    return ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, batch, [1] * slots), cr)
+    return ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, batch, [1] * SLOTS[kind]), cr)
 
 
 class ClockSampler:
@@ -94,66 +103,158 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU / reference
-def cpu_reference_time(batch_cpu=2, reps=2):
-    """Reference execute() (FP64, OpenMP, all host cores) on a batch subset of each layer.
-
-    Returns (seconds for the subset forward of all layers, FLOPs of that subset, kind, cores)."""
+def cpu_reference_sample(batch_cpu=CPU_SAMPLE_BATCH, reps=1):
+    """The reference's execute() (oracle/_ref: unmodified convexpr, FP64, OpenMP on all host
+    cores) on a batch-`batch_cpu` sample of each layer.  Expression, ranks, plan
+    (optimal, training cost mode, as the GPU arm) and the executed multiplications all come
+    from the reference library.  Returns (seconds, FLOPs = 2 * multiplications, kind, cores, note)."""
     import numpy as np
     from oracle import ref
     cores = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     total_s, total_flops = 0.0, 0.0
-    kind = "reference"
+    if ref.available():
+        for k, cr in LAYERS:
+            lj = json.dumps({"kind": k, "T": [256], "S": [256], "H": 3, "W": 3, "Hp": 14, "Wp": 14, "B": batch_cpu,
+                             "rank": [1] * SLOTS[k]})
+            expr, dims, _, _ = ref.layer(lj, cr)
+            ins = [np.asarray(np.float32(ref.fill_random(d, 1000 + i)), dtype=np.float64) for i, d in enumerate(dims)]
+            s, mults = ref.time_execute_mults(expr, dims, ins, "same", "training", reps=reps)
+            total_s += s
+            total_flops += 2.0 * mults
+        return total_s, total_flops, "reference", cores, "oracle/_ref (unmodified convexpr sources)"
+    # the reference could not be compiled on this host: the numpy port of it (oracle/np_oracle.py)
+    from oracle import np_oracle as npo
+    import paper_2401_03384_b200 as ce  # planner only (bit-exact with the reference's, tests/test_planner.py)
     for k, cr in LAYERS:
         le = layer_expr(k, cr, batch_cpu)
-        import paper_2401_03384_b200 as ce
         p = ce.optimal(le.expr, le.dims, "same", "training")
-        ins = [np.asarray(np.float32(ref.fill_random(d, 1000 + i) if ref.available() else 0), dtype=np.float64)
-               for i, d in enumerate(le.dims)]
-        if ref.available():
-            s = ref.time_execute(le.expr, le.dims, ins, "same", "training", reps=reps)
-        else:  # numpy port of the reference (oracle/np_oracle.py)
-            from oracle import np_oracle as npo
-            kind = "port"
-            nodes = [(n["left"], n["right"], n["result"]) for n in json.loads(p.to_json())["nodes"]]
-            ins = [npo.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
-            t0 = time.perf_counter()
-            npo.execute(le.expr, le.dims, nodes, ins)
-            s = time.perf_counter() - t0
-            cores = 1
-        total_s += s
+        nodes = [(n["left"], n["right"], n["result"]) for n in json.loads(p.to_json())["nodes"]]
+        ins = [npo.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
+        t0 = time.perf_counter()
+        npo.execute(le.expr, le.dims, nodes, ins)
+        total_s += time.perf_counter() - t0
         total_flops += 2.0 * p.flops_actual
-    return total_s, total_flops, kind, cores
+    return total_s, total_flops, "port", 1, "oracle/np_oracle.py (numpy port; reference not built)"
 
 
 def run_reference_arm(args, rank, world):
     """--impl reference: the reference's own CPU executor (forward only: it has no backward)."""
     if rank != 0:
         return
-    batch_cpu = 2
-    secs = []
-    flops = None
     for _ in range(args.warmup):
-        cpu_reference_time(batch_cpu, reps=1)
+        cpu_reference_sample(reps=1)
+    secs, flops, kind, cores, src = [], None, "reference", 1, ""
     for _ in range(args.steps):
-        s, flops, kind, cores = cpu_reference_time(batch_cpu, reps=1)
+        s, flops, kind, cores, src = cpu_reference_sample(reps=1)
         secs.append(s)
     t = statistics.median(secs)
-    # scale the bounded sample to the GPU arm's workload: forward FLOPs are exactly linear in B
     value = flops / t / 1e12
+    gpu_batch = PER_GPU_BATCH * world
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3 * (PER_GPU_BATCH * world / batch_cpu),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg2 TK+TT 3x3 conv layers cr{0.1,1.0}, 256->256, 14x14",
-                   "global_batch": PER_GPU_BATCH * world, "sample_batch": batch_cpu,
-                   "note": "reference has no backward: forward only, FLOPs-normalised"},
+        "config": {"workload": WORKLOAD, "global_batch": gpu_batch, "sample_batch": CPU_SAMPLE_BATCH,
+                   "note": "the reference has no backward: its forward of the same four layers (same training-mode "
+                           "plans), on a batch-%d sample; value = 2 * executed multiplications / time" % CPU_SAMPLE_BATCH},
+        "projected_ms_at_global_batch": round(t * 1e3 * gpu_batch / CPU_SAMPLE_BATCH, 1),
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
-                         "sample": f"reference execute() forward of the 4 layers at batch {batch_cpu} (of 128), "
-                                   f"OMP_NUM_THREADS={cores}"},
+                         "sample": f"reference execute() forward of the 4 cfg2 layers at batch {CPU_SAMPLE_BATCH} "
+                                   f"(median of {args.steps}), OMP_NUM_THREADS={cores}; {src}"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- self-launch for N > 1
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn(args):
+    """`python bench.py --gpus N` outside torchrun: re-run this script under
+    torch.distributed.run with N local ranks (rank 0 prints the JSON line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+# ----------------------------------------------------------------------------- measured TF32 peak
+def measure_tf32_peak(dev):
+    """Dense TF32 tensor-core peak of THIS box, for the roofline denominator only: FP32 matmul
+    8192^3 with TF32 allowed (cuBLAS), best of 10, CUDA events.  Never part of the product path."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=dev)
+        b = torch.randn(n, n, device=dev)
+        for _ in range(3):
+            torch.matmul(a, b)
+        best = 1e30
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+# ----------------------------------------------------------------------------- cfg3 stack
+RTR_FACT = {3: [1, 1, 3], 64: [4, 4, 4], 128: [4, 4, 8], 256: [4, 8, 8], 512: [8, 8, 8]}
+RESNET34 = [(3, 64, 7, 112, 1), (64, 64, 3, 56, 6), (64, 128, 3, 28, 1), (128, 128, 3, 28, 7),
+            (128, 256, 3, 14, 1), (256, 256, 3, 14, 11), (256, 512, 3, 7, 1), (512, 512, 3, 7, 5)]
+
+
+def time_cfg3_stack(ctx, flush, iters=2):
+    """cfg3: tensor-ring reshaped (M=3) ResNet-34 conv stack, batch 256, cr 0.1, fwd+bwd.
+    Each distinct layer shape (stride-2 layers run stride-1 at output resolution) is timed
+    (median of `iters` after a warm-up, L2 flushed) and weighted by its count in the 33 convs."""
+    import torch
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import Executor
+    tot_ms, tot_fl, per = 0.0, 0.0, {}
+    for s, t, k, hp, count in RESNET34:
+        le = ce.expression(ce.LayerSpec("rtr", RTR_FACT[t], RTR_FACT[s], k, k, hp, hp, 256, [1, 1, 1, 1]), 0.1)
+        plan = ce.optimal(le.expr, le.dims, "same", "training")
+        ex = Executor(ctx, plan, backward=True)
+        xs = [ctx.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
+        dout = ctx.fill_random(plan.out_dims, 2000)
+        out = torch.empty(plan.out_dims, device=dout.device)
+        ex.execute(xs, out)
+        ex.backward(xs, dout)
+        ts = []
+        for _ in range(iters):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ctx.torch_stream)
+            ex.execute(xs, out)
+            ex.backward(xs, dout)
+            e1.record(ctx.torch_stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        fl = 6.0 * plan.flops_actual
+        per[f"{s}->{t}@{hp}x{count}"] = round(ms, 3)
+        tot_ms += count * ms
+        tot_fl += count * fl
+        del ex, xs, dout, out
+        torch.cuda.empty_cache()
+    return {"workload": "cfg3 RTR (M=3) ResNet-34 conv stack, batch 256, cr 0.1, fwd+bwd, 33 convs",
+            "stack_fwd_bwd_ms": round(tot_ms, 2), "tflops": round(tot_fl / (tot_ms * 1e-3) / 1e12, 2),
+            "per_layer_ms": per}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -164,8 +265,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cfg3", action="store_true", help="skip the cfg3 stack extra key")
     ap.add_argument("--profile-json", default=None, help="write per-kernel times here")
     args = ap.parse_args()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(spawn(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -207,9 +311,10 @@ def main():
         layers.append(dict(kind=kind, cr=cr, le=le, plan=plan, ex=ex, xs=xs, dout=dout,
                            flops=3.0 * fwd_flops, out=torch.empty(plan.out_dims, device=dev)))
     step_flops = sum(l["flops"] for l in layers)
+    layer_desc = [f"{l['kind']} cr={l['cr']} R={l['le'].ranks[0]} tree={l['plan'].tree_encoding()}" for l in layers]
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
-    def one_step(collect=None):
+    def one_step():
         launches = 0
         works = []
         for l in layers:
@@ -247,24 +352,28 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
     ms = statistics.mean(times)
+    ms_median = statistics.median(times)
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * step_flops / (ms * 1e-3) / 1e12
 
-    # per-layer fwd+bwd latency (device, one more pass, events per layer)
+    # per-layer fwd+bwd latency (device, median of 5 passes, events per layer)
     lat = {}
     for l in layers:
-        flush.fill_(1.0)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        l["ex"].execute(l["xs"], l["out"])
-        l["ex"].backward(l["xs"], l["dout"])
-        e1.record(stream)
-        torch.cuda.synchronize()
-        lat[f"{l['kind']}_cr{l['cr']}_R{l['le'].ranks[0]}"] = round(e0.elapsed_time(e1), 4)
+        ts = []
+        for _ in range(5):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            l["ex"].execute(l["xs"], l["out"])
+            l["ex"].backward(l["xs"], l["dout"])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        lat[f"{l['kind']}_cr{l['cr']}_R{l['le'].ranks[0]}"] = round(statistics.median(ts), 4)
 
     # ---------------------------------------------------------------- e2e through the public API, host buffers
     pinned = []
@@ -339,7 +448,7 @@ def main():
 
     # ---------------------------------------------------------------- live per-kernel roofline
     hbm, bf16, peak_kind = load_peaks()
-    tf32_peak = bf16 / 2.0
+    tf32_peak = measure_tf32_peak(dev)
     kern = []
     for l in layers:
         l["ex"].set_profiling(True)
@@ -357,9 +466,9 @@ def main():
     top = max(kern, key=lambda k: k[2])
     name, kind, t_ms, fl, by = top
     # DRAM traffic per launch of that kernel from the committed `ncu --set full` captures
-    traffic = None
+    traffic, traffic_src = None, "profiles/ncu_traffic_r02.json"
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")) as f:
+        with open(os.path.join(ROOT, traffic_src)) as f:
             tj = json.load(f)
         if name in tj.get("kernels", {}):
             traffic = tj["kernels"][name]["dram_bytes_per_launch"]
@@ -367,38 +476,54 @@ def main():
         traffic = None
     if kind == "tc":
         ach = fl / (t_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": tf32_peak, "unit": "TFLOP/s",
-                "frac": round(ach / tf32_peak, 4), "traffic": traffic,
+        roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
+                "frac": round(ach / tf32_peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": name, "share_of_step": round(t_ms / total_k, 3),
-                "peak_note": f"TF32 dense = bf16_tflops/2 of {peak_kind} ({bf16} TF)",
+                "peak_note": "dense TF32 measured on this box (FP32 8192^3 matmul, TF32 allowed, best of 10); "
+                             f"bf16 {peak_kind} {bf16} TF/s",
                 "hbm_frac": round(by / (t_ms * 1e-3) / 1e9 / hbm, 4)}
     else:
         ach = by / (t_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(ach / hbm, 4), "traffic": traffic, "kernel": name,
+                "frac": round(ach / hbm, 4), "traffic": traffic, "traffic_source": traffic_src, "kernel": name,
                 "share_of_step": round(t_ms / total_k, 3), "peak_note": f"{peak_kind} copy bandwidth"}
+    # step-level attainable bound: sum over the algorithmic steps (packs excluded: they carry no
+    # algorithmic work) of max(FLOPs / TF32 peak, compulsory bytes / HBM peak)
+    t_att = sum(max(fl_ / (tf32_peak * 1e12), by_ / (hbm * 1e9)) for (_, k_, _, fl_, by_) in kern if k_ != "permute")
+    roof["step_attainable_ms"] = round(t_att * 1e3, 4)
+    roof["step_attainable_frac"] = round(t_att * 1e3 / ms, 4)
+    roof["kernel_time_share"] = {k_: round(sum(t for (_, kk, t, _, _) in kern if kk == k_) / total_k, 3)
+                                 for k_ in sorted({k[1] for k in kern})}
     if args.profile_json and rank == 0:
         with open(args.profile_json, "w") as f:
             json.dump([dict(name=n, kind=k, ms=t, flops=fl, bytes=by,
                             tflops=fl / (t * 1e-3) / 1e12 if t > 0 else 0, gbs=by / (t * 1e-3) / 1e9 if t > 0 else 0)
                        for (n, k, t, fl, by) in kern], f, indent=1)
 
+    # ---------------------------------------------------------------- cfg3 stack (largest single-GPU config)
+    cfg3 = None
+    if rank == 0 and world == 1 and not args.no_cfg3:
+        for l in layers:
+            l.clear()
+        torch.cuda.empty_cache()
+        cfg3 = time_cfg3_stack(ctx, flush)
+
     # ---------------------------------------------------------------- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        s, fl_cpu, kindc, cores = cpu_reference_time(2, reps=2)
+        s, fl_cpu, kindc, cores, src = cpu_reference_sample(CPU_SAMPLE_BATCH, reps=2)
         cpu = {"value": fl_cpu / s / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kindc,
-               "sample": "reference execute() FORWARD (no backward exists) of the 4 layers at batch 2 of 128, "
-                         "FP64, best of 2; FLOPs-normalised"}
+               "sample": f"reference execute() FORWARD (no backward exists) of the 4 layers at batch "
+                         f"{CPU_SAMPLE_BATCH} of 128, FP64, best of 2, {s * 1e3:.0f} ms; {src}"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "ms_per_step_median": round(ms_median, 4),
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "tf32", "data": "synthetic (SplitMix64 fill_random, reference seeds)",
-            "config": {"workload": "cfg2: Tucker + TT 3x3 conv layers, 256->256 ch, 14x14, fwd+bwd (all grads)",
-                       "layers": [f"{l['kind']} cr={l['cr']} R={l['le'].ranks[0]} tree={l['plan'].tree_encoding()}"
-                                  for l in layers],
+            "config": {"workload": WORKLOAD,
+                       "layers": layer_desc,
                        "global_batch": PER_GPU_BATCH * world, "per_gpu_batch": PER_GPU_BATCH,
                        "parallelism": f"batch-sharded x{world}, factor-grad NCCL all-reduce" if world > 1 else "1 GPU",
                        "l2": "flushed (256 MiB write) between timed steps",
@@ -411,6 +536,7 @@ def main():
             "gpu_launches": launches,
             "roofline": roof,
             "cpu_baseline": cpu,
+            "cfg3_stack": cfg3,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

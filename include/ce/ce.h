@@ -58,7 +58,10 @@ typedef struct ce_plan ce_plan;
 typedef enum { CE_PLAN_OPTIMAL = 0, CE_PLAN_LEFT_TO_RIGHT = 1, CE_PLAN_OPTIMAL_CAPPED = 2 } ce_plan_strategy;
 
 /* dims: all input dims concatenated; ranks[i]: number of axes of input i.
- * mode: "full" | "same" | "valid" | "circular" (resolve_conv_modes, kernels.cpp:38-43).
+ * mode: "full" | "same" | "valid" | "circular" applied through resolve_conv_modes
+ * (kernels.cpp:38-43: atoms shared by >= 3 inputs become circular), or an explicit per-atom
+ * ConvModeMap (kernels.hpp:27-32) "h=same,w=circular,(r1)=full" naming every conv atom
+ * (accepted by every entry point below that takes a mode).
  * cost_mode: "inference" | "training" (cost.hpp:8).
  * Replaces: optimal()/left_to_right() (sequencer.hpp:44-63). */
 ce_status ce_plan_create(const char* expr, const int64_t* dims, const int* ranks, int n_inputs, const char* mode,
@@ -67,6 +70,14 @@ ce_status ce_plan_create(const char* expr, const int64_t* dims, const int* ranks
 ce_status ce_plan_from_joins(const char* expr, const int64_t* dims, const int* ranks, int n_inputs,
                              const char* mode, const char* cost_mode, const int* joins, int n_joins,
                              ce_plan** out);
+/* Replays a caller's EvaluationPlan (sequencer.hpp:30-41) exactly: node j joins operand ids
+ * joins[2j], joins[2j+1] (inputs 0..N-1, node k is N+k) and keeps exactly the atoms of
+ * results[j] in that order ("bhw(r2)", the plan_to_json "result" field), with the per-atom
+ * modes of `mode`.  This is what the reference's execute(plan, inputs) runs; the optimal /
+ * left_to_right / from_joins entry points re-derive the result orders instead. */
+ce_status ce_plan_from_nodes(const char* expr, const int64_t* dims, const int* ranks, int n_inputs,
+                             const char* mode, const char* cost_mode, const int* joins,
+                             const char* const* results, int n_nodes, ce_plan** out);
 void ce_plan_destroy(ce_plan* plan);
 /* plan_to_json (sequencer.cpp:466-480), byte-identical to the reference. */
 ce_status ce_plan_json(const ce_plan* plan, char* buf, size_t cap);
@@ -93,9 +104,13 @@ ce_status ce_plan_node(const ce_plan* plan, int node, int* left, int* right, cha
 ce_status ce_plan_describe_steps(const ce_plan* plan, int want_backward, int math, char* buf, size_t cap);
 
 /* ----------------------------------------------------------------- layers -- */
+#define CE_MAX_LAYER_INPUTS 32 /* capacity of ranks_of_input[] (entries) */
+#define CE_MAX_LAYER_RANKS 32  /* capacity of ranks_out[] (entries) */
 /* expression() (layers.hpp:71): kind name as in layer_kind_from_string (layers.cpp:29-45).
  * With cr > 0 the ranks are solved by rank_for_compression (layers.cpp:341-366) and
- * written to ranks_out.  dims_out/ranks_of_input receive the per-input shapes. */
+ * written to ranks_out.  dims_out/ranks_of_input receive the per-input shapes.
+ * ranks_of_input must hold CE_MAX_LAYER_INPUTS entries and ranks_out CE_MAX_LAYER_RANKS;
+ * a layer needing more fails with CE_ERR_SHAPE before anything is written to them. */
 ce_status ce_layer_expression(const char* kind, const int64_t* t_factors, int n_t, const int64_t* s_factors,
                               int n_s, int64_t filter_h, int64_t filter_w, int64_t feature_h, int64_t feature_w,
                               int64_t batch, const int64_t* ranks, int n_ranks, double cr, char* expr_out,
@@ -193,6 +208,10 @@ ce_status ce_ctx_init_comm(ce_ctx* ctx, int nranks, int rank, const void* id128)
  * orders the ctx stream after every collective issued so far. */
 ce_status ce_allreduce_grads(ce_ctx* ctx, float* const* bufs, const int64_t* counts, int n);
 ce_status ce_comm_wait(ce_ctx* ctx);
+/* Non-blocking communicator health poll (ncclCommGetAsyncError; also done by
+ * ce_allreduce_grads and ce_comm_wait): CE_ERR_NCCL after an asynchronous failure, in which
+ * case the communicator has been aborted and the context no longer has one. */
+ce_status ce_comm_check(ce_ctx* ctx);
 
 #ifdef __cplusplus
 }

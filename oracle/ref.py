@@ -102,6 +102,18 @@ def time_execute(expr, dims, inputs, mode="same", cost_mode="inference", reps=3)
     return best.value
 
 
+def time_execute_mults(expr, dims, inputs, mode="same", cost_mode="inference", reps=1):
+    """(best seconds, ExecutionResult.multiplications) of the reference execute()."""
+    d, r, n = _dims(dims)
+    keep, ptrs = _inputs(inputs)
+    best = ctypes.c_double()
+    out = _buf(128)
+    _check(lib().ref_time_execute2(expr.encode(), d, r, n, mode.encode(), cost_mode.encode(), ptrs,
+                                   int(reps), ctypes.byref(best), out, len(out)))
+    del keep
+    return best.value, int(out.value.decode())
+
+
 def eval_brute(expr, dims, inputs, out_shape, mode="same"):
     d, r, n = _dims(dims)
     keep, ptrs = _inputs(inputs)

@@ -184,6 +184,29 @@ int ref_time_execute(const char* expr, const int64_t* dims, const int* ranks, in
   });
 }
 
+// As ref_time_execute, and also returns ExecutionResult.multiplications (the sum of
+// flops_actual over the executed nodes, sequencer.cpp:429) as a decimal string in `mults`.
+int ref_time_execute2(const char* expr, const int64_t* dims, const int* ranks, int n, const char* mode,
+                      const char* cost_mode, const double* const* inputs, int reps, double* best_seconds,
+                      char* mults, int cap) {
+  return guard([&] {
+    Problem p = make_problem(expr, dims, ranks, n, mode);
+    EvaluationPlan plan = optimal(p.spec, p.env, p.modes, cost_mode_from_string(cost_mode));
+    auto ts = wrap_inputs(p, inputs);
+    double best = 1e30;
+    u128 m = 0;
+    for (int i = 0; i < reps; ++i) {
+      auto t0 = std::chrono::steady_clock::now();
+      ExecutionResult r = execute(plan, ts);
+      double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (s < best) best = s;
+      m = r.multiplications;
+    }
+    *best_seconds = best;
+    put(u128s(m), mults, cap);
+  });
+}
+
 // reference::eval (reference.cpp:76-222): brute-force nested sum.
 int ref_eval_brute(const char* expr, const int64_t* dims, const int* ranks, int n,
                    const char* mode, const double* const* inputs, double* out, int64_t out_cap) {

@@ -7,12 +7,12 @@ is missing — there is no CPU fallback.
 """
 from . import _lib
 from .api import (CeError, LayerExpression, LayerSpec, ParseError, Plan, PlanError, ShapeError,  # noqa: F401
-                  classify, expression, flops_actual, left_to_right, optimal, parse, plan_from_joins, plan_to_json,
+                  classify, expression, flops_actual, left_to_right, optimal, parse, plan_from_joins, plan_from_nodes, plan_to_json,
                   rank_for_compression, render, resnet34_cp_blocks, tree_encoding)
 
 _lib.lib()  # load now: no silent fallback
 
-__all__ = ["parse", "render", "classify", "optimal", "left_to_right", "plan_from_joins", "plan_to_json",
+__all__ = ["parse", "render", "classify", "optimal", "left_to_right", "plan_from_joins", "plan_from_nodes", "plan_to_json",
            "tree_encoding", "Plan", "LayerSpec", "LayerExpression", "expression", "rank_for_compression",
            "resnet34_cp_blocks", "flops_actual", "ParseError", "ShapeError", "PlanError", "CeError"]
 

@@ -51,6 +51,9 @@ SIGNATURES = {
                                       ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "ce_plan_from_joins": (ctypes.c_int, [ctypes.c_char_p, c_i64p, c_intp, ctypes.c_int, ctypes.c_char_p,
                                           ctypes.c_char_p, c_intp, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "ce_plan_from_nodes": (ctypes.c_int, [ctypes.c_char_p, c_i64p, c_intp, ctypes.c_int, ctypes.c_char_p,
+                                          ctypes.c_char_p, c_intp, ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_void_p)]),
     "ce_plan_destroy": (None, [ctypes.c_void_p]),
     "ce_plan_json": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
     "ce_plan_tree_encoding": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
@@ -91,6 +94,7 @@ SIGNATURES = {
     "ce_ctx_init_comm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     "ce_allreduce_grads": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), c_i64p, ctypes.c_int]),
     "ce_comm_wait": (ctypes.c_int, [ctypes.c_void_p]),
+    "ce_comm_check": (ctypes.c_int, [ctypes.c_void_p]),
 }
 
 STATUS = {0: "OK", 1: "OTHER", 2: "PARSE", 3: "SHAPE", 4: "NUMERIC", 5: "PLAN", 6: "OVERFLOW",

@@ -110,6 +110,19 @@ class Plan:
                                        ctypes.byref(h)))
         return Plan(h, expr, dims, mode, cost_mode)
 
+    @classmethod
+    def from_nodes(cls, expr, dims, nodes, mode="same", cost_mode="inference"):
+        """Replay a caller's plan: nodes = [(left id, right id, result subscripts)] (plan_to_json's
+        node fields); mode may be a per-atom map "h=same,w=circular"."""
+        d, r, n = _dims_arg(dims)
+        flat = [int(x) for (l, rr, _) in nodes for x in (l, rr)]
+        arr = (ctypes.c_int * max(1, len(flat)))(*flat)
+        res = (ctypes.c_char_p * max(1, len(nodes)))(*[str(x[2]).encode() for x in nodes])
+        h = ctypes.c_void_p()
+        check(lib().ce_plan_from_nodes(expr.encode(), d, r, n, mode.encode(), cost_mode.encode(), arr, res,
+                                       len(nodes), ctypes.byref(h)))
+        return Plan(h, expr, dims, mode, cost_mode)
+
     def to_json(self) -> str:
         buf = ctypes.create_string_buffer(1 << 20)
         check(lib().ce_plan_json(self._h, buf, len(buf)))
@@ -154,6 +167,10 @@ def left_to_right(expr, dims, mode="same", cost_mode="inference") -> Plan:
 
 def plan_from_joins(expr, dims, joins, mode="same", cost_mode="inference") -> Plan:
     return Plan.from_joins(expr, dims, joins, mode, cost_mode)
+
+
+def plan_from_nodes(expr, dims, nodes, mode="same", cost_mode="inference") -> Plan:
+    return Plan.from_nodes(expr, dims, nodes, mode, cost_mode)
 
 
 def plan_to_json(plan: Plan) -> str:

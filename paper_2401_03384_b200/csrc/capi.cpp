@@ -105,13 +105,46 @@ void split_u128(u128 v, uint64_t* lo, uint64_t* hi) {
   if (hi) *hi = static_cast<uint64_t>(v >> 64);
 }
 
+// The conv-mode argument of every plan-building entry point: either one mode name, applied
+// through resolve_conv_modes (kernels.cpp:38-43: atoms shared by >= 3 inputs become Circular),
+// or an explicit per-atom ConvModeMap (kernels.hpp:27-32) as "h=same,w=circular,(r1)=full"
+// that must name every convolution atom of the expression (and nothing else).
+ConvModeMap modes_arg(const ExpressionSpec& spec, const char* mode) {
+  const std::string m(mode ? mode : "");
+  if (m.find('=') == std::string::npos) return resolve_conv_modes(spec, conv_mode_from_string(m));
+  ConvModeMap out;
+  std::size_t pos = 0;
+  while (pos <= m.size()) {
+    const std::size_t end = std::min(m.find(',', pos), m.size());
+    const std::string item = m.substr(pos, end - pos);
+    const std::size_t eq = item.find('=');
+    if (eq == std::string::npos) throw ShapeError("mode map entry without '=': '" + item + "'");
+    std::string name = item.substr(0, eq);
+    if (name.size() >= 2 && name.front() == '(' && name.back() == ')') name = name.substr(1, name.size() - 2);
+    const Atom a(name);
+    if (!spec.is_conv(a)) throw ShapeError("mode map names '" + name + "', which is not a convolution atom");
+    if (out.count(a)) throw ShapeError("mode map names '" + name + "' twice");
+    out[a] = conv_mode_from_string(item.substr(eq + 1));
+    pos = end + 1;
+  }
+  for (const auto& a : spec.conv_atoms)
+    if (!out.count(a)) throw ShapeError("mode map has no mode for convolution atom '" + a.name + "'");
+  return out;
+}
+
+// Subscripts of a result string such as "bhw(r2)" (the tokens of the reference's parser).
+Subscripts parse_subscripts(const std::string& s) {
+  ExpressionSpec one = parse(s + "->" + s);
+  return one.output;
+}
+
 // A one-node plan for pairwise_eval with the planner's node construction.
 EvaluationPlan pairwise_plan(const char* expr, const int64_t* dims, const int* ranks, const char* mode) {
   EvaluationPlan plan;
   plan.spec = parse(expr);
   if (plan.spec.inputs.size() != 2) throw ShapeError("pairwise expression must have exactly two inputs");
   plan.env = make_shape_env(plan.spec, split_dims(dims, ranks, 2));
-  plan.modes = resolve_conv_modes(plan.spec, conv_mode_from_string(mode));
+  plan.modes = modes_arg(plan.spec, mode);
   std::set<Atom> keep(plan.spec.output.begin(), plan.spec.output.end());
   PlanNode node;
   node.left = 0;
@@ -137,6 +170,8 @@ struct NcclApi {
   ncclResult_t (*group_start)() = nullptr;
   ncclResult_t (*group_end)() = nullptr;
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*comm_abort)(ncclComm_t) = nullptr;
+  ncclResult_t (*get_async_error)(ncclComm_t, ncclResult_t*) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
 };
 
@@ -158,6 +193,8 @@ const NcclApi& nccl() {
     api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
     api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
     api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+    api.comm_abort = reinterpret_cast<decltype(api.comm_abort)>(dlsym(h, "ncclCommAbort"));
+    api.get_async_error = reinterpret_cast<decltype(api.get_async_error)>(dlsym(h, "ncclCommGetAsyncError"));
   });
   if (!api.all_reduce || !api.comm_init_rank || !api.get_unique_id || !api.group_start || !api.group_end)
     throw NcclError("NCCL unavailable: " + (why.empty() ? std::string("missing symbols") : why));
@@ -168,6 +205,21 @@ void nccl_ok(ncclResult_t r, const char* what) {
   if (r != ncclSuccess)
     throw NcclError(std::string("NCCL error in ") + what + ": " +
                     (nccl().error_string ? nccl().error_string(r) : std::to_string(static_cast<int>(r))));
+}
+
+// Non-blocking health check of a communicator (ncclCommGetAsyncError): a peer that died or a
+// network failure surfaces here instead of as a hang in a later collective.  On an error the
+// communicator is aborted (its pending work is cancelled) and CE_ERR_NCCL is raised.
+void comm_health(ce_ctx* ctx) {
+  if (!ctx->comm || !nccl().get_async_error) return;
+  ncclResult_t async = ncclSuccess;
+  nccl_ok(nccl().get_async_error(ctx->comm, &async), "ncclCommGetAsyncError");
+  if (async != ncclSuccess && async != ncclInProgress) {
+    const std::string why = nccl().error_string ? nccl().error_string(async) : std::to_string(static_cast<int>(async));
+    if (nccl().comm_abort) nccl().comm_abort(ctx->comm);
+    ctx->comm = nullptr;
+    throw NcclError("NCCL communicator failed asynchronously: " + why);
+  }
 }
 
 void fill_stats(const Executor& ex, ce_exec_stats* st, bool bwd) {
@@ -202,7 +254,7 @@ ce_status ce_plan_create(const char* expr, const int64_t* dims, const int* ranks
   return guard([&] {
     ExpressionSpec spec = parse(expr);
     ShapeEnv env = make_shape_env(spec, split_dims(dims, ranks, n_inputs));
-    ConvModeMap modes = resolve_conv_modes(spec, conv_mode_from_string(mode));
+    ConvModeMap modes = modes_arg(spec, mode);
     CostMode cm = cost_mode_from_string(cost_mode);
     auto p = std::make_unique<ce_plan>();
     if (strategy == CE_PLAN_LEFT_TO_RIGHT) {
@@ -224,8 +276,25 @@ ce_status ce_plan_from_joins(const char* expr, const int64_t* dims, const int* r
     std::vector<std::pair<int, int>> j;
     for (int i = 0; i < n_joins; ++i) j.push_back({joins[2 * i], joins[2 * i + 1]});
     auto p = std::make_unique<ce_plan>();
-    p->plan = plan_from_joins(spec, env, resolve_conv_modes(spec, conv_mode_from_string(mode)),
-                              cost_mode_from_string(cost_mode), j);
+    p->plan = plan_from_joins(spec, env, modes_arg(spec, mode), cost_mode_from_string(cost_mode), j);
+    *out = p.release();
+  });
+}
+
+ce_status ce_plan_from_nodes(const char* expr, const int64_t* dims, const int* ranks, int n_inputs, const char* mode,
+                             const char* cost_mode, const int* joins, const char* const* results, int n_nodes,
+                             ce_plan** out) {
+  return guard([&] {
+    ExpressionSpec spec = parse(expr);
+    ShapeEnv env = make_shape_env(spec, split_dims(dims, ranks, n_inputs));
+    std::vector<std::pair<int, int>> j;
+    std::vector<Subscripts> res;
+    for (int i = 0; i < n_nodes; ++i) {
+      j.push_back({joins[2 * i], joins[2 * i + 1]});
+      res.push_back(parse_subscripts(results[i]));
+    }
+    auto p = std::make_unique<ce_plan>();
+    p->plan = plan_from_nodes(spec, env, modes_arg(spec, mode), cost_mode_from_string(cost_mode), j, res);
     *out = p.release();
   });
 }
@@ -300,6 +369,13 @@ ce_status ce_layer_expression(const char* kind, const int64_t* t_factors, int n_
       l.ranks.assign(ranks, ranks + n_ranks);
     }
     LayerExpression ex = expression(l);
+    // ranks_of_input / ranks_out are caller arrays of CE_MAX_LAYER_INPUTS / CE_MAX_LAYER_RANKS
+    if (ex.env.dims.size() > CE_MAX_LAYER_INPUTS)
+      throw ShapeError("layer has " + std::to_string(ex.env.dims.size()) + " inputs (CE_MAX_LAYER_INPUTS " +
+                       std::to_string(CE_MAX_LAYER_INPUTS) + ")");
+    if (l.ranks.size() > CE_MAX_LAYER_RANKS)
+      throw ShapeError("layer has " + std::to_string(l.ranks.size()) + " rank slots (CE_MAX_LAYER_RANKS " +
+                       std::to_string(CE_MAX_LAYER_RANKS) + ")");
     copy_out(render(ex.spec), expr_out, expr_cap);
     int pos = 0;
     for (std::size_t i = 0; i < ex.env.dims.size(); ++i) {
@@ -496,8 +572,7 @@ ce_status ce_conv_einsum(ce_ctx* ctx, const char* expr, const int64_t* dims, con
     if (it == ctx->cached.end()) {
       ExpressionSpec spec = parse(expr);
       ShapeEnv env = make_shape_env(spec, split_dims(dims, ranks, n_inputs));
-      EvaluationPlan plan =
-          optimal(spec, env, resolve_conv_modes(spec, conv_mode_from_string(mode)), cost_mode_from_string(cost_mode));
+      EvaluationPlan plan = optimal(spec, env, modes_arg(spec, mode), cost_mode_from_string(cost_mode));
       ExecConfig cfg;
       cfg.math = ctx->opts.math;
       auto ex = std::make_unique<Executor>(plan, false, cfg);
@@ -532,6 +607,7 @@ ce_status ce_ctx_init_comm(ce_ctx* ctx, int nranks, int rank, const void* id128)
 ce_status ce_allreduce_grads(ce_ctx* ctx, float* const* bufs, const int64_t* counts, int n) {
   return guard([&] {
     if (!ctx->comm) throw std::runtime_error("ce_allreduce_grads: no communicator (ce_ctx_init_comm)");
+    comm_health(ctx);
     cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
     cuda_ok(cudaEventRecord(ctx->comm_in, ctx->stream), "cudaEventRecord");
     cuda_ok(cudaStreamWaitEvent(ctx->comm_stream, ctx->comm_in, 0), "cudaStreamWaitEvent");
@@ -550,7 +626,15 @@ ce_status ce_allreduce_grads(ce_ctx* ctx, float* const* bufs, const int64_t* cou
 ce_status ce_comm_wait(ce_ctx* ctx) {
   return guard([&] {
     if (!ctx->comm) return;
+    comm_health(ctx);
     cuda_ok(cudaStreamWaitEvent(ctx->stream, ctx->comm_out, 0), "cudaStreamWaitEvent");
+  });
+}
+
+ce_status ce_comm_check(ce_ctx* ctx) {
+  return guard([&] {
+    if (!ctx->comm) throw std::runtime_error("ce_comm_check: no communicator (ce_ctx_init_comm)");
+    comm_health(ctx);
   });
 }
 

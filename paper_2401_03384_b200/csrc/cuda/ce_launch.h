@@ -12,7 +12,7 @@
 
 #include <cstdlib>
 #include <mutex>
-#include <unordered_set>
+#include <set>
 #include <utility>
 
 __device__ __forceinline__ void ce_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -37,14 +37,17 @@ inline bool ce_pdl_enabled() {
 // CE_CARVEOUT=0 leaves the driver default.
 inline void ce_prefer_max_smem(const void* fn) {
   static std::mutex mu;
-  static std::unordered_set<const void*> seen;
+  static std::set<std::pair<const void*, int>> seen;
   static const bool on = [] {
     const char* e = std::getenv("CE_CARVEOUT");
     return !(e && *e == '0');
   }();
   if (!on) return;
+  // (a function attribute is set per device: key on (kernel, device))
+  int dev = 0;
+  cudaGetDevice(&dev);
   std::lock_guard<std::mutex> g(mu);
-  if (seen.insert(fn).second) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (seen.insert({fn, dev}).second) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 template <typename... Exp, typename... Act>

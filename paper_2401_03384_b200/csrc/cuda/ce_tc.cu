@@ -1009,15 +1009,24 @@ bool encode(CUtensorMap* map, const void* ptr, const uint64_t* gdim, const uint6
   return r == CUDA_SUCCESS;
 }
 
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 || dev >= kMaxDevices ? 0 : dev;
+}
+
+// SM count of the current device (cached per device: one process may drive several GPUs)
 int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static int n[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!n[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
   }
-  return n;
+  return n[dev];
 }
 
 template <int BN, int STAGES, bool PAIR>
@@ -1027,15 +1036,17 @@ cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
       (2 * BN + 2 * (BN / 4) + 2 * TC_BM) * 8 + 4 * static_cast<int>(sizeof(Tile)) + 8 * (3 * STAGES + 4) + 16 + 64 +
       static_cast<int>(sizeof(TcParams)) + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
-  static bool configured = false;
-  if (!configured) {
+  // the dynamic-smem opt-in is a per-device function attribute
+  static bool configured[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!configured[dev]) {
     cudaError_t e =
         cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     if (cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES, PAIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
         cudaSuccess)
       cudaGetLastError();
-    configured = true;
+    configured[dev] = true;
   }
   const int csize = P.mcast ? 2 : 1;
   const int64_t groups = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;

@@ -1122,10 +1122,19 @@ void Executor::forward(const float* const* inputs, float* out, cudaStream_t s) {
   out_ = out;
   last_launches_ = 0;
   launch_pass(fwd_, nullptr, s, 0);
+  fwd_inputs_ = inputs_;
+  fwd_ran_ = true;
 }
 
 void Executor::backward(const float* const* inputs, const float* dout, float* const* dinputs, cudaStream_t s) {
   if (!want_backward_) throw std::runtime_error("executor was created without backward support");
+  // the backward reads the intermediates (and repacked inputs) the preceding forward left in
+  // the workspace: it must have run on these very input buffers
+  if (!fwd_ran_) throw std::runtime_error("backward: no forward has run on this executor");
+  for (int i = 0; i < n_; ++i)
+    if (fwd_inputs_[static_cast<std::size_t>(i)] != inputs[i])
+      throw std::runtime_error("backward: input " + std::to_string(i) +
+                               " is not the buffer the last forward ran on (run forward on these inputs first)");
   ensure_workspace();
   dout_ = dout;
   // intermediate gradients are only needed above requested inputs

@@ -100,6 +100,8 @@ class Executor {
   char* ws_ = nullptr;
   // bound per call
   std::vector<const float*> inputs_;
+  std::vector<const float*> fwd_inputs_;  // inputs of the last forward (its intermediates are in ws_)
+  bool fwd_ran_ = false;
   float* out_ = nullptr;
   const float* dout_ = nullptr;
   std::vector<float*> dinputs_;

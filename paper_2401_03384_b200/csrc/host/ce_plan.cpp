@@ -339,6 +339,76 @@ EvaluationPlan plan_from_joins(const ExpressionSpec& spec, const ShapeEnv& env,
   return build_plan(t, order);
 }
 
+EvaluationPlan plan_from_nodes(const ExpressionSpec& spec, const ShapeEnv& env, const ConvModeMap& modes,
+                               CostMode cost_mode, const std::vector<std::pair<int, int>>& joins,
+                               const std::vector<Subscripts>& results) {
+  const int n = static_cast<int>(spec.inputs.size());
+  if (joins.size() != results.size()) throw PlanError("plan_from_nodes: one result per join expected");
+  if (n > 1 && static_cast<int>(joins.size()) != n - 1)
+    throw PlanError("plan_from_nodes: expected " + std::to_string(n - 1) + " nodes");
+  for (const auto& a : spec.conv_atoms)
+    if (!modes.count(a)) throw ShapeError("plan_from_nodes: no convolution mode for atom '" + a.name + "'");
+  EvaluationPlan plan;
+  plan.spec = spec;
+  plan.env = env;
+  plan.modes = modes;
+  plan.cost_mode = cost_mode;
+  std::vector<Subscripts> subs(spec.inputs.begin(), spec.inputs.end());
+  std::vector<std::vector<int64_t>> dims(env.dims.begin(), env.dims.end());
+  std::vector<char> used(static_cast<std::size_t>(n), 0);
+  uint64_t peak = 0;
+  for (std::size_t j = 0; j < joins.size(); ++j) {
+    const auto [l, r] = joins[j];
+    const int count = static_cast<int>(subs.size());
+    if (l < 0 || r < 0 || l >= count || r >= count || l == r)
+      throw PlanError("plan_from_nodes: operand id out of range");
+    if (used[static_cast<std::size_t>(l)] || used[static_cast<std::size_t>(r)])
+      throw PlanError("plan_from_nodes: operand used twice");
+    used[static_cast<std::size_t>(l)] = used[static_cast<std::size_t>(r)] = 1;
+    // an atom the rest of the plan still needs (output, or an operand not joined yet) must survive
+    for (const Subscripts* side : {&subs[static_cast<std::size_t>(l)], &subs[static_cast<std::size_t>(r)]})
+      for (const Atom& a : *side) {
+        bool needed = spec.in_output(a);
+        for (int k = 0; k < count && !needed; ++k)
+          if (k != l && k != r && !used[static_cast<std::size_t>(k)] && find_atom(subs[static_cast<std::size_t>(k)], a) >= 0)
+            needed = true;
+        if (needed && find_atom(results[j], a) < 0)
+          throw PlanError("plan_from_nodes: node " + std::to_string(j) + " drops atom '" + a.name +
+                          "' that a later node or the output needs");
+      }
+    const std::set<Atom> keep(results[j].begin(), results[j].end());
+    PlanNode node;
+    node.left = l;
+    node.right = r;
+    node.op = make_pairwise_op(subs[static_cast<std::size_t>(l)], dims[static_cast<std::size_t>(l)],
+                               subs[static_cast<std::size_t>(r)], dims[static_cast<std::size_t>(r)], keep, modes,
+                               results[j]);
+    node.cost = pairwise_cost(node.op, cost_mode).total;
+    plan.total_cost = add_checked(plan.total_cost, node.cost);
+    peak = std::max(peak, static_cast<uint64_t>(node.op.result_elements()));
+    subs.push_back(node.op.result);
+    dims.push_back(node.op.result_dims);
+    used.push_back(0);
+    plan.nodes.push_back(std::move(node));
+  }
+  plan.peak_intermediate_elements = peak;
+  if (plan.nodes.empty()) {
+    const auto& in0 = spec.inputs[0];
+    for (std::size_t j = 0; j < in0.size(); ++j)
+      if (spec.in_output(in0[j])) {
+        plan.root_subs.push_back(in0[j]);
+        plan.root_dims.push_back(env.dims[0][j]);
+      }
+  } else {
+    plan.root_subs = plan.nodes.back().op.result;
+    plan.root_dims = plan.nodes.back().op.result_dims;
+    for (const Atom& a : spec.output)
+      if (find_atom(plan.root_subs, a) < 0)
+        throw ShapeError("execute: root is missing output atom '" + a.name + "'");
+  }
+  return plan;
+}
+
 u128 plan_cost(const EvaluationPlan& plan, CostMode mode) {
   u128 total = 0;
   for (const auto& n : plan.nodes) total = add_checked(total, pairwise_cost(n.op, mode).total);

@@ -49,6 +49,14 @@ std::vector<EvaluationPlan> enumerate_all(const ExpressionSpec& spec, const Shap
 EvaluationPlan plan_from_joins(const ExpressionSpec& spec, const ShapeEnv& env,
                                const ConvModeMap& modes, CostMode cost_mode,
                                const std::vector<std::pair<int, int>>& joins);
+// A caller's plan replayed node by node (the reference's EvaluationPlan is a plain struct its
+// callers may build or edit, sequencer.hpp:30-41): node j joins operand ids (left, right)
+// (inputs 0..N-1, node k is N+k) and keeps exactly `results[j]`'s atoms in that order, i.e.
+// make_pairwise_op(..., keep = set(results[j]), modes, results[j]) as the planner's node_op
+// (sequencer.cpp:117-123).  Costs, total and peak are recomputed as build_plan does.
+EvaluationPlan plan_from_nodes(const ExpressionSpec& spec, const ShapeEnv& env, const ConvModeMap& modes,
+                               CostMode cost_mode, const std::vector<std::pair<int, int>>& joins,
+                               const std::vector<Subscripts>& results);
 u128 plan_cost(const EvaluationPlan& plan, CostMode mode);
 std::string tree_encoding(const EvaluationPlan& plan);
 std::string plan_to_json(const EvaluationPlan& plan);

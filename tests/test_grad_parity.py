@@ -1,0 +1,122 @@
+"""Elementwise gradient parity at the benchmarked (full) shapes.
+
+The executor runs the FULL layer (batch 128 for cfg2/cfg5, so the launches are exactly the
+benchmarked ones: BN=256 tiles, K tails such as R=229 = 7*32+5, split-K factor gradients,
+repacks) with an upstream gradient dY that is zero except on a few samples S.  Because
+every layer expression is multilinear and `b` appears only in X and Y (layers.cpp:159-176):
+
+  * dX[b] for b in S depends only on dY[b] and the factors -> compared elementwise with the
+    FP64 adjoint oracle (oracle/np_oracle.py backward) run at batch |S|;
+  * dX[b] for b not in S is exactly zero (no cross-sample leakage);
+  * every factor gradient dW = sum_b dW_b equals the oracle's factor gradient at batch |S|
+    (the other samples contribute exact zeros), so it is compared elementwise too;
+  * the forward output of the samples in S is compared with the oracle's forward.
+
+Tolerances (normwise max |y - y*| / max |y*|) as tests/test_gpu_parity.py: TF32 5e-3
+forward, 1e-2 gradients; FP32 SIMT 1e-5.
+"""
+import json
+
+import numpy as np
+import pytest
+
+from oracle import np_oracle as npo
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": (1e-5, 1e-5), "auto": (5e-3, 1e-2)}
+
+# (name, kind, T factors, S factors, filter, H', batch, cr)
+CASES = [
+    ("cfg2 TK cr0.1", "tk", [256], [256], 3, 14, 128, 0.1),
+    ("cfg2 TK cr1.0", "tk", [256], [256], 3, 14, 128, 1.0),
+    ("cfg2 TT cr0.1", "tt", [256], [256], 3, 14, 128, 0.1),
+    ("cfg2 TT cr1.0", "tt", [256], [256], 3, 14, 128, 1.0),
+    ("cfg5 CP cr0.5", "cp", [256], [256], 3, 14, 128, 0.5),
+    ("cfg5 TR cr0.05", "tr", [256], [256], 3, 14, 128, 0.05),
+    ("cfg5 TR cr0.5", "tr", [256], [256], 3, 14, 128, 0.5),
+    ("cfg5 dense", "standard", [256], [256], 3, 14, 128, None),
+    ("cfg4 CP conv2_x cr1.0 B128", "cp", [64], [64], 3, 56, 128, 1.0),
+    ("cfg4 CP conv5_x cr0.1 B128", "cp", [512], [512], 3, 7, 128, 0.1),
+    ("cfg4 CP conv1 cr1.0 B16", "cp", [64], [3], 7, 112, 16, 1.0),
+    ("cfg3 RTR 64->128 @28 B64", "rtr", [4, 4, 8], [4, 4, 4], 3, 28, 64, 0.1),
+    ("cfg3 RTR 256 @14 cr1.0 B256", "rtr", [4, 8, 8], [4, 8, 8], 3, 14, 256, 1.0),
+]
+
+
+def _nerr(y, ref):
+    y = np.asarray(y, dtype=np.float64).ravel()
+    ref = np.asarray(ref, dtype=np.float64).ravel()
+    return float(np.abs(y - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def _layer(ce, kind, tf, sf, k, hp, batch, cr, ranks=None):
+    slots = {"cp": 1, "tk": 2, "tt": 3, "tr": 4, "rtr": 4, "standard": 0}[kind]
+    spec = ce.LayerSpec(kind, tf, sf, k, k, hp, hp, batch, ranks if ranks is not None else [1] * slots)
+    return ce.expression(spec, None if (cr is None or ranks is not None) else cr)
+
+
+@pytest.fixture(params=["auto", "fp32"])
+def mode_ctx(request, ctx, ctx_simt):
+    return (ctx if request.param == "auto" else ctx_simt), request.param
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_full_shape_gradients_elementwise(mode_ctx, case):
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import Executor
+    c_, mode = mode_ctx
+    name, kind, tf, sf, k, hp, B, cr = case
+    if mode == "fp32" and B * hp * hp > 128 * 14 * 14 * 4:
+        pytest.skip("FP32-SIMT anchor only at the cfg2-sized shapes (runtime)")
+    le = _layer(ce, kind, tf, sf, k, hp, B, cr)
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    ex = Executor(c_, plan, backward=True)
+    xs = [c_.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
+    S = sorted({0, B // 2, B - 1})
+    dout = c_.fill_random(plan.out_dims, 2000)
+    mask = torch.zeros(B, device=dout.device)
+    mask[S] = 1.0
+    dout = dout * mask.view([B] + [1] * (dout.dim() - 1))
+    out = ex.execute(xs)
+    grads = ex.backward(xs, dout)
+    torch.cuda.synchronize()
+
+    # oracle at batch |S| with the same samples (the tree may differ: same multilinear map)
+    sub = _layer(ce, kind, tf, sf, k, hp, len(S), cr, ranks=le.ranks if cr is not None else [])
+    p1 = ce.optimal(sub.expr, sub.dims, "same", "training")
+    nodes = [(n["left"], n["right"], n["result"]) for n in json.loads(p1.to_json())["nodes"]]
+    ins = [xs[0][S].double().cpu().numpy()] + [x.double().cpu().numpy() for x in xs[1:]]
+    dy = dout[S].double().cpu().numpy()
+    ref_y, _ = npo.execute(sub.expr, sub.dims, nodes, ins)
+    ref_g = npo.backward(sub.expr, sub.dims, nodes, ins, dy)
+
+    tol_f, tol_g = TOL[mode]
+    assert _nerr(out[S].cpu().numpy(), ref_y) <= tol_f, (name, "forward")
+    g0 = grads[0]
+    assert _nerr(g0[S].cpu().numpy(), ref_g[0]) <= tol_g, (name, "dX")
+    others = [b for b in range(B) if b not in S]
+    assert float(g0[others].abs().max()) == 0.0, (name, "dX leaks into samples with zero dY")
+    for i in range(1, len(xs)):
+        assert _nerr(grads[i].cpu().numpy(), ref_g[i]) <= tol_g, (name, f"dW{i}")
+
+
+def test_cfg3_full_batch_forward_per_sample(ctx):
+    """cfg3's largest-batch RTR layer shape (64->64 at 56x56, B=256): per-sample forward of
+    samples 0, 128, 255 against the oracle at batch 1 (sample b depends only on X[b])."""
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import Executor
+    le = _layer(ce, "rtr", [4, 4, 4], [4, 4, 4], 3, 56, 256, 0.1)
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    ex = Executor(ctx, plan)
+    xs = [ctx.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
+    out = ex.execute(xs)
+    torch.cuda.synchronize()
+    one = _layer(ce, "rtr", [4, 4, 4], [4, 4, 4], 3, 56, 1, 0.1, ranks=le.ranks)
+    p1 = ce.optimal(one.expr, one.dims, "same", "inference")
+    nodes = [(n["left"], n["right"], n["result"]) for n in json.loads(p1.to_json())["nodes"]]
+    for b in (0, 128, 255):
+        ins = [xs[0][b:b + 1].double().cpu().numpy()] + [x.double().cpu().numpy() for x in xs[1:]]
+        ref, _ = npo.execute(one.expr, one.dims, nodes, ins)
+        assert _nerr(out[b:b + 1].cpu().numpy(), ref) <= TOL["auto"][0], b
