@@ -441,8 +441,14 @@ __device__ __forceinline__ int64_t tile_offset(const TcParams& P, const int32_t*
 // PAIR: CTA pair (cluster of 2) running M=256 tcgen05.mma.cta_group::2 issued by the even
 // CTA; each CTA stages its own 128 A rows and half of the B columns, so per-SM smem traffic
 // per MMA drops by a quarter and the ring gets deeper.
-template <int BN, int STAGES, bool PAIR>
-__global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constant__ TcParams Pg, float* __restrict__ C) {
+// LEAN: no transposer warps (native MN-major or K-major operands only), 192 threads and a
+// shared-memory footprint under half an SM, so two CTAs are resident per SM -- two of this
+// launch, or one of it and the PDL-launched next kernel, whose set-up (barriers, TMEM
+// allocation, first tile decode) then overlaps this kernel's last epilogue.  Short-K steps.
+template <int BN, int STAGES, bool PAIR, bool LEAN>
+__global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 2 : 1)
+    ce_tc_kernel(const __grid_constant__ TcParams Pg, float* __restrict__ C) {
+  constexpr int NT = LEAN ? 64 + 32 * kEpiWarps : kThreads;
   constexpr int A_BYTES = TC_BM * 128;
   constexpr int B_BYTES = PAIR ? BN * 64 : BN * 128;
   extern __shared__ uint8_t smem_raw[];
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  constexpr int EPI_GROUPS = BN == 64 ? 2 : 1;  // small tiles: a second epilogue warp group
+  constexpr int EPI_GROUPS = (BN == 64 && !LEAN) ? 2 : 1;  // small tiles: a second epilogue warp group
   float* stage_out = reinterpret_cast<float*>(sB + STAGES * B_BYTES);  // [EPI_GROUPS*kEpiWarps][32][kStagePitch]
   int64_t* col_off = reinterpret_cast<int64_t*>(stage_out + EPI_GROUPS * kEpiWarps * 32 * kStagePitch);  // [2][BN]
   int64_t* grp_off = col_off + 2 * BN;                                  // [2][BN/4]: 16-B column groups
@@ -470,13 +476,13 @@ __global__ void __launch_bounds__(kThreads, 1) ce_tc_kernel(const __grid_constan
   {
     const uint4* src = reinterpret_cast<const uint4*>(&Pg);
     uint4* dst = reinterpret_cast<uint4*>(sP);
-    for (int i = threadIdx.x; i < static_cast<int>(sizeof(TcParams) / 16); i += kThreads) dst[i] = src[i];
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(TcParams) / 16); i += NT) dst[i] = src[i];
   }
   const TcParams& P = *sP;
   if (TC_DBG(Pg) & 128) return;  // timing experiment: launch cost only
   // MN-major operands are either read by the MMA directly (native: transpose bits in the
   // instruction descriptor, MN-major smem descriptors) or transposed in smem by warps 6..9
-  const bool xpose = !Pg.native_mn && (Pg.oa.mn_major || Pg.ob.mn_major);
+  const bool xpose = !LEAN && !Pg.native_mn && (Pg.oa.mn_major || Pg.ob.mn_major);
   // (the single-CTA B multicast, mcast 1, is no longer planned -- see ce_tc_plan.cpp;
   // compiled out so the non-pair instances carry no multicast code)
   constexpr bool mc = false;
@@ -1029,31 +1035,33 @@ int sm_count() {
   return n[dev];
 }
 
-template <int BN, int STAGES, bool PAIR>
-cudaError_t launch(const TcParams& P, float* C, cudaStream_t s) {
+template <int BN, int STAGES, bool PAIR, bool LEAN = false>
+cudaError_t launch(const TcParams& P, float* C, cudaStream_t s, int per_sm = 1) {
   constexpr int smem =
-      STAGES * (TC_BM * 128 + (PAIR ? BN * 64 : BN * 128)) + (BN == 64 ? 2 : 1) * kEpiWarps * 32 * kStagePitch * 4 +
+      STAGES * (TC_BM * 128 + (PAIR ? BN * 64 : BN * 128)) + ((BN == 64 && !LEAN) ? 2 : 1) * kEpiWarps * 32 * kStagePitch * 4 +
       (2 * BN + 2 * (BN / 4) + 2 * TC_BM) * 8 + 4 * static_cast<int>(sizeof(Tile)) + 8 * (3 * STAGES + 4) + 16 + 64 +
       static_cast<int>(sizeof(TcParams)) + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
+  static_assert(!LEAN || smem <= 113 * 1024, "LEAN: two CTAs per SM");
   // the dynamic-smem opt-in is a per-device function attribute
   static bool configured[kMaxDevices] = {};
   const int dev = current_device();
   if (!configured[dev]) {
     cudaError_t e =
-        cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES, PAIR, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    if (cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES, PAIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+    if (cudaFuncSetAttribute(ce_tc_kernel<BN, STAGES, PAIR, LEAN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
         cudaSuccess)
       cudaGetLastError();
     configured[dev] = true;
   }
   const int csize = P.mcast ? 2 : 1;
   const int64_t groups = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
-  const int64_t max_groups = sm_count() / csize;
+  const int64_t max_groups = static_cast<int64_t>(sm_count()) * per_sm / csize;
   const int grid = static_cast<int>((groups < max_groups ? groups : max_groups) * csize);
   (void)grid;
-  return ce_launch_cluster(ce_tc_kernel<BN, STAGES, PAIR>, dim3(grid), dim3(kThreads), smem, s,
+  return ce_launch_cluster(ce_tc_kernel<BN, STAGES, PAIR, LEAN>, dim3(grid), dim3(LEAN ? 64 + 32 * kEpiWarps : kThreads),
+                           smem, s,
                            static_cast<unsigned>(csize),
                            P, C);
 }
@@ -1092,11 +1100,26 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
   }
   if (static_cast<int64_t>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_split >= (1ll << 32))
     return cudaErrorInvalidConfiguration;
+  // LEAN instances (two CTAs per SM, see ce_tc_kernel) for short K loops with N tiles <= 128
+  // and no in-smem transposes.  CE_TC_LEAN: 0 off, 1 one CTA of this launch per SM (the
+  // second slot takes the next kernel's set-up), 2 (default) two CTAs of this launch per SM.
+  // cfg2 step (same-box A/B x3): off 1.127-1.131, 1 1.131-1.138, 2 1.119-1.121 ms.
+  static const int lean_mode = [] {
+    const char* e = getenv("CE_TC_LEAN");
+    return e ? atoi(e) : 2;
+  }();
+  static const int lean_kmax = [] {
+    const char* e = getenv("CE_TC_LEAN_KMAX");
+    return e ? atoi(e) : 24;
+  }();
+  const bool lean = lean_mode > 0 && !P.mcast && plan.bn <= 128 && P.k_per <= lean_kmax &&
+                    (P.native_mn || (!P.oa.mn_major && !P.ob.mn_major)) && !(P.oa.mn_major && P.oa.wide);
+  const int per_sm = lean ? (lean_mode >= 2 ? 2 : 1) : 1;
   {
     // stream-K tail of a partial last round (see TcParams::sk_r)
     const int64_t csize = P.mcast ? 2 : 1;
     const int64_t items = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
-    const int64_t ngroups = std::min<int64_t>(items, sm_count() / csize);
+    const int64_t ngroups = std::min<int64_t>(items, static_cast<int64_t>(sm_count()) * per_sm / csize);
     P.n_items = static_cast<uint32_t>(items);
     P.sk_full = 0;
     P.sk_r = 0;
@@ -1140,6 +1163,10 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
       case 128: return launch<128, 8, true>(P, C, s);
       default: return launch<256, 6, true>(P, C, s);
     }
+  }
+  if (lean) {
+    if (plan.bn == 64) return launch<64, 3, false, true>(P, C, s, per_sm);
+    return launch<128, 2, false, true>(P, C, s, per_sm);
   }
   switch (plan.bn) {
     case 64: return launch<64, 7, false>(P, C, s);

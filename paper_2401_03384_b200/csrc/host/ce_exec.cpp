@@ -670,11 +670,12 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       }
     }
     if (!ok && try_col2im()) return;
-    // CE_MN_REPACK: 1 (default) both long-K repack rules below, 2 only the double-MN-major one,
-    // 0 none (native MN-major operands are read by the MMA directly; A/B knob)
+    // CE_MN_REPACK: 2 (default) only the double-MN-major rule, 1 both long-K repack rules below,
+    // 0 none.  Native MN-major operands are read by the MMA directly, so the single-MN-major
+    // repack no longer pays: cfg2 step 1.186 -> 1.133 ms with 2 (same-box A/B x3, round 2)
     static const int mn_repack = [] {
       const char* e = std::getenv("CE_MN_REPACK");
-      return e ? std::atoi(e) : 1;
+      return e ? std::atoi(e) : 2;
     }();
     if (ok && mn_repack >= 1 && st.tc.params.oa.mn_major && st.tc.params.ob.mn_major && st.tc.params.k_iters > 64) {
       // Both operands would be transposed in shared memory every stage: over a long K

@@ -369,6 +369,24 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     // (a long K loop is split across CTAs instead: split-K fills the machine)
     if (cols >= 128 && k_elems <= 64.0 * TC_BK && out_elems / (static_cast<double>(P.m_rows) * cols) < 74)
       ncap = 128;
+    // store-bound launches (a K loop of a few stages, e.g. the rank -> channel 1x1 GEMMs writing
+    // a [b,t,h,w] activation): half-width N tiles run on the LEAN instances, two CTAs per SM,
+    // so two epilogues drain per SM.  CE_TC_SHORTK_NCAP=0 off.
+  }
+  {
+    // store-bound launches (a K loop of a few stages, e.g. the rank -> channel 1x1 GEMMs writing
+    // a [b,t,h,w] activation): N tiles of at most 128 columns run on the LEAN instances, two
+    // CTAs per SM, so two epilogues drain per SM.  CE_TC_SHORTK_NCAP=<K stages> (0 off).
+    static const int shortk_kmax = [] {
+      const char* e = std::getenv("CE_TC_SHORTK_NCAP");
+      return e ? std::atoi(e) : 4;
+    }();
+    double k_elems = 1, n_elems = 1;
+    for (int v = 0; v < p.nv; ++v) {
+      if (p.cls[v] == CE_K) k_elems *= static_cast<double>(p.ext[v]);
+      if (p.cls[v] == CE_N) n_elems *= static_cast<double>(p.ext[v]);
+    }
+    if (n_elems > 128 && k_elems <= static_cast<double>(shortk_kmax) * TC_BK) ncap = std::min(ncap, 128);
   }
   P.n_cols = tile(B, b_mn == 1, CE_N, ncap, P.nt, &P.nn, TC_SRC_NTILE);
   if (P.nm == 0) return fail("no M tile unit");
