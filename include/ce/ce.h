@@ -100,7 +100,8 @@ ce_status ce_plan_node(const ce_plan* plan, int node, int* left, int* right, cha
                        uint64_t* flops_actual_lo, uint64_t* cost_lo);
 
 /* The kernel steps an executor would launch for this plan (no device needed):
- * one line per step "fwd|bwd label kind details", then "workspace_bytes N". */
+ * one line per step "fwd|bwd label kind details", then "workspace_bytes N" (liveness-
+ * shared arena) and "workspace_bytes_unshared N" (every buffer alive throughout). */
 ce_status ce_plan_describe_steps(const ce_plan* plan, int want_backward, int math, char* buf, size_t cap);
 
 /* ----------------------------------------------------------------- layers -- */
@@ -164,7 +165,8 @@ ce_status ce_backward(ce_executor* ex, const float* const* inputs, const float* 
 /* Per-kernel device timing: when enabled, every launched step is bracketed by
  * CUDA events on the ctx stream.  ce_executor_profile reports the last forward
  * (backward = 0) or backward call: newline-separated labels, kind (0 direct,
- * 1 tiled, 2 tensor-core, 3 memset, 4 reduce), ms, algorithmic FLOPs and bytes. */
+ * 1 tiled, 2 tensor-core, 3 memset, 4 reduce, 5 permute, 6 fused chain), ms, algorithmic
+ * FLOPs and bytes. */
 ce_status ce_executor_set_profiling(ce_executor* ex, int enable);
 ce_status ce_executor_profile(ce_executor* ex, int backward, int max_steps, int* n_steps, char* labels,
                               size_t labels_cap, int* kinds, float* ms, double* flops, double* bytes);

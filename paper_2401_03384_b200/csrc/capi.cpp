@@ -397,7 +397,9 @@ ce_status ce_plan_describe_steps(const ce_plan* plan, int want_backward, int mat
     ExecConfig cfg;
     cfg.math = math;
     Executor ex(plan->plan, want_backward != 0, cfg);
-    copy_out(ex.describe() + "workspace_bytes " + std::to_string(ex.workspace_bytes()) + "\n", buf, cap);
+    copy_out(ex.describe() + "workspace_bytes " + std::to_string(ex.workspace_bytes()) + "\n" +
+                 "workspace_bytes_unshared " + std::to_string(ex.workspace_bytes_unshared()) + "\n",
+             buf, cap);
   });
 }
 

@@ -715,14 +715,23 @@ template <int KT, int SA, int SB>
 __global__ void __launch_bounds__(256) ce_dwgrad_kernel(const SvDesc d, const float* __restrict__ A,
                                                         const float* __restrict__ B, float* __restrict__ C) {
   ce_pdl_enter();
+  // few lane quads (outs <= 256): the K slices of one CTA are first summed in shared memory
+  // (block-scope atomics), then one global atomic per (CTA, output) -- so the K range can be
+  // cut into enough slices to fill the GPU without every slice contending on the same words
+  __shared__ float sred[256 * KT * 4];
+  const bool cta_red = d.mode == 2 && d.outs <= 256;
+  if (cta_red) {
+    for (int i = threadIdx.x; i < static_cast<int>(d.outs) * KT * 4; i += 256) sred[i] = 0.f;
+    __syncthreads();
+  }
   const uint32_t t = blockIdx.x * 256u + threadIdx.x;
   const uint32_t nslices = (d.K + d.kper - 1) / d.kper;
-  if (t >= d.outs * nslices) return;
-  const uint32_t slice = tc_quo(t, d.odiv[0]);
-  const uint32_t o = t - slice * d.outs;
+  const bool live = t < d.outs * nslices;
+  const uint32_t slice = tc_quo(live ? t : 0u, d.odiv[0]);
+  const uint32_t o = (live ? t : 0u) - slice * d.outs;
   const int32_t lane0 = static_cast<int32_t>(o) * 4;
   const uint32_t k0 = slice * d.kper;
-  const uint32_t k1 = min(d.K, k0 + d.kper);
+  const uint32_t k1 = live ? min(d.K, k0 + d.kper) : k0;
   int32_t kv[SV_K];
   int32_t offAk = 0, offBk = 0;
   uint32_t rest = k0;
@@ -833,7 +842,23 @@ __global__ void __launch_bounds__(256) ce_dwgrad_kernel(const SvDesc d, const fl
       }
     }
   }
-  const int32_t offC = lane0 * d.osc[0], sc0 = d.osc[0], sc1 = d.osc[1];
+  const int32_t sc0 = d.osc[0], sc1 = d.osc[1];
+  if (cta_red) {
+    if (live)
+#pragma unroll
+      for (int q = 0; q < KT; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) atomicAdd_block(&sred[(o * KT + q) * 4 + e], acc[q][e]);
+    __syncthreads();
+    // the CTA's outputs: quads present in it (all of them once it spans >= outs threads)
+    for (int i = threadIdx.x; i < static_cast<int>(d.outs) * KT * 4; i += 256) {
+      const int e = i & 3, q = (i >> 2) % KT, oq = (i >> 2) / KT;
+      if (oq * 4 + e < d.lext && sred[i] != 0.f) atomicAdd(C + (oq * 4 + e) * sc0 + q * sc1, sred[i]);
+    }
+    return;
+  }
+  if (!live) return;
+  const int32_t offC = lane0 * d.osc[0];
 #pragma unroll
   for (int q = 0; q < KT; ++q)
 #pragma unroll
@@ -1211,8 +1236,18 @@ bool sv_build(const CeSimtDesc& sd, const float* A, const float* B, const float*
       const char* e = std::getenv("CE_DWG_SLICES");
       return e ? std::atoll(e) : int64_t{16384};
     }();
-    split = std::max<int64_t>(1, std::min<int64_t>((148 * 256 * 4 + outs - 1) / outs, K / 64));
-    if (cap > 0 && outs < 16) split = std::min<int64_t>(split, std::max<int64_t>(1, cap / outs));
+    // (outs <= 256: the kernel sums a CTA's slices in shared memory first, so contention no
+    // longer caps the slice count -- ~8 CTAs per SM, each thread >= 48 K steps)
+    static const int64_t kmin = [] {
+      const char* e = std::getenv("CE_DWG_KMIN");
+      return e ? std::atoll(e) : int64_t{48};
+    }();
+    if (outs <= 256) {
+      split = std::max<int64_t>(1, std::min<int64_t>((148 * 256 * 8 + outs - 1) / outs, K / kmin));
+    } else {
+      split = std::max<int64_t>(1, std::min<int64_t>((148 * 256 * 4 + outs - 1) / outs, K / 64));
+      if (cap > 0 && outs < 16) split = std::min<int64_t>(split, std::max<int64_t>(1, cap / outs));
+    }
   }
   else if (blocks < 148 * 8 && K >= 64)
     split = std::min<int64_t>((148 * 8 + blocks - 1) / blocks, K / (klane ? 1024 : 32));

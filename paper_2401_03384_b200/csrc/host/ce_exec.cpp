@@ -48,8 +48,23 @@ Executor::Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cf
   }
   build_forward();
   if (want_backward_) build_backward();
+  static const bool fuse_on = [] {  // CE_FUSE=0: no node fusion
+    const char* e = std::getenv("CE_FUSE");
+    return !(e && *e == '0');
+  }();
+  if (fuse_on && cfg_.math == 0) {
+    fuse_chains(fwd_);
+    fuse_chains(bwd_);
+  }
+  // hazards by buffer identity first (the happens-before order assign_offsets may alias
+  // under), then again once buffers share memory (those extra edges are already implied)
   compute_deps(fwd_);
   compute_deps(bwd_);
+  assign_offsets();
+  if (ws_reuse_mode_ >= 2) {  // (mode 1 shares only along edges the identity hazards already imply)
+    compute_deps(fwd_);
+    compute_deps(bwd_);
+  }
   if (const char* e = std::getenv("CE_CONCURRENT"); e && *e == '0') concurrent_ = false;
   if (const char* dbg = std::getenv("CE_DEBUG"); dbg && *dbg == '1') std::fputs(describe().c_str(), stderr);
 }
@@ -73,22 +88,134 @@ Executor::~Executor() {
   if (fork_ev_) cudaEventDestroy(fork_ev_);
 }
 
-// Read-after-write, write-after-write and write-after-read hazards between the steps of
-// one pass.  Buffers are identified by their reference: workspace buffers come from a
-// bump allocator, so distinct offsets never overlap.
-void Executor::compute_deps(std::vector<Step>& steps) {
-  auto same = [](const BufRef& x, const BufRef& y) {
-    return x.kind != BufRef::kNone && x.kind == y.kind && x.index == y.index;
+// Two references that may touch the same bytes: the same caller buffer, or workspace
+// buffers whose assigned ranges intersect (distinct buffers share memory when their
+// lifetimes are disjoint, see assign_offsets).
+bool Executor::overlap(const BufRef& x, const BufRef& y) const {
+  if (x.kind == BufRef::kNone || x.kind != y.kind) return false;
+  if (x.index == y.index) return true;
+  if (x.kind != BufRef::kWork || buf_off_.empty()) return false;
+  const auto i = static_cast<std::size_t>(x.index), j = static_cast<std::size_t>(y.index);
+  return buf_off_[i] < buf_off_[j] + buf_bytes_[j] && buf_off_[j] < buf_off_[i] + buf_bytes_[i];
+}
+
+// Liveness-based workspace placement (the reference keeps every intermediate
+// alive, sequencer.cpp:421-433).  Two buffers may share memory only when every step touching
+// one HAPPENS BEFORE every step touching the other in the passes' existing dependency order
+// (the forward pass entirely precedes the backward pass; within a pass, the transitive
+// closure of the identity hazards of compute_deps), so sharing never adds a synchronisation
+// the side streams did not already have.  Buffers are placed largest first at the lowest
+// offset free of every placed buffer they may not share with.  CE_WS_REUSE=0: bump layout.
+void Executor::assign_offsets() {
+  const std::size_t nb = buf_bytes_.size();
+  ws_unshared_ = 0;
+  for (int64_t b : buf_bytes_) ws_unshared_ += b;
+  buf_off_.assign(nb, 0);
+  // CE_WS_REUSE: 0 bump layout; 1 share only along the existing happens-before order (no
+  // new synchronisation: cfg2 step within noise of the bump layout); 2 share whenever the
+  // lifetimes are disjoint on the step timeline (the hazard edges this adds between side
+  // streams cost the cfg2 step ~7%, same-box A/B).  Default: 1, or 2 when the bump layout
+  // would exceed CE_WS_TIGHT_GB (16) -- e.g. cfg3's 64->128 layer at B=256: 54 -> 22 GB.
+  static const int reuse_env = [] {
+    const char* e = std::getenv("CE_WS_REUSE");
+    return e ? std::atoi(e) : -1;
+  }();
+  static const double tight_gb = [] {
+    const char* e = std::getenv("CE_WS_TIGHT_GB");
+    return e ? std::atof(e) : 16.0;
+  }();
+  const int reuse = reuse_env >= 0 ? reuse_env : (static_cast<double>(ws_unshared_) > tight_gb * 1073741824.0 ? 2 : 1);
+  ws_reuse_mode_ = reuse;
+  if (!reuse) {
+    int64_t off = 0;
+    for (std::size_t i = 0; i < nb; ++i) {
+      buf_off_[i] = off;
+      off += buf_bytes_[i];
+    }
+    ws_bytes_ = off;
+    return;
+  }
+  // global step index t: forward steps 0..F-1, backward steps F..F+B-1
+  const std::size_t F = fwd_.size(), T = F + bwd_.size();
+  std::vector<std::vector<uint64_t>> before(T, std::vector<uint64_t>((T + 63) / 64, 0));  // before[t]: steps ordered before t
+  auto set = [&](std::size_t t, std::size_t u) { before[t][u / 64] |= 1ull << (u % 64); };
+  auto get = [&](std::size_t t, std::size_t u) { return (before[t][u / 64] >> (u % 64)) & 1ull; };
+  for (std::size_t t = 0; t < T; ++t) {
+    const bool bwd = t >= F;
+    const Step& st = bwd ? bwd_[t - F] : fwd_[t];
+    if (bwd)
+      for (std::size_t u = 0; u < F; ++u) set(t, u);
+    for (int d : st.deps) {
+      const std::size_t u = (bwd ? F : 0) + static_cast<std::size_t>(d);
+      set(t, u);
+      for (std::size_t w = 0; w < before[t].size(); ++w) before[t][w] |= before[u][w];
+    }
+  }
+  std::vector<std::vector<std::size_t>> uses(nb);
+  std::vector<int> last(nb, -1);
+  {
+    std::size_t t = 0;
+    for (const auto* list : {&fwd_, &bwd_})
+      for (const Step& st : *list) {
+        for (const BufRef* r : {&st.a, &st.b, &st.c, &st.b2, &st.c2})
+          if (r->kind == BufRef::kWork) {
+            const auto i = static_cast<std::size_t>(r->index);
+            if (uses[i].empty() || uses[i].back() != t) uses[i].push_back(t);
+            last[i] = static_cast<int>(t);
+          }
+        ++t;
+      }
+  }
+  auto ordered = [&](std::size_t x, std::size_t y) {  // every use of x happens before every use of y
+    if (reuse >= 2) return !uses[x].empty() && !uses[y].empty() && uses[x].back() < uses[y].front();
+    for (std::size_t u : uses[y])
+      for (std::size_t v : uses[x])
+        if (!get(u, v)) return false;
+    return true;
   };
+  std::vector<int> first(nb, INT32_MAX);
+  for (std::size_t i = 0; i < nb; ++i)
+    if (!uses[i].empty()) first[i] = static_cast<int>(uses[i].front());
+  std::vector<std::size_t> order(nb);
+  for (std::size_t i = 0; i < nb; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](std::size_t x, std::size_t y) {
+    if (buf_bytes_[x] != buf_bytes_[y]) return buf_bytes_[x] > buf_bytes_[y];
+    return first[x] < first[y];
+  });
+  std::vector<std::size_t> placed;
+  ws_bytes_ = 0;
+  for (std::size_t i : order) {
+    if (last[i] < 0) continue;  // never referenced by a step (e.g. an intermediate a fusion keeps on chip)
+    std::vector<std::pair<int64_t, int64_t>> busy;  // ranges of placed buffers alive with i
+    for (std::size_t j : placed)
+      if (!(ordered(i, j) || ordered(j, i))) busy.push_back({buf_off_[j], buf_off_[j] + buf_bytes_[j]});
+    std::sort(busy.begin(), busy.end());
+    int64_t off = 0;
+    for (const auto& r : busy) {
+      if (off + buf_bytes_[i] <= r.first) break;
+      off = std::max(off, r.second);
+    }
+    buf_off_[i] = off;
+    ws_bytes_ = std::max(ws_bytes_, off + buf_bytes_[i]);
+    placed.push_back(i);
+  }
+}
+
+// Read-after-write, write-after-write and write-after-read hazards between the steps of
+// one pass (buffers that may share bytes, overlap()).
+void Executor::compute_deps(std::vector<Step>& steps) const {
+  auto same = [this](const BufRef& x, const BufRef& y) { return overlap(x, y); };
   for (std::size_t i = 0; i < steps.size(); ++i) {
     Step& si = steps[i];
     si.deps.clear();
     for (std::size_t j = 0; j < i; ++j) {
       const Step& sj = steps[j];
-      const bool raw = same(sj.c, si.a) || same(sj.c, si.b);
-      const bool waw = same(sj.c, si.c);
-      const bool war = same(sj.a, si.c) || same(sj.b, si.c);
-      if (raw || waw || war) si.deps.push_back(static_cast<int>(j));
+      bool hazard = false;
+      for (const BufRef* w : {&sj.c, &sj.c2})
+        for (const BufRef* r : {&si.a, &si.b, &si.b2, &si.c, &si.c2}) hazard = hazard || same(*w, *r);  // RAW, WAW
+      for (const BufRef* r : {&sj.a, &sj.b, &sj.b2})
+        for (const BufRef* w : {&si.c, &si.c2}) hazard = hazard || same(*r, *w);  // WAR
+      if (hazard) si.deps.push_back(static_cast<int>(j));
     }
   }
 }
@@ -126,6 +253,10 @@ void Executor::launch_pass(std::vector<Step>& steps, const std::vector<char>* ne
     key.push_back(resolve(st.a));
     key.push_back(resolve(st.b));
     key.push_back(resolve(st.c));
+    if (st.kind == Step::kDw2) {
+      key.push_back(resolve(st.b2));
+      key.push_back(resolve(st.c2));
+    }
   }
   if (need)
     for (char c : *need) key.push_back(reinterpret_cast<const void*>(static_cast<uintptr_t>(c)));
@@ -184,9 +315,8 @@ double problem_bytes(const CeProblem& p) {
 }  // namespace
 
 int64_t Executor::alloc(int64_t elems) {
-  const int64_t off = ws_bytes_;
-  ws_bytes_ += (elems * 4 + 255) / 256 * 256;
-  return off;
+  buf_bytes_.push_back((elems * 4 + 255) / 256 * 256);
+  return static_cast<int64_t>(buf_bytes_.size()) - 1;
 }
 
 std::vector<int64_t> Executor::output_dims() const {
@@ -813,6 +943,68 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
   list.push_back(st);
 }
 
+// Node fusion along plan chains: a depthwise stencil step whose output is
+// the A operand of a later depthwise stencil step (CP's `bhwr,rh->bhwr` -> `bhwr,rw->bhwr`,
+// layers.cpp:184-190, and the two input-gradient adjoints of that pair in the backward pass)
+// becomes one fused step (ce_fuse.cu).  The intermediate is still stored when any other step
+// of either pass reads it (the forward's Y1 feeds the backward's filter gradient).
+void Executor::fuse_chains(std::vector<Step>& list) {
+  auto refs_elsewhere = [&](const BufRef& r, const Step* x, const Step* y) {
+    for (const auto* l : {&fwd_, &bwd_})
+      for (const Step& st : *l) {
+        if (&st == x || &st == y) continue;
+        for (const BufRef* q : {&st.a, &st.b, &st.c, &st.b2, &st.c2})
+          if (q->kind == r.kind && q->index == r.index) return true;
+      }
+    return false;
+  };
+  auto same = [](const BufRef& x, const BufRef& y) { return x.kind != BufRef::kNone && x.kind == y.kind && x.index == y.index; };
+  for (std::size_t i = 0; i < list.size(); ++i) {
+    Step& si = list[i];
+    if (si.kind != Step::kDirect || si.a.kind != BufRef::kWork || si.c.kind != BufRef::kWork) continue;
+    for (std::size_t j = i + 1; j < list.size(); ++j) {
+      Step& sj = list[j];
+      if (sj.kind != Step::kDirect || !same(sj.a, si.c) || sj.c.kind != BufRef::kWork) continue;
+      // moving sj up to i's slot: nothing in between may touch its output, write its filter,
+      // or write what si reads / produces
+      bool ok = true;
+      for (std::size_t k = i + 1; k < j && ok; ++k) {
+        const Step& sk = list[k];
+        for (const BufRef* w : {&sk.c, &sk.c2})
+          ok = ok && !same(*w, sj.c) && !same(*w, sj.b) && !same(*w, si.c) && !same(*w, si.a) && !same(*w, si.b);
+        for (const BufRef* r : {&sk.a, &sk.b, &sk.b2}) ok = ok && !same(*r, sj.c);
+      }
+      if (!ok) break;
+      const bool write_mid = refs_elsewhere(si.c, &si, &sj);
+      // When the intermediate must be stored anyway (training: the backward's filter gradient
+      // reads it) fusion saves only its re-read, and the two stencil launches stream at
+      // ~4.8 TB/s against ~3 TB/s for the fused tile kernel: fuse those pairs only while the
+      // intermediate is small enough for the saved launch to dominate (CP cr 0.1 layers:
+      // conv1 1.23 -> 1.15 ms; R = 275 @56: 376 -> 432 us, not fused).  CE_FUSE_MAX_MB.
+      static const double max_mb = [] {
+        const char* e = std::getenv("CE_FUSE_MAX_MB");
+        return e ? std::atof(e) : 96.0;
+      }();
+      if (write_mid && 4.0 * operand_elems(si.desc.p, 2) > max_mb * 1048576.0) break;
+      CeDw2Desc d{};
+      if (!ce_dw2_plan(si.desc.p, sj.desc.p, write_mid, &d)) break;
+      Step f = si;
+      f.kind = Step::kDw2;
+      f.dw2 = d;
+      f.b2 = sj.b;
+      f.c2 = sj.c;
+      if (!write_mid) f.c = BufRef{};
+      f.flops = si.flops + sj.flops;
+      f.bytes = problem_bytes(sj.desc.p) - 4.0 * operand_elems(sj.desc.p, 0) + 4.0 * operand_elems(si.desc.p, 0) +
+                (write_mid ? 4.0 * operand_elems(si.desc.p, 2) : 0.0);
+      f.label = si.label + "+" + sj.label;
+      list[i] = f;
+      list.erase(list.begin() + static_cast<std::ptrdiff_t>(j));
+      break;
+    }
+  }
+}
+
 void Executor::build_forward() {
   const auto& spec = plan_.spec;
   const View out_view = dense_view(spec.output, output_dims());
@@ -912,7 +1104,7 @@ float* Executor::resolve(const BufRef& r) const {
   switch (r.kind) {
     case BufRef::kInput: return const_cast<float*>(inputs_[r.index]);
     case BufRef::kOutput: return out_;
-    case BufRef::kWork: return reinterpret_cast<float*>(ws_ + r.index);
+    case BufRef::kWork: return reinterpret_cast<float*>(ws_ + buf_off_[static_cast<std::size_t>(r.index)]);
     case BufRef::kDOut: return const_cast<float*>(dout_);
     case BufRef::kDInput: return r.index < static_cast<int64_t>(dinputs_.size()) ? dinputs_[r.index] : nullptr;
     default: return nullptr;
@@ -920,7 +1112,7 @@ float* Executor::resolve(const BufRef& r) const {
 }
 
 std::string Executor::describe() const {
-  static const char* kinds[] = {"direct", "tiled", "tc", "zero", "reduce", "permute"};
+  static const char* kinds[] = {"direct", "tiled", "tc", "zero", "reduce", "permute", "dw2"};
   std::string out;
   char line[512];
   for (const auto* list : {&fwd_, &bwd_})
@@ -948,6 +1140,9 @@ std::string Executor::describe() const {
           }
           std::snprintf(line + n, sizeof line - n, "%s\n", u.c_str());
         }
+      } else if (st.kind == Step::kDw2) {
+        std::snprintf(line + n, sizeof line - n, " fused taps=%d J=%d signs=%d,%d store_mid=%d\n", st.dw2.KT, st.dw2.J,
+                      st.dw2.SA, st.dw2.SB, st.dw2.write_mid);
       } else if (st.kind == Step::kPermute) {
         char pd[256];
         ce_permute_describe(st.desc.p, pd, sizeof pd);
@@ -983,7 +1178,7 @@ void Executor::run(std::vector<Step>& steps, const std::vector<char>* need, cuda
   for (Step& st : steps) {
     st.ran = false;
     if (need && st.node >= 0 && !(*need)[static_cast<std::size_t>(st.node)]) continue;
-    if (!resolve(st.c)) continue;  // gradient not requested
+    if (!resolve(st.kind == Step::kDw2 ? st.c2 : st.c)) continue;  // gradient not requested
     st.ran = true;
     launch_step(st, s);
   }
@@ -1008,7 +1203,7 @@ void Executor::run_concurrent(std::vector<Step>& steps, const std::vector<char>*
     Step& st = steps[i];
     st.ran = false;
     if (need && st.node >= 0 && !(*need)[static_cast<std::size_t>(st.node)]) continue;
-    if (!resolve(st.c)) continue;
+    if (!resolve(st.kind == Step::kDw2 ? st.c2 : st.c)) continue;
     st.ran = true;
     if (!st.done) cuda_check(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming), "cudaEventCreate");
     // continue the chain of a dependency when it is the last step of its stream,
@@ -1085,6 +1280,7 @@ void Executor::launch_step(Step& st, cudaStream_t s) {
       case Step::kZero: e = cudaMemsetAsync(C, 0, static_cast<size_t>(st.zero_elems) * 4, s); break;
       case Step::kReduce: e = ce_launch_reduce(exact(st), A, B, C, st.zero_elems, s); break;
       case Step::kPermute: e = ce_launch_permute(st.desc.p, A, C, s); break;
+      case Step::kDw2: e = ce_launch_dw2(st.dw2, A, B, resolve(st.b2), C, resolve(st.c2), s); break;
     }
     cuda_check(e, st.label.c_str());
     if (profiling_) cuda_check(cudaEventRecordWithFlags(st.ev1, s, cudaEventRecordExternal), "cudaEventRecord");

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../cuda/ce_device.h"
+#include "../cuda/ce_fuse.h"
 #include "../cuda/ce_tc.h"
 #include "ce_lower.hpp"
 #include "ce_plan.hpp"
@@ -20,15 +21,19 @@ namespace ce {
 
 struct BufRef {
   enum Kind { kNone, kInput, kOutput, kWork, kDOut, kDInput } kind = kNone;
-  int64_t index = 0;  // input index or workspace offset (bytes)
+  int64_t index = 0;  // input index, or workspace buffer id (its offset is assigned by liveness)
 };
 
 struct Step {
-  enum Kind { kDirect, kTiled, kTc, kZero, kReduce, kPermute } kind = kDirect;
+  enum Kind { kDirect, kTiled, kTc, kZero, kReduce, kPermute, kDw2 } kind = kDirect;
   CeSimtDesc desc{};
   int a_kfast = 0, b_kfast = 0;
   TcPlan tc{};
   BufRef a, b, c;
+  // kDw2 (two chained depthwise stencils, ce_fuse.h): a -(b)-> c (stored only when read
+  // later; else kNone) -(b2)-> c2
+  CeDw2Desc dw2{};
+  BufRef b2, c2;
   int64_t zero_elems = 0;
   double flops = 0;   // algorithmic FLOPs (2 x flops_actual of the node / adjoint)
   double bytes = 0;   // compulsory bytes (|A| + |B| + |C|) x 4
@@ -56,6 +61,8 @@ class Executor {
 
   const EvaluationPlan& plan() const { return plan_; }
   int64_t workspace_bytes() const { return ws_bytes_; }
+  // bytes a bump allocator (every buffer alive for the whole executor) would need
+  int64_t workspace_bytes_unshared() const { return ws_unshared_; }
   int last_launches() const { return last_launches_; }
   int tc_steps(bool bwd) const;
   const std::vector<Step>& forward_steps() const { return fwd_; }
@@ -83,7 +90,10 @@ class Executor {
   void run(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s);
   void run_concurrent(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s);
   void launch_step(Step& st, cudaStream_t s);
-  static void compute_deps(std::vector<Step>& steps);
+  void compute_deps(std::vector<Step>& steps) const;
+  void assign_offsets();
+  void fuse_chains(std::vector<Step>& list);
+  bool overlap(const BufRef& x, const BufRef& y) const;
   float* resolve(const BufRef& r) const;
 
   EvaluationPlan plan_;
@@ -96,7 +106,9 @@ class Executor {
   std::vector<View> red_view_[2];  // per node, post-self-sum view of left/right
   std::vector<BufRef> red_ref_[2];
   std::vector<Step> fwd_, bwd_;
-  int64_t ws_bytes_ = 0;
+  int64_t ws_bytes_ = 0, ws_unshared_ = 0;
+  std::vector<int64_t> buf_bytes_, buf_off_;  // per workspace buffer id
+  int ws_reuse_mode_ = 0;
   char* ws_ = nullptr;
   // bound per call
   std::vector<const float*> inputs_;

@@ -1,0 +1,44 @@
+"""Liveness-based workspace reuse: the executor's arena holds a buffer only
+from its first to its last step (the reference keeps every intermediate alive,
+sequencer.cpp:421-433).  Host-only: the step list and arena sizes come from the plan
+compiler, no device needed.  Correctness of the shared arena on the device is covered by
+every -m gpu parity test (they run with reuse on, the default)."""
+import pytest
+
+import paper_2401_03384_b200 as ce
+
+
+def _ws(kind, tf, sf, k, hp, batch, cr):
+    slots = {"cp": 1, "tk": 2, "tt": 3, "tr": 4, "rtr": 4}[kind]
+    le = ce.expression(ce.LayerSpec(kind, tf, sf, k, k, hp, hp, batch, [1] * slots), cr)
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    lines = plan.describe_steps(True, "auto").splitlines()
+    vals = {l.split()[0]: int(l.split()[1]) for l in lines if l.startswith("workspace_bytes")}
+    return vals["workspace_bytes"], vals["workspace_bytes_unshared"]
+
+
+@pytest.mark.parametrize("case,frac", [
+    # above CE_WS_TIGHT_GB (16 GB unshared): buffers share across the whole step timeline
+    (("rtr", [4, 4, 8], [4, 4, 4], 3, 28, 256, 0.1), 0.5),   # cfg3 64->128 @28, B=256: 54 -> 22 GB
+    # below it: sharing only along the passes' happens-before order (no new synchronisation)
+    (("rtr", [4, 4, 4], [1, 1, 3], 7, 112, 256, 0.1), 0.8),  # cfg3 conv1
+    (("rtr", [4, 4, 4], [4, 4, 4], 3, 56, 256, 0.1), 0.8),   # cfg3 64->64 @56
+    (("tt", [256], [256], 3, 14, 128, 1.0), 0.8),             # cfg2 TT cr 1.0
+])
+def test_workspace_shrinks_by_liveness(case, frac):
+    shared, unshared = _ws(*case)
+    assert 0 < shared <= frac * unshared, (case, shared, unshared)
+
+
+def test_workspace_never_exceeds_bump_layout():
+    for case in [("cp", [64], [64], 3, 32, 8, None), ("tk", [256], [256], 3, 14, 128, 0.1),
+                 ("tr", [256], [256], 3, 14, 128, 0.5)]:
+        kind, tf, sf, k, hp, b, cr = case
+        if cr is None:
+            le = ce.expression(ce.LayerSpec(kind, tf, sf, k, k, hp, hp, b, [16]))
+        else:
+            le = ce.expression(ce.LayerSpec(kind, tf, sf, k, k, hp, hp, b, [1] * {"cp": 1, "tk": 2, "tr": 4}[kind]), cr)
+        plan = ce.optimal(le.expr, le.dims, "same", "training")
+        lines = plan.describe_steps(True, "auto").splitlines()
+        vals = {l.split()[0]: int(l.split()[1]) for l in lines if l.startswith("workspace_bytes")}
+        assert vals["workspace_bytes"] <= vals["workspace_bytes_unshared"]

@@ -91,69 +91,76 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "configs_r01.json"))
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--quick", action="store_true", help="fewer cfg5 points")
+    ap.add_argument("--only", default="cfg1,cfg2,cfg3,cfg4,cfg5", help="comma-separated subset of configs")
     args = ap.parse_args()
+    only = set(args.only.split(","))
     ctx = Context(0, "auto")
     torch.cuda.set_stream(ctx.torch_stream)
     flush = torch.empty(64 * 1024 * 1024, device="cuda")
     res = {"device": torch.cuda.get_device_name(0), "timestamp": time.time(), "l2": "flushed before each iteration"}
 
     # cfg1
-    le = ce.expression(ce.LayerSpec("cp", [64], [64], 3, 3, 32, 32, 8, [16]))
-    res["cfg1"] = {"forward": time_layer(ctx, le, False, 20, flush), "fwd_bwd": time_layer(ctx, le, True, 20, flush),
-                   "cpu_reference_forward": cpu_forward(le)}
-    print("cfg1", res["cfg1"]["forward"]["ms"], flush=True)
+    if "cfg1" in only:
+        le = ce.expression(ce.LayerSpec("cp", [64], [64], 3, 3, 32, 32, 8, [16]))
+        res["cfg1"] = {"forward": time_layer(ctx, le, False, 20, flush), "fwd_bwd": time_layer(ctx, le, True, 20, flush),
+                       "cpu_reference_forward": cpu_forward(le)}
+        print("cfg1", res["cfg1"]["forward"]["ms"], flush=True)
 
     # cfg2
-    res["cfg2"] = {}
-    for kind, cr in [("tk", 0.1), ("tk", 0.25), ("tk", 1.0), ("tt", 0.1), ("tt", 0.25), ("tt", 1.0)]:
-        slots = {"tk": 2, "tt": 3}[kind]
-        le = ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, 128, [1] * slots), cr)
-        res["cfg2"][f"{kind}_cr{cr}"] = time_layer(ctx, le, True, args.iters, flush)
-        print("cfg2", kind, cr, res["cfg2"][f"{kind}_cr{cr}"]["ms"], flush=True)
+    if "cfg2" in only:
+        res["cfg2"] = {}
+        for kind, cr in [("tk", 0.1), ("tk", 0.25), ("tk", 1.0), ("tt", 0.1), ("tt", 0.25), ("tt", 1.0)]:
+            slots = {"tk": 2, "tt": 3}[kind]
+            le = ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, 128, [1] * slots), cr)
+            res["cfg2"][f"{kind}_cr{cr}"] = time_layer(ctx, le, True, args.iters, flush)
+            print("cfg2", kind, cr, res["cfg2"][f"{kind}_cr{cr}"]["ms"], flush=True)
 
     # cfg3: RTR stack, batch 256, cr 0.1
-    layers, tot_ms, tot_fl = [], 0.0, 0.0
-    for s, t, k, hp, count in RESNET34:
-        le = ce.expression(ce.LayerSpec("rtr", RTR_FACT[t], RTR_FACT[s], k, k, hp, hp, 256, [1, 1, 1, 1]), 0.1)
-        r = time_layer(ctx, le, True, args.iters, flush)
-        r.update({"S": s, "T": t, "k": k, "Hp": hp, "count": count})
-        layers.append(r)
-        tot_ms += count * r["ms"]
-        tot_fl += count * r["flops"]
-        print("cfg3", s, t, hp, r["ms"], flush=True)
-        torch.cuda.empty_cache()
-    res["cfg3"] = {"batch": 256, "cr": 0.1, "layers": layers, "stack_fwd_bwd_ms": round(tot_ms, 3),
-                   "stack_tflops": round(tot_fl / (tot_ms * 1e-3) / 1e12, 2)}
-
-    # cfg4: CP stack, per-GPU batch 128
-    res["cfg4"] = {}
-    for cr in (0.1, 1.0):
+    if "cfg3" in only:
         layers, tot_ms, tot_fl = [], 0.0, 0.0
         for s, t, k, hp, count in RESNET34:
-            le = ce.expression(ce.LayerSpec("cp", [t], [s], k, k, hp, hp, 128, [1]), cr)
+            le = ce.expression(ce.LayerSpec("rtr", RTR_FACT[t], RTR_FACT[s], k, k, hp, hp, 256, [1, 1, 1, 1]), 0.1)
             r = time_layer(ctx, le, True, args.iters, flush)
             r.update({"S": s, "T": t, "k": k, "Hp": hp, "count": count})
             layers.append(r)
             tot_ms += count * r["ms"]
             tot_fl += count * r["flops"]
+            print("cfg3", s, t, hp, r["ms"], flush=True)
             torch.cuda.empty_cache()
-        res["cfg4"][f"cr{cr}"] = {"per_gpu_batch": 128, "layers": layers, "stack_fwd_bwd_ms": round(tot_ms, 3),
-                                  "stack_tflops": round(tot_fl / (tot_ms * 1e-3) / 1e12, 2),
-                                  "images_per_s_per_gpu": round(128 / (tot_ms * 1e-3), 1)}
-        print("cfg4", cr, tot_ms, flush=True)
+        res["cfg3"] = {"batch": 256, "cr": 0.1, "layers": layers, "stack_fwd_bwd_ms": round(tot_ms, 3),
+                       "stack_tflops": round(tot_fl / (tot_ms * 1e-3) / 1e12, 2)}
+
+    # cfg4: CP stack, per-GPU batch 128
+    if "cfg4" in only:
+        res["cfg4"] = {}
+        for cr in (0.1, 1.0):
+            layers, tot_ms, tot_fl = [], 0.0, 0.0
+            for s, t, k, hp, count in RESNET34:
+                le = ce.expression(ce.LayerSpec("cp", [t], [s], k, k, hp, hp, 128, [1]), cr)
+                r = time_layer(ctx, le, True, args.iters, flush)
+                r.update({"S": s, "T": t, "k": k, "Hp": hp, "count": count})
+                layers.append(r)
+                tot_ms += count * r["ms"]
+                tot_fl += count * r["flops"]
+                torch.cuda.empty_cache()
+            res["cfg4"][f"cr{cr}"] = {"per_gpu_batch": 128, "layers": layers, "stack_fwd_bwd_ms": round(tot_ms, 3),
+                                      "stack_tflops": round(tot_fl / (tot_ms * 1e-3) / 1e12, 2),
+                                      "images_per_s_per_gpu": round(128 / (tot_ms * 1e-3), 1)}
+            print("cfg4", cr, tot_ms, flush=True)
 
     # cfg5: compression sweep + dense
-    crs = [0.05, 0.1, 0.5] if args.quick else [0.05, 0.1, 0.2, 0.3, 0.4, 0.5]
-    sweep = {}
-    for kind in ("cp", "tk", "tt", "tr"):
-        slots = {"cp": 1, "tk": 2, "tt": 3, "tr": 4}[kind]
-        for cr in crs:
-            le = ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, 128, [1] * slots), cr)
-            sweep[f"{kind}_cr{cr}"] = time_layer(ctx, le, True, args.iters, flush)
-    le = ce.expression(ce.LayerSpec("standard", [256], [256], 3, 3, 14, 14, 128, []))
-    sweep["dense"] = time_layer(ctx, le, True, args.iters, flush)
-    res["cfg5"] = sweep
-    print("cfg5 dense", sweep["dense"]["ms"], flush=True)
+    if "cfg5" in only:
+        crs = [0.05, 0.1, 0.5] if args.quick else [0.05, 0.1, 0.2, 0.3, 0.4, 0.5]
+        sweep = {}
+        for kind in ("cp", "tk", "tt", "tr"):
+            slots = {"cp": 1, "tk": 2, "tt": 3, "tr": 4}[kind]
+            for cr in crs:
+                le = ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, 128, [1] * slots), cr)
+                sweep[f"{kind}_cr{cr}"] = time_layer(ctx, le, True, args.iters, flush)
+        le = ce.expression(ce.LayerSpec("standard", [256], [256], 3, 3, 14, 14, 128, []))
+        sweep["dense"] = time_layer(ctx, le, True, args.iters, flush)
+        res["cfg5"] = sweep
+        print("cfg5 dense", sweep["dense"]["ms"], flush=True)
 
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
