@@ -137,6 +137,13 @@ void ce_ctx_destroy(ce_ctx* ctx);
 void* ce_ctx_stream(ce_ctx* ctx); /* the cudaStream_t all work of this ctx is ordered on */
 ce_status ce_ctx_synchronize(ce_ctx* ctx);
 
+/* Device memory for callers without their own CUDA runtime (the CLI, FFI bindings):
+ * cudaMalloc / cudaFree on the ctx's device, and stream-ordered copies on the ctx stream
+ * (ce_ctx_memcpy returns once the copy completed). */
+ce_status ce_ctx_alloc(ce_ctx* ctx, size_t bytes, void** out);
+ce_status ce_ctx_free(ce_ctx* ctx, void* p);
+ce_status ce_ctx_memcpy(ce_ctx* ctx, void* dst, const void* src, size_t bytes); /* any direction (UVA) */
+
 /* Device SplitMix64 fill (tensor.cpp:107-130): dst[i] = (float) fill_random(seed)[i]. */
 ce_status ce_fill_random(ce_ctx* ctx, float* dst, int64_t n, uint64_t seed);
 
@@ -172,6 +179,34 @@ ce_status ce_executor_profile(ce_executor* ex, int backward, int max_steps, int*
                               size_t labels_cap, int* kinds, float* ms, double* flops, double* bytes);
 /* Host-buffer convenience (e2e path): H2D copy, execute, D2H copy, synchronize. */
 ce_status ce_execute_host(ce_executor* ex, const float* const* host_inputs, float* host_out);
+
+/* ------------------------------------------------------------ wire formats - */
+/* The reference's serialisations, FP64 on the wire like DenseTensor
+ * (tensor.hpp:24-36).  *_len / *count receive the required size even when the buffer is
+ * too small (then CE_ERR_OTHER), so a NULL/0 call queries it.
+ * tensor_to_json (tensor.cpp:132-137): {"data":[...],"shape":[...]}, numbers as nlohmann's
+ * dump() prints them (shortest round trip). */
+ce_status ce_tensor_to_json(const int64_t* shape, int rank, const double* data, char* buf, size_t cap,
+                            size_t* len_out);
+/* tensor_from_json (tensor.cpp:139-147): CE_ERR_PARSE on malformed text, CE_ERR_SHAPE when
+ * the data length does not match the shape. */
+ce_status ce_tensor_from_json(const char* text, int64_t* shape, int shape_cap, int* rank, double* data,
+                              int64_t data_cap, int64_t* count);
+/* tensor_write_binary / tensor_read_binary (tensor.cpp:149-186): little-endian u64 rank,
+ * u64 dims, f64 payload; CE_ERR_SHAPE on a truncated stream. */
+ce_status ce_tensor_to_binary(const int64_t* shape, int rank, const double* data, unsigned char* buf, size_t cap,
+                              size_t* len_out);
+ce_status ce_tensor_from_binary(const unsigned char* bytes, size_t len, int64_t* shape, int shape_cap, int* rank,
+                                double* data, int64_t data_cap, int64_t* count);
+/* layer_to_json / layer_from_json (layers.cpp:425-467).  ce_layer_from_json fills kind,
+ * T / S factors (CE_MAX_LAYER_RANKS entries each), hw = {H, W, Hp, Wp, B} and the ranks
+ * (a scalar "rank" is broadcast to every slot, as the reference does); validate() errors
+ * (layers.cpp) come back as CE_ERR_SHAPE. */
+ce_status ce_layer_to_json(const char* kind, const int64_t* t_factors, int n_t, const int64_t* s_factors, int n_s,
+                           int64_t filter_h, int64_t filter_w, int64_t feature_h, int64_t feature_w, int64_t batch,
+                           const int64_t* ranks, int n_ranks, char* buf, size_t cap);
+ce_status ce_layer_from_json(const char* text, char* kind, size_t kind_cap, int64_t* t_factors, int* n_t,
+                             int64_t* s_factors, int* n_s, int64_t* hw5, int64_t* ranks, int* n_ranks);
 
 /* ------------------------------------------------------------ pairwise ----- */
 /* pairwise_eval (kernels.cpp:425-470) for the op make_pairwise_op builds from

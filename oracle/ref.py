@@ -187,3 +187,39 @@ def parse(expr):
     _check(lib().ref_parse(expr.encode(), out, len(out)))
     r, cls = out.value.decode().split("\n")
     return r, dict(x.split(":") for x in cls.split()) if cls else {}
+
+
+def tensor_to_json(arr):
+    a = np.ascontiguousarray(arr, dtype=np.float64)
+    shp = (ctypes.c_int64 * max(1, a.ndim))(*a.shape)
+    out = _buf(max(1 << 16, 32 * a.size + 256))
+    _check(lib().ref_tensor_to_json(shp, a.ndim, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), out, len(out)))
+    return out.value.decode()
+
+
+def tensor_from_json(text):
+    shp = (ctypes.c_int64 * 64)()
+    rank = ctypes.c_int()
+    cnt = ctypes.c_int64()
+    data = np.zeros(max(1, len(text)), dtype=np.float64)
+    _check(lib().ref_tensor_from_json(text.encode(), shp, ctypes.byref(rank),
+                                      data.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.c_int64(data.size),
+                                      ctypes.byref(cnt)))
+    return data[:cnt.value].reshape([shp[i] for i in range(rank.value)])
+
+
+def tensor_to_binary(arr):
+    a = np.ascontiguousarray(arr, dtype=np.float64)
+    shp = (ctypes.c_int64 * max(1, a.ndim))(*a.shape)
+    cap = 8 * (1 + a.ndim + a.size)
+    out = ctypes.create_string_buffer(cap)
+    ln = ctypes.c_int64()
+    _check(lib().ref_tensor_to_binary(shp, a.ndim, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), out,
+                                      ctypes.c_int64(cap), ctypes.byref(ln)))
+    return out.raw[:ln.value]
+
+
+def layer_json_roundtrip(layer_json):
+    out = _buf(1 << 12)
+    _check(lib().ref_layer_json_roundtrip(layer_json.encode(), out, len(out)))
+    return out.value.decode()

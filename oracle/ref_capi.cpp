@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <exception>
 #include <string>
 #include <vector>
@@ -307,6 +308,44 @@ int ref_parse(const char* expr, char* out, int cap) {
     }
     put(s, out, cap);
   });
+}
+
+// Wire formats (tensor.cpp:132-186, layers.cpp:425-467), for the F3 parity tests.
+int ref_tensor_to_json(const int64_t* shape, int rank, const double* data, char* out, int cap) {
+  return guard([&] {
+    DenseTensor t(std::vector<int64_t>(shape, shape + rank));
+    std::memcpy(t.data.data(), data, sizeof(double) * t.data.size());
+    put(tensor_to_json(t), out, cap);
+  });
+}
+
+int ref_tensor_from_json(const char* text, int64_t* shape, int* rank, double* data, int64_t cap, int64_t* count) {
+  return guard([&] {
+    DenseTensor t = tensor_from_json(text);
+    *rank = static_cast<int>(t.shape.size());
+    for (std::size_t i = 0; i < t.shape.size(); ++i) shape[i] = t.shape[i];
+    *count = static_cast<int64_t>(t.data.size());
+    if (*count > cap) throw std::runtime_error("data buffer too small");
+    std::memcpy(data, t.data.data(), sizeof(double) * t.data.size());
+  });
+}
+
+int ref_tensor_to_binary(const int64_t* shape, int rank, const double* data, unsigned char* out, int64_t cap,
+                         int64_t* len) {
+  return guard([&] {
+    DenseTensor t(std::vector<int64_t>(shape, shape + rank));
+    std::memcpy(t.data.data(), data, sizeof(double) * t.data.size());
+    std::ostringstream os;
+    tensor_write_binary(t, os);
+    const std::string s = os.str();
+    *len = static_cast<int64_t>(s.size());
+    if (*len > cap) throw std::runtime_error("buffer too small");
+    std::memcpy(out, s.data(), s.size());
+  });
+}
+
+int ref_layer_json_roundtrip(const char* layer_json, char* out, int cap) {
+  return guard([&] { put(layer_to_json(layer_from_json(layer_json)), out, cap); });
 }
 
 }  // extern "C"

@@ -71,6 +71,9 @@ SIGNATURES = {
     "ce_ctx_destroy": (None, [ctypes.c_void_p]),
     "ce_ctx_stream": (ctypes.c_void_p, [ctypes.c_void_p]),
     "ce_ctx_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
+    "ce_ctx_alloc": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "ce_ctx_free": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "ce_ctx_memcpy": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
     "ce_fill_random": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64]),
     "ce_executor_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "ce_executor_destroy": (None, [ctypes.c_void_p]),
@@ -95,6 +98,19 @@ SIGNATURES = {
     "ce_allreduce_grads": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), c_i64p, ctypes.c_int]),
     "ce_comm_wait": (ctypes.c_int, [ctypes.c_void_p]),
     "ce_comm_check": (ctypes.c_int, [ctypes.c_void_p]),
+    "ce_tensor_to_json": (ctypes.c_int, [c_i64p, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_char_p,
+                                         ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    "ce_tensor_from_json": (ctypes.c_int, [ctypes.c_char_p, c_i64p, ctypes.c_int, c_intp,
+                                           ctypes.POINTER(ctypes.c_double), ctypes.c_int64, c_i64p]),
+    "ce_tensor_to_binary": (ctypes.c_int, [c_i64p, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_char_p,
+                                           ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    "ce_tensor_from_binary": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, c_i64p, ctypes.c_int, c_intp,
+                                             ctypes.POINTER(ctypes.c_double), ctypes.c_int64, c_i64p]),
+    "ce_layer_to_json": (ctypes.c_int, [ctypes.c_char_p, c_i64p, ctypes.c_int, c_i64p, ctypes.c_int, ctypes.c_int64,
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, c_i64p,
+                                        ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t]),
+    "ce_layer_from_json": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t, c_i64p, c_intp, c_i64p,
+                                          c_intp, c_i64p, c_i64p, c_intp]),
 }
 
 STATUS = {0: "OK", 1: "OTHER", 2: "PARSE", 3: "SHAPE", 4: "NUMERIC", 5: "PLAN", 6: "OVERFLOW",

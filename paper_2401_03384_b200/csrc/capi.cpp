@@ -14,6 +14,7 @@
 #include "../../include/ce/ce.h"
 #include "cuda/ce_kernels.h"
 #include "host/ce_exec.hpp"
+#include "host/ce_io.hpp"
 #include "host/ce_layers.hpp"
 
 using namespace ce;
@@ -39,6 +40,15 @@ struct ce_executor {
   ce_ctx* ctx = nullptr;
   std::unique_ptr<Executor> ex;
 };
+
+// (wire formats) copy a vector to a caller buffer of `cap` entries; *count gets the size
+template <class T>
+static void fill_out(const std::vector<T>& v, T* out, int64_t cap, int64_t* count) {
+  if (count) *count = static_cast<int64_t>(v.size());
+  if (static_cast<int64_t>(v.size()) > cap || (!out && !v.empty()))
+    throw std::runtime_error("output buffer too small (need " + std::to_string(v.size()) + ")");
+  if (!v.empty()) std::memcpy(out, v.data(), v.size() * sizeof(T));
+}
 
 namespace {
 
@@ -392,6 +402,90 @@ ce_status ce_layer_expression(const char* kind, const int64_t* t_factors, int n_
   });
 }
 
+
+ce_status ce_tensor_to_json(const int64_t* shape, int rank, const double* data, char* buf, size_t cap,
+                            size_t* len_out) {
+  return guard([&] {
+    const std::string s = tensor_to_json(std::vector<int64_t>(shape, shape + rank), data);
+    if (len_out) *len_out = s.size() + 1;
+    copy_out(s, buf, cap);
+  });
+}
+
+ce_status ce_tensor_from_json(const char* text, int64_t* shape, int shape_cap, int* rank, double* data,
+                              int64_t data_cap, int64_t* count) {
+  return guard([&] {
+    std::vector<int64_t> sh;
+    std::vector<double> d;
+    tensor_from_json(text, &sh, &d);
+    int64_t r = 0;
+    fill_out(sh, shape, shape_cap, &r);
+    *rank = static_cast<int>(r);
+    fill_out(d, data, data_cap, count);
+  });
+}
+
+ce_status ce_tensor_to_binary(const int64_t* shape, int rank, const double* data, unsigned char* buf, size_t cap,
+                              size_t* len_out) {
+  return guard([&] {
+    const std::string s = tensor_to_binary(std::vector<int64_t>(shape, shape + rank), data);
+    if (len_out) *len_out = s.size();
+    if (!buf || s.size() > cap) throw std::runtime_error("output buffer too small (need " + std::to_string(s.size()) + ")");
+    std::memcpy(buf, s.data(), s.size());
+  });
+}
+
+ce_status ce_tensor_from_binary(const unsigned char* bytes, size_t len, int64_t* shape, int shape_cap, int* rank,
+                                double* data, int64_t data_cap, int64_t* count) {
+  return guard([&] {
+    std::vector<int64_t> sh;
+    std::vector<double> d;
+    tensor_from_binary(std::string(reinterpret_cast<const char*>(bytes), len), &sh, &d);
+    int64_t r = 0;
+    fill_out(sh, shape, shape_cap, &r);
+    *rank = static_cast<int>(r);
+    fill_out(d, data, data_cap, count);
+  });
+}
+
+ce_status ce_layer_to_json(const char* kind, const int64_t* t_factors, int n_t, const int64_t* s_factors, int n_s,
+                           int64_t filter_h, int64_t filter_w, int64_t feature_h, int64_t feature_w, int64_t batch,
+                           const int64_t* ranks, int n_ranks, char* buf, size_t cap) {
+  return guard([&] {
+    LayerSpec l;
+    l.kind = layer_kind_from_string(kind);
+    l.t_factors.assign(t_factors, t_factors + n_t);
+    l.s_factors.assign(s_factors, s_factors + n_s);
+    l.filter_h = filter_h;
+    l.filter_w = filter_w;
+    l.feature_h = feature_h;
+    l.feature_w = feature_w;
+    l.batch = batch;
+    l.ranks.assign(ranks, ranks + n_ranks);
+    copy_out(layer_to_json(l), buf, cap);
+  });
+}
+
+ce_status ce_layer_from_json(const char* text, char* kind, size_t kind_cap, int64_t* t_factors, int* n_t,
+                             int64_t* s_factors, int* n_s, int64_t* hw5, int64_t* ranks, int* n_ranks) {
+  return guard([&] {
+    const LayerSpec l = layer_from_json(text);
+    copy_out(to_string(l.kind), kind, kind_cap);
+    int64_t n = 0;
+    fill_out(l.t_factors, t_factors, CE_MAX_LAYER_RANKS, &n);
+    *n_t = static_cast<int>(n);
+    fill_out(l.s_factors, s_factors, CE_MAX_LAYER_RANKS, &n);
+    *n_s = static_cast<int>(n);
+    fill_out(l.ranks, ranks, CE_MAX_LAYER_RANKS, &n);
+    *n_ranks = static_cast<int>(n);
+    hw5[0] = l.filter_h;
+    hw5[1] = l.filter_w;
+    hw5[2] = l.feature_h;
+    hw5[3] = l.feature_w;
+    hw5[4] = l.batch;
+  });
+}
+
 ce_status ce_plan_describe_steps(const ce_plan* plan, int want_backward, int math, char* buf, size_t cap) {
   return guard([&] {
     ExecConfig cfg;
@@ -437,6 +531,29 @@ void* ce_ctx_stream(ce_ctx* ctx) { return ctx->stream; }
 
 ce_status ce_ctx_synchronize(ce_ctx* ctx) {
   return guard([&] { cuda_ok(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize"); });
+}
+
+ce_status ce_ctx_alloc(ce_ctx* ctx, size_t bytes, void** out) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
+    *out = nullptr;
+    cuda_ok(cudaMalloc(out, bytes ? bytes : 1), "cudaMalloc");
+  });
+}
+
+ce_status ce_ctx_free(ce_ctx* ctx, void* p) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (p) cuda_ok(cudaFree(p), "cudaFree");
+  });
+}
+
+ce_status ce_ctx_memcpy(ce_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cuda_ok(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream), "cudaMemcpyAsync");
+    cuda_ok(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+  });
 }
 
 ce_status ce_fill_random(ce_ctx* ctx, float* dst, int64_t n, uint64_t seed) {
