@@ -103,6 +103,7 @@ ce_status ce_plan_node(const ce_plan* plan, int node, int* left, int* right, cha
  * one line per step "fwd|bwd label kind details", then "workspace_bytes N" (liveness-
  * shared arena) and "workspace_bytes_unshared N" (every buffer alive throughout). */
 ce_status ce_plan_describe_steps(const ce_plan* plan, int want_backward, int math, char* buf, size_t cap);
+/* (want_backward takes the same CE_EXEC_RECOMPUTE flag as ce_executor_create) */
 
 /* ----------------------------------------------------------------- layers -- */
 #define CE_MAX_LAYER_INPUTS 32 /* capacity of ranks_of_input[] (entries) */
@@ -158,7 +159,14 @@ typedef struct {
 } ce_exec_stats;
 
 /* Binds a plan to a context and sizes its workspace (intermediates, packed
- * operands and, with want_backward, gradient buffers). */
+ * operands and, with want_backward, gradient buffers).  want_backward: 0, 1, or
+ * 1 | CE_EXEC_RECOMPUTE: gradient checkpointing -- execute keeps no
+ * intermediates for the backward pass, ce_backward recomputes them first (one more forward's
+ * work, a smaller workspace, and no need for a preceding ce_execute). */
+#define CE_EXEC_RECOMPUTE 0x100
+/* Bytes of the arena a context shares among its CE_EXEC_RECOMPUTE executors (the largest
+ * workspace of any of them bound so far; executors that keep intermediates own theirs). */
+ce_status ce_ctx_workspace_bytes(ce_ctx* ctx, size_t* bytes);
 ce_status ce_executor_create(ce_ctx* ctx, const ce_plan* plan, int want_backward, ce_executor** out);
 void ce_executor_destroy(ce_executor* ex);
 /* execute (sequencer.cpp:403-447): inputs[i] device FP32 dense in spec.inputs[i]

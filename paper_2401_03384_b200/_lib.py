@@ -71,6 +71,7 @@ SIGNATURES = {
     "ce_ctx_destroy": (None, [ctypes.c_void_p]),
     "ce_ctx_stream": (ctypes.c_void_p, [ctypes.c_void_p]),
     "ce_ctx_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
+    "ce_ctx_workspace_bytes": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t)]),
     "ce_ctx_alloc": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "ce_ctx_free": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "ce_ctx_memcpy": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),

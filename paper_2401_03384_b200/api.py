@@ -23,6 +23,9 @@ from ._lib import CeError, ParseError, PlanError, ShapeError, check, lib  # noqa
 MODES = ("full", "same", "valid", "circular")
 
 
+CE_EXEC_RECOMPUTE = 0x100  # include/ce/ce.h: gradient checkpointing flag of want_backward
+
+
 def _dims_arg(dims: Sequence[Sequence[int]]):
     flat = [int(d) for ds in dims for d in ds]
     ranks = [len(ds) for ds in dims]
@@ -133,10 +136,11 @@ class Plan:
         check(lib().ce_plan_tree_encoding(self._h, buf, len(buf)))
         return buf.value.decode()
 
-    def describe_steps(self, backward: bool = False, math: str = "auto") -> str:
+    def describe_steps(self, backward: bool = False, math: str = "auto", recompute: bool = False) -> str:
         """Kernel steps the device executor compiles this plan into (no GPU needed)."""
         buf = ctypes.create_string_buffer(1 << 20)
-        check(lib().ce_plan_describe_steps(self._h, int(backward), 0 if math in ("auto", "tf32") else 1, buf, len(buf)))
+        wb = int(backward) | (CE_EXEC_RECOMPUTE if recompute else 0)
+        check(lib().ce_plan_describe_steps(self._h, wb, 0 if math in ("auto", "tf32") else 1, buf, len(buf)))
         return buf.value.decode()
 
     def nodes(self):

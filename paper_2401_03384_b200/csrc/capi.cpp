@@ -34,6 +34,10 @@ struct ce_ctx {
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t comm_in = nullptr, comm_out = nullptr;
+  // arena shared by the context's recompute executors (they keep nothing between calls, and
+  // every call is ordered on the ctx stream): sized to the largest of them
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
 };
 
 struct ce_executor {
@@ -490,7 +494,8 @@ ce_status ce_plan_describe_steps(const ce_plan* plan, int want_backward, int mat
   return guard([&] {
     ExecConfig cfg;
     cfg.math = math;
-    Executor ex(plan->plan, want_backward != 0, cfg);
+    cfg.recompute = (want_backward & CE_EXEC_RECOMPUTE) != 0;
+    Executor ex(plan->plan, (want_backward & ~CE_EXEC_RECOMPUTE) != 0, cfg);
     copy_out(ex.describe() + "workspace_bytes " + std::to_string(ex.workspace_bytes()) + "\n" +
                  "workspace_bytes_unshared " + std::to_string(ex.workspace_bytes_unshared()) + "\n",
              buf, cap);
@@ -522,6 +527,10 @@ void ce_ctx_destroy(ce_ctx* ctx) {
     cudaStreamDestroy(ctx->comm_stream);
     cudaEventDestroy(ctx->comm_in);
     cudaEventDestroy(ctx->comm_out);
+  }
+  if (ctx->arena) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->arena);
   }
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -570,7 +579,8 @@ ce_status ce_executor_create(ce_ctx* ctx, const ce_plan* plan, int want_backward
     e->ctx = ctx;
     ExecConfig cfg;
     cfg.math = ctx->opts.math;
-    e->ex = std::make_unique<Executor>(plan->plan, want_backward != 0, cfg);
+    cfg.recompute = (want_backward & CE_EXEC_RECOMPUTE) != 0;
+    e->ex = std::make_unique<Executor>(plan->plan, (want_backward & ~CE_EXEC_RECOMPUTE) != 0, cfg);
     e->ex->set_use_graphs(ctx->opts.use_graphs != 0);
     *out = e.release();
   });
@@ -578,9 +588,35 @@ ce_status ce_executor_create(ce_ctx* ctx, const ce_plan* plan, int want_backward
 
 void ce_executor_destroy(ce_executor* ex) { delete ex; }
 
+namespace {
+// recompute executors run on the context's shared arena (grown, after a stream sync, when a
+// larger one is bound)
+void bind_shared_arena(ce_executor* ex) {
+  if (!ex->ex->recompute()) return;
+  ce_ctx* c = ex->ctx;
+  const size_t need = static_cast<size_t>(ex->ex->workspace_bytes());
+  if (need > c->arena_bytes) {
+    if (c->arena) {
+      cuda_ok(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+      cuda_ok(cudaFree(c->arena), "cudaFree");
+      c->arena = nullptr;
+      c->arena_bytes = 0;
+    }
+    cuda_ok(cudaMalloc(reinterpret_cast<void**>(&c->arena), need), "cudaMalloc(shared arena)");
+    c->arena_bytes = need;
+  }
+  ex->ex->bind_workspace(c->arena);
+}
+}  // namespace
+
+ce_status ce_ctx_workspace_bytes(ce_ctx* ctx, size_t* bytes) {
+  return guard([&] { *bytes = ctx->arena_bytes; });
+}
+
 ce_status ce_execute(ce_executor* ex, const float* const* inputs, float* out, ce_exec_stats* stats) {
   return guard([&] {
     cuda_ok(cudaSetDevice(ex->ctx->device), "cudaSetDevice");
+    bind_shared_arena(ex);
     ex->ex->forward(inputs, out, ex->ctx->stream);
     fill_stats(*ex->ex, stats, false);
   });
@@ -590,6 +626,7 @@ ce_status ce_backward(ce_executor* ex, const float* const* inputs, const float* 
                       ce_exec_stats* stats) {
   return guard([&] {
     cuda_ok(cudaSetDevice(ex->ctx->device), "cudaSetDevice");
+    bind_shared_arena(ex);
     ex->ex->backward(inputs, dout, dinputs, ex->ctx->stream);
     fill_stats(*ex->ex, stats, true);
   });
@@ -631,6 +668,7 @@ ce_status ce_execute_host(ce_executor* ex, const float* const* host_inputs, floa
     const size_t obytes = static_cast<size_t>(element_count(ex->ex->output_dims())) * 4;
     float* dout = nullptr;
     cuda_ok(cudaMallocAsync(&dout, obytes, s), "cudaMallocAsync");
+    bind_shared_arena(ex);
     ex->ex->forward(dev.data(), dout, s);
     cuda_ok(cudaMemcpyAsync(host_out, dout, obytes, cudaMemcpyDeviceToHost, s), "D2H");
     for (float* d : dev) cudaFreeAsync(d, s);

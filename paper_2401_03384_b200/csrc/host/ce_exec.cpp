@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <stdexcept>
 
@@ -52,6 +53,9 @@ Executor::Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cf
     const char* e = std::getenv("CE_FUSE");
     return !(e && *e == '0');
   }();
+  // (recompute first: the forward pass's intermediates are then read by no backward step,
+  // so a fused forward pair need not store its intermediate)
+  if (want_backward_ && cfg_.recompute) add_recompute();
   if (fuse_on && cfg_.math == 0) {
     fuse_chains(fwd_);
     fuse_chains(bwd_);
@@ -1005,6 +1009,38 @@ void Executor::fuse_chains(std::vector<Step>& list) {
   }
 }
 
+// Gradient checkpointing: the backward pass starts by re-running every
+// forward step that writes workspace (the node results and repacks its steps read; the root
+// node writes the caller's output and is skipped) into fresh buffers, and every backward
+// reference to a forward-written buffer is redirected to its recomputed twin.  The forward
+// pass's buffers then die with the forward pass (assign_offsets shares their memory with the
+// backward's), and backward() no longer depends on a preceding forward().
+void Executor::add_recompute() {
+  std::map<int64_t, int64_t> twin;  // forward-written workspace buffer id -> backward copy
+  for (const Step& st : fwd_)
+    for (const BufRef* w : {&st.c, &st.c2})
+      if (w->kind == BufRef::kWork && !twin.count(w->index)) {
+        twin[w->index] = static_cast<int64_t>(buf_bytes_.size());
+        buf_bytes_.push_back(buf_bytes_[static_cast<std::size_t>(w->index)]);
+      }
+  auto remap = [&](Step& st) {
+    for (BufRef* r : {&st.a, &st.b, &st.c, &st.b2, &st.c2})
+      if (r->kind == BufRef::kWork && twin.count(r->index)) r->index = twin[r->index];
+  };
+  std::vector<Step> pre;
+  for (const Step& st : fwd_) {
+    if (st.c.kind != BufRef::kWork && st.c2.kind != BufRef::kWork) continue;
+    Step r = st;
+    r.node = -1;  // always runs (node ids of backward steps index operand gradients)
+    r.label = "recompute:" + st.label;
+    r.ev0 = r.ev1 = r.done = nullptr;
+    remap(r);
+    pre.push_back(r);
+  }
+  for (Step& st : bwd_) remap(st);
+  bwd_.insert(bwd_.begin(), pre.begin(), pre.end());
+}
+
 void Executor::build_forward() {
   const auto& spec = plan_.spec;
   const View out_view = dense_view(spec.output, output_dims());
@@ -1104,7 +1140,8 @@ float* Executor::resolve(const BufRef& r) const {
   switch (r.kind) {
     case BufRef::kInput: return const_cast<float*>(inputs_[r.index]);
     case BufRef::kOutput: return out_;
-    case BufRef::kWork: return reinterpret_cast<float*>(ws_ + buf_off_[static_cast<std::size_t>(r.index)]);
+    case BufRef::kWork:
+      return reinterpret_cast<float*>((ext_ws_ ? ext_ws_ : ws_) + buf_off_[static_cast<std::size_t>(r.index)]);
     case BufRef::kDOut: return const_cast<float*>(dout_);
     case BufRef::kDInput: return r.index < static_cast<int64_t>(dinputs_.size()) ? dinputs_[r.index] : nullptr;
     default: return nullptr;
@@ -1161,7 +1198,7 @@ std::string Executor::describe() const {
 }
 
 void Executor::ensure_workspace() {
-  if (!ws_ && ws_bytes_ > 0) cuda_check(cudaMalloc(&ws_, static_cast<size_t>(ws_bytes_)), "cudaMalloc(workspace)");
+  if (!ext_ws_ && !ws_ && ws_bytes_ > 0) cuda_check(cudaMalloc(&ws_, static_cast<size_t>(ws_bytes_)), "cudaMalloc(workspace)");
 }
 
 int Executor::tc_steps(bool bwd) const {
@@ -1326,12 +1363,14 @@ void Executor::forward(const float* const* inputs, float* out, cudaStream_t s) {
 void Executor::backward(const float* const* inputs, const float* dout, float* const* dinputs, cudaStream_t s) {
   if (!want_backward_) throw std::runtime_error("executor was created without backward support");
   // the backward reads the intermediates (and repacked inputs) the preceding forward left in
-  // the workspace: it must have run on these very input buffers
-  if (!fwd_ran_) throw std::runtime_error("backward: no forward has run on this executor");
-  for (int i = 0; i < n_; ++i)
-    if (fwd_inputs_[static_cast<std::size_t>(i)] != inputs[i])
-      throw std::runtime_error("backward: input " + std::to_string(i) +
-                               " is not the buffer the last forward ran on (run forward on these inputs first)");
+  // the workspace: it must have run on these very input buffers (unless it recomputes them)
+  if (!cfg_.recompute) {
+    if (!fwd_ran_) throw std::runtime_error("backward: no forward has run on this executor");
+    for (int i = 0; i < n_; ++i)
+      if (fwd_inputs_[static_cast<std::size_t>(i)] != inputs[i])
+        throw std::runtime_error("backward: input " + std::to_string(i) +
+                                 " is not the buffer the last forward ran on (run forward on these inputs first)");
+  }
   ensure_workspace();
   dout_ = dout;
   // intermediate gradients are only needed above requested inputs

@@ -47,6 +47,9 @@ struct Step {
 
 struct ExecConfig {
   int math = 0;  // 0 auto (tensor cores where mappable), 1 FP32 SIMT only
+  // gradient checkpointing: the forward pass keeps no
+  // intermediates; the backward pass recomputes them first (one extra forward's work)
+  bool recompute = false;
 };
 
 class Executor {
@@ -93,6 +96,7 @@ class Executor {
   void compute_deps(std::vector<Step>& steps) const;
   void assign_offsets();
   void fuse_chains(std::vector<Step>& list);
+  void add_recompute();
   bool overlap(const BufRef& x, const BufRef& y) const;
   float* resolve(const BufRef& r) const;
 
@@ -110,6 +114,7 @@ class Executor {
   std::vector<int64_t> buf_bytes_, buf_off_;  // per workspace buffer id
   int ws_reuse_mode_ = 0;
   char* ws_ = nullptr;
+  char* ext_ws_ = nullptr;
   // bound per call
   std::vector<const float*> inputs_;
   std::vector<const float*> fwd_inputs_;  // inputs of the last forward (its intermediates are in ws_)
@@ -144,6 +149,10 @@ class Executor {
 
  public:
   void set_use_graphs(bool on) { use_graphs_ = on; }
+  // Run on a caller-owned arena of >= workspace_bytes() (e.g. one arena a context shares
+  // among its recompute executors: they keep nothing between calls); nullptr: own arena.
+  void bind_workspace(char* base) { ext_ws_ = base; }
+  bool recompute() const { return cfg_.recompute; }
 };
 
 }  // namespace ce

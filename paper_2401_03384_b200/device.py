@@ -148,10 +148,14 @@ def _check_inputs(plan: Plan, inputs):
 class Executor:
     """execute() (sequencer.cpp:403-447) + backward on one device."""
 
-    def __init__(self, ctx: Context, plan: Plan, backward: bool = False):
+    def __init__(self, ctx: Context, plan: Plan, backward: bool = False, recompute: bool = False):
+        """recompute: gradient checkpointing -- backward() recomputes the
+        forward intermediates instead of reading ones execute() kept."""
+        from .api import CE_EXEC_RECOMPUTE
         self.ctx, self.plan = ctx, plan
         h = ctypes.c_void_p()
-        check(lib().ce_executor_create(ctx.handle, plan._h, int(backward), ctypes.byref(h)))
+        wb = int(backward) | (CE_EXEC_RECOMPUTE if (backward and recompute) else 0)
+        check(lib().ce_executor_create(ctx.handle, plan._h, wb, ctypes.byref(h)))
         self._h = h
         self._destroy = lib().ce_executor_destroy
         self.stats = _lib.ExecStats()

@@ -42,3 +42,24 @@ def test_workspace_never_exceeds_bump_layout():
         lines = plan.describe_steps(True, "auto").splitlines()
         vals = {l.split()[0]: int(l.split()[1]) for l in lines if l.startswith("workspace_bytes")}
         assert vals["workspace_bytes"] <= vals["workspace_bytes_unshared"]
+
+
+def _ws2(kind, tf, sf, k, hp, batch, cr, recompute):
+    slots = {"cp": 1, "tk": 2, "tt": 3, "tr": 4, "rtr": 4}[kind]
+    le = ce.expression(ce.LayerSpec(kind, tf, sf, k, k, hp, hp, batch, [1] * slots), cr)
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    return plan.describe_steps(True, "auto", recompute=recompute)
+
+
+def test_recompute_steps():
+    """Gradient checkpointing: the backward pass starts with the forward
+    steps that write workspace (not the root node, which writes the caller's output), into
+    fresh buffers; a fused forward stencil pair no longer stores its intermediate."""
+    keep = _ws2("cp", [64], [64], 3, 56, 8, 0.1, False).splitlines()
+    rec = _ws2("cp", [64], [64], 3, 56, 8, 0.1, True).splitlines()
+    fwd_keep = [l for l in keep if l.startswith("fwd")]
+    fwd_rec = [l for l in rec if l.startswith("fwd")]
+    assert len(fwd_keep) == len(fwd_rec)
+    assert any("store_mid=1" in l for l in fwd_keep) and all("store_mid=1" not in l for l in fwd_rec)
+    recomputed = [l for l in rec if l.startswith("bwd recompute:")]
+    assert len(recomputed) == len(fwd_rec) - 1  # every forward step but the root node
