@@ -1,5 +1,5 @@
-"""Run one cfg2 layer forward+backward a few times (for ncu captures).
-usage: python tools/run_layer.py tk 1.0 [iters]"""
+"""Run one layer forward+backward a few times (for ncu captures).
+usage: python tools/run_layer.py tk 1.0 [iters] [T S k Hp B]   (default: the cfg2 shape 256 256 3 14 128)"""
 import os
 import sys
 
@@ -14,7 +14,8 @@ iters = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 ctx = Context(0, "auto")
 torch.cuda.set_stream(ctx.torch_stream)
 slots = {"tk": 2, "tt": 3, "cp": 1, "tr": 4}[kind]
-le = ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, 128, [1] * slots), cr)
+T, S, k, hp, B = (int(x) for x in sys.argv[4:9]) if len(sys.argv) > 8 else (256, 256, 3, 14, 128)
+le = ce.expression(ce.LayerSpec(kind, [T], [S], k, k, hp, hp, B, [1] * slots), cr)
 plan = ce.optimal(le.expr, le.dims, "same", "training")
 print(plan.describe_steps(True), flush=True)
 ex = Executor(ctx, plan, backward=True)
