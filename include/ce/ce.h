@@ -231,6 +231,23 @@ ce_status ce_pairwise_grad(ce_ctx* ctx, const char* expr, const int64_t* dims, c
 ce_status ce_flops_actual(const char* expr, const int64_t* dims, const int* ranks, const char* mode, uint64_t* lo,
                           uint64_t* hi);
 
+/* ------------------------------------------------------ like-mode merging -- */
+/* merge_like_modes (kernels.hpp:88-94, kernels.cpp:246-265) on the device: permutes `in`
+ * (FP32, dense in `subs` order, shape `dims`) into `out` in the canonical class order
+ * batch | contraction (+ self) | free | convolution (members in their order of appearance),
+ * and reports the merged subscripts / dims: each class's atoms become one compound atom
+ * named by concatenating the member names, except singletons and convolution atoms
+ * (kernels.cpp:191-235).  `classes` lists "atom:class" pairs as ce_parse emits them.
+ * `record` receives the MergeRecord as text "compound=member:dim,member:dim;..." for
+ * ce_unmerge_modes.  Stream-ordered on the ctx stream. */
+ce_status ce_merge_like_modes(ce_ctx* ctx, const char* subs, const int64_t* dims, const char* classes,
+                              const float* in, float* out, char* merged_subs, size_t subs_cap, int64_t* merged_dims,
+                              int* merged_rank, char* record, size_t record_cap);
+/* unmerge_modes (kernels.cpp:267-286): a reshape (no data movement): every compound atom of
+ * `subs` named in `record` is expanded back into its members. */
+ce_status ce_unmerge_modes(const char* subs, const int64_t* dims, const char* record, char* out_subs,
+                           size_t subs_cap, int64_t* out_dims, int* out_rank);
+
 /* ------------------------------------------------------------ conv_einsum -- */
 /* The paper's call form conv_einsum("...", T1, T2, ...): parse ->
  * make_shape_env -> resolve_conv_modes -> optimal(cost_mode) -> execute, with the

@@ -223,3 +223,17 @@ def layer_json_roundtrip(layer_json):
     out = _buf(1 << 12)
     _check(lib().ref_layer_json_roundtrip(layer_json.encode(), out, len(out)))
     return out.value.decode()
+
+
+def merge_like_modes(expr1, dims, data):
+    """Reference merge_like_modes + unmerge_modes on a one-input expression's classes:
+    (permuted data, merged subs, merged dims, record, unmerged subs, unmerged dims)."""
+    a = np.ascontiguousarray(data, dtype=np.float64)
+    d = (ctypes.c_int64 * max(1, len(dims)))(*dims)
+    out = np.zeros(max(1, a.size), dtype=np.float64)
+    info = _buf(1 << 14)
+    P = ctypes.POINTER(ctypes.c_double)
+    _check(lib().ref_merge_like_modes(expr1.encode(), d, a.ctypes.data_as(P), out.ctypes.data_as(P), info, len(info)))
+    ms, md, rec, us, ud = info.value.decode().split("\n")
+    md = [int(x) for x in md.split(",")]
+    return out[:a.size].reshape(md), ms, md, rec, us, [int(x) for x in ud.split(",")]

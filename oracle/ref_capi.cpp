@@ -348,4 +348,31 @@ int ref_layer_json_roundtrip(const char* layer_json, char* out, int cap) {
   return guard([&] { put(layer_to_json(layer_from_json(layer_json)), out, cap); });
 }
 
+// merge_like_modes / unmerge_modes (kernels.cpp:246-286): "merged_subs\nrecord" out (record as
+// "compound=member:dim,...;..."), permuted data in `out`; unmerged subscripts + dims back.
+int ref_merge_like_modes(const char* expr1, const int64_t* dims, const double* data, double* out, char* info,
+                         int cap) {
+  return guard([&] {
+    // expr1: a one-input expression "subs->output|convs" whose classify() gives the classes
+    ExpressionSpec spec = parse(expr1);
+    const Subscripts& subs = spec.inputs.at(0);
+    DenseTensor t(std::vector<int64_t>(dims, dims + subs.size()));
+    std::memcpy(t.data.data(), data, sizeof(double) * t.data.size());
+    auto [m, msubs, rec] = merge_like_modes(t, subs, classify(spec));
+    std::memcpy(out, m.data.data(), sizeof(double) * m.data.size());
+    std::string r;
+    for (const auto& g : rec.groups) {
+      r += (r.empty() ? "" : ";") + g.compound.name + "=";
+      for (std::size_t k = 0; k < g.members.size(); ++k)
+        r += (k ? "," : "") + g.members[k].name + ":" + std::to_string(g.member_dims[k]);
+    }
+    auto [u, usubs] = unmerge_modes(m, msubs, rec);
+    std::string ud;
+    for (std::size_t i = 0; i < u.shape.size(); ++i) ud += (i ? "," : "") + std::to_string(u.shape[i]);
+    std::string md;
+    for (std::size_t i = 0; i < m.shape.size(); ++i) md += (i ? "," : "") + std::to_string(m.shape[i]);
+    put(render(msubs) + "\n" + md + "\n" + r + "\n" + render(usubs) + "\n" + ud, info, cap);
+  });
+}
+
 }  // extern "C"

@@ -99,6 +99,11 @@ SIGNATURES = {
     "ce_allreduce_grads": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), c_i64p, ctypes.c_int]),
     "ce_comm_wait": (ctypes.c_int, [ctypes.c_void_p]),
     "ce_comm_check": (ctypes.c_int, [ctypes.c_void_p]),
+    "ce_merge_like_modes": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, c_i64p, ctypes.c_char_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t, c_i64p, c_intp,
+                                           ctypes.c_char_p, ctypes.c_size_t]),
+    "ce_unmerge_modes": (ctypes.c_int, [ctypes.c_char_p, c_i64p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t,
+                                        c_i64p, c_intp]),
     "ce_tensor_to_json": (ctypes.c_int, [c_i64p, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_char_p,
                                          ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
     "ce_tensor_from_json": (ctypes.c_int, [ctypes.c_char_p, c_i64p, ctypes.c_int, c_intp,

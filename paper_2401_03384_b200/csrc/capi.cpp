@@ -715,6 +715,148 @@ ce_status ce_flops_actual(const char* expr, const int64_t* dims, const int* rank
   return guard([&] { split_u128(flops_actual(pairwise_plan(expr, dims, ranks, mode).nodes[0].op), lo, hi); });
 }
 
+// ------------------------------------------------------------------ like-mode merging
+namespace {
+Subscripts parse_subs(const char* subs) {
+  ExpressionSpec spec = parse(std::string(subs) + "->");
+  return spec.inputs.at(0);
+}
+AtomClass class_from_string(const std::string& c) {
+  for (AtomClass k : {AtomClass::Convolution, AtomClass::BatchProduct, AtomClass::Contraction, AtomClass::Free,
+                      AtomClass::SelfContraction})
+    if (c == to_string(k)) return k;
+  throw ShapeError("merge: unknown atom class '" + c + "'");
+}
+}  // namespace
+
+ce_status ce_merge_like_modes(ce_ctx* ctx, const char* subs, const int64_t* dims, const char* classes,
+                              const float* in, float* out, char* merged_subs, size_t subs_cap, int64_t* merged_dims,
+                              int* merged_rank, char* record, size_t record_cap) {
+  return guard([&] {
+    cuda_ok(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const Subscripts sub = parse_subs(subs);
+    const std::vector<int64_t> d(dims, dims + sub.size());
+    std::map<Atom, AtomClass> cls;
+    {
+      std::string s = classes;
+      std::size_t pos = 0;
+      while (pos < s.size()) {
+        const std::size_t end = std::min(s.find(' ', pos), s.size());
+        const std::string tok = s.substr(pos, end - pos);
+        pos = end + 1;
+        if (tok.empty()) continue;
+        const std::size_t colon = tok.rfind(':');
+        if (colon == std::string::npos) throw ShapeError("merge: class entry '" + tok + "' is not atom:class");
+        cls[Atom{tok.substr(0, colon)}] = class_from_string(tok.substr(colon + 1));
+      }
+    }
+    // canonical class order; members keep their order of appearance (kernels.cpp:249-264)
+    std::vector<std::pair<AtomClass, Subscripts>> groups = {
+        {AtomClass::BatchProduct, {}}, {AtomClass::Contraction, {}}, {AtomClass::Free, {}}, {AtomClass::Convolution, {}}};
+    for (const Atom& a : sub) {
+      auto it = cls.find(a);
+      if (it == cls.end()) throw ShapeError("merge: atom '" + a.name + "' has no class");
+      const int g = it->second == AtomClass::BatchProduct ? 0
+                    : (it->second == AtomClass::Contraction || it->second == AtomClass::SelfContraction) ? 1
+                    : it->second == AtomClass::Free ? 2 : 3;
+      groups[static_cast<std::size_t>(g)].second.push_back(a);
+    }
+    Subscripts order;
+    std::vector<int64_t> odims;
+    for (const auto& g : groups)
+      for (const Atom& a : g.second) {
+        order.push_back(a);
+        odims.push_back(d[static_cast<std::size_t>(find_atom(sub, a))]);
+      }
+    // the data movement: one permute (family c) into the canonical order
+    const CeProblem p = lower_unary(dense_view(sub, d), dense_view(order, odims));
+    if (element_count(d) > 0) {
+      cudaError_t e = ce_permute_supported(p) ? ce_launch_permute(p, in, out, ctx->stream)
+                                              : ce_launch_direct(simt_desc(p), in, nullptr, out, ctx->stream);
+      cuda_ok(e, "merge_like_modes permute");
+    }
+    // the reshape: compound axes per class (singletons and conv atoms keep their own axes)
+    Subscripts msubs;
+    std::vector<int64_t> mdims;
+    std::string rec;
+    std::size_t pos = 0;
+    for (const auto& [c, members] : groups) {
+      if (members.empty()) continue;
+      if (members.size() == 1 || c == AtomClass::Convolution) {
+        for (const Atom& a : members) {
+          msubs.push_back(a);
+          mdims.push_back(odims[pos++]);
+        }
+        continue;
+      }
+      std::string name;
+      int64_t dim = 1;
+      rec += rec.empty() ? "" : ";";
+      std::string mem;
+      for (const Atom& a : members) {
+        name += a.name;
+        mem += (mem.empty() ? "" : ",") + a.name + ":" + std::to_string(odims[pos]);
+        dim *= odims[pos++];
+      }
+      msubs.push_back(Atom{name});
+      mdims.push_back(dim);
+      rec += name + "=" + mem;
+    }
+    copy_out(render(msubs), merged_subs, subs_cap);
+    for (std::size_t i = 0; i < mdims.size(); ++i) merged_dims[i] = mdims[i];
+    *merged_rank = static_cast<int>(mdims.size());
+    copy_out(rec, record, record_cap);
+  });
+}
+
+ce_status ce_unmerge_modes(const char* subs, const int64_t* dims, const char* record, char* out_subs,
+                           size_t subs_cap, int64_t* out_dims, int* out_rank) {
+  return guard([&] {
+    const Subscripts sub = parse_subs(subs);
+    // record: "compound=member:dim,member:dim;..."
+    std::map<std::string, std::vector<std::pair<std::string, int64_t>>> groups;
+    std::string r = record ? record : "";
+    std::size_t pos = 0;
+    while (pos < r.size()) {
+      const std::size_t end = std::min(r.find(';', pos), r.size());
+      const std::string g = r.substr(pos, end - pos);
+      pos = end + 1;
+      const std::size_t eq = g.find('=');
+      if (eq == std::string::npos) throw ShapeError("unmerge: malformed record group '" + g + "'");
+      auto& mem = groups[g.substr(0, eq)];
+      std::size_t q = eq + 1;
+      while (q < g.size()) {
+        const std::size_t e2 = std::min(g.find(',', q), g.size());
+        const std::string m = g.substr(q, e2 - q);
+        q = e2 + 1;
+        const std::size_t colon = m.rfind(':');
+        if (colon == std::string::npos) throw ShapeError("unmerge: malformed member '" + m + "'");
+        mem.push_back({m.substr(0, colon), std::stoll(m.substr(colon + 1))});
+      }
+    }
+    Subscripts os;
+    std::vector<int64_t> od;
+    for (std::size_t i = 0; i < sub.size(); ++i) {
+      auto it = groups.find(sub[i].name);
+      if (it == groups.end()) {
+        os.push_back(sub[i]);
+        od.push_back(dims[i]);
+        continue;
+      }
+      int64_t prod = 1;
+      for (const auto& [n, dd] : it->second) {
+        os.push_back(Atom{n});
+        od.push_back(dd);
+        prod *= dd;
+      }
+      if (prod != dims[i]) throw ShapeError("unmerge: compound '" + sub[i].name + "' dim does not match its members");
+    }
+    copy_out(render(os), out_subs, subs_cap);
+    for (std::size_t i = 0; i < od.size(); ++i) out_dims[i] = od[i];
+    *out_rank = static_cast<int>(od.size());
+  });
+}
+
 ce_status ce_conv_einsum(ce_ctx* ctx, const char* expr, const int64_t* dims, const int* ranks, int n_inputs,
                          const char* mode, const char* cost_mode, const float* const* inputs, float* out) {
   return guard([&] {

@@ -305,3 +305,38 @@ class _ConvEinsumFn(torch.autograd.Function):
 def conv_einsum(expr: str, *tensors: torch.Tensor, mode: str = "same", math: str = "auto") -> torch.Tensor:
     """The paper's call form conv_einsum("...", T1, T2, ...), differentiable."""
     return _ConvEinsumFn.apply(expr, mode, math, *tensors)
+
+
+# ----------------------------------------------------------------------------- like-mode merging
+def merge_like_modes(ctx: Context, t: torch.Tensor, subs: str, classes: dict):
+    """merge_like_modes (kernels.hpp:88-94) on the device: returns (merged tensor, merged
+    subscripts, record).  `classes`: atom -> class name as api.classify() returns."""
+    if not (t.is_cuda and t.dtype == torch.float32):
+        raise TypeError("merge_like_modes: a CUDA float32 tensor")
+    t = t.contiguous()
+    d = (ctypes.c_int64 * max(1, t.dim()))(*t.shape)
+    cls = " ".join(f"{a}:{c}" for a, c in classes.items()).encode()
+    out = torch.empty_like(t)
+    ms = ctypes.create_string_buffer(1024)
+    md = (ctypes.c_int64 * 64)()
+    mr = ctypes.c_int()
+    rec = ctypes.create_string_buffer(4096)
+    cur = torch.cuda.current_stream(t.device)
+    ctx.torch_stream.wait_stream(cur)
+    check(lib().ce_merge_like_modes(ctx.handle, subs.encode(), d, cls, ctypes.c_void_p(t.data_ptr()),
+                                    ctypes.c_void_p(out.data_ptr()), ms, len(ms), md, ctypes.byref(mr), rec,
+                                    len(rec)))
+    cur.wait_stream(ctx.torch_stream)
+    t.record_stream(ctx.torch_stream)
+    out.record_stream(cur)
+    return out.view([int(md[i]) for i in range(mr.value)]), ms.value.decode(), rec.value.decode()
+
+
+def unmerge_modes(t: torch.Tensor, subs: str, record: str):
+    """unmerge_modes (kernels.hpp:96-98): a reshape back to the member axes."""
+    d = (ctypes.c_int64 * max(1, t.dim()))(*t.shape)
+    us = ctypes.create_string_buffer(1024)
+    ud = (ctypes.c_int64 * 64)()
+    ur = ctypes.c_int()
+    check(lib().ce_unmerge_modes(subs.encode(), d, record.encode(), us, len(us), ud, ctypes.byref(ur)))
+    return t.view([int(ud[i]) for i in range(ur.value)]), us.value.decode()
