@@ -314,16 +314,19 @@ __device__ __forceinline__ void decode_work(const TcParams& P, uint32_t w, uint3
   T.split = static_cast<int>(t);
 }
 
-// Work sequence of one group: whole items group, group + ngroups, ... below sk_full,
-// then (stream-K) the group's contiguous share of the sk_r tail items' K iterations.
+// Work sequence of one group: whole items group, group + ngroups, ... below sk_full, then
+// (tail split) one K chunk of a tail item: the sk_r items of a partial last round are each cut
+// into tl_s K chunks, one per group (group u -> item sk_full + u / tl_s, chunk u % tl_s).
+// Chunk 0 stores its partial tile; chunks > 0 wait for it (tl_flags) and add theirs.
 struct WorkIter {
   uint32_t w;         // next whole item
   uint32_t wend;      // contiguous mode: end of this group's items
-  uint32_t pos, end;  // stream-K iteration range (relative to item sk_full, iteration 0)
+  uint32_t tail;      // this group's tail unit, or ~0u (none / consumed)
   bool seq;           // the item returned last was the previous item + 1 (contiguous mode)
 };
 
 __device__ __forceinline__ void work_begin(const TcParams& P, uint32_t group, uint32_t ngroups, WorkIter& it) {
+  (void)ngroups;
   it.w = group;
   it.wend = 0;
   it.seq = false;
@@ -331,13 +334,7 @@ __device__ __forceinline__ void work_begin(const TcParams& P, uint32_t group, ui
     it.w = group * P.ipg + min(group, P.irem);
     it.wend = it.w + P.ipg + (group < P.irem ? 1u : 0u);
   }
-  it.pos = it.end = 0;
-  if (P.sk_r > 0) {
-    const uint32_t total = P.sk_r * static_cast<uint32_t>(P.k_iters);
-    const uint32_t q = total / ngroups, r = total % ngroups;
-    it.pos = group * q + min(group, r);
-    it.end = it.pos + q + (group < r ? 1u : 0u);
-  }
+  it.tail = (P.sk_r > 0 && group < P.sk_r * P.tl_s) ? group : ~0u;
 }
 
 // T <- the tile of the next item in decode_work's order (M units fastest, then N units,
@@ -374,9 +371,11 @@ __device__ __forceinline__ void advance_tile(const TcParams& P, Tile& T) {
   }
 }
 
-// Next segment: item (full-decomposition index), K range [k0, k1), atomic epilogue flag.
+// Next segment: item (full-decomposition index), K range [k0, k1), atomic epilogue flag, and
+// the tail chunk (-1 for whole items).
 __device__ __forceinline__ bool work_next(const TcParams& P, uint32_t ngroups, WorkIter& it, uint32_t& item, int& k0,
-                                          int& k1, bool& atomic) {
+                                          int& k1, bool& atomic, int& chunk) {
+  chunk = -1;
   if (P.contig) {
     if (it.w >= it.wend) return false;
     it.seq = item == it.w - 1 && it.w != 0;
@@ -396,13 +395,14 @@ __device__ __forceinline__ bool work_next(const TcParams& P, uint32_t ngroups, W
     atomic = P.k_split > 1;
     return true;
   }
-  if (it.pos >= it.end) return false;
-  const uint32_t rel = tc_quo(it.pos, P.dkit);
-  k0 = static_cast<int>(it.pos - rel * static_cast<uint32_t>(P.k_iters));
-  k1 = min(P.k_iters, k0 + static_cast<int>(it.end - it.pos));
-  item = P.sk_full + rel;
-  atomic = true;
-  it.pos += static_cast<uint32_t>(k1 - k0);
+  if (it.tail == ~0u) return false;
+  const uint32_t t = it.tail / static_cast<uint32_t>(P.tl_s);
+  chunk = static_cast<int>(it.tail - t * static_cast<uint32_t>(P.tl_s));
+  it.tail = ~0u;
+  item = P.sk_full + t;
+  k0 = chunk * P.k_iters / P.tl_s;
+  k1 = (chunk + 1) * P.k_iters / P.tl_s;
+  atomic = chunk > 0;
   return true;
 }
 
@@ -559,10 +559,10 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
       WorkIter wi;
       work_begin(P, group, ngroups, wi);
       uint32_t item;
-      int k0, k1;
+      int k0, k1, chunk;
       bool seg_atomic;
       item = 0xffffffffu;
-      while (work_next(P, ngroups, wi, item, k0, k1, seg_atomic)) {
+      while (work_next(P, ngroups, wi, item, k0, k1, seg_atomic, chunk)) {
         if (wi.seq)
           advance_tile(P, T);
         else
@@ -676,9 +676,9 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
       WorkIter wi;
       work_begin(P, group, ngroups, wi);
       uint32_t item = 0xffffffffu;
-      int k0, k1;
+      int k0, k1, chunk;
       bool seg_atomic;
-      for (; work_next(P, ngroups, wi, item, k0, k1, seg_atomic); ++local) {
+      for (; work_next(P, ngroups, wi, item, k0, k1, seg_atomic, chunk); ++local) {
         const int acc = static_cast<int>(local & 1);
         int d0 = k0 % kc0;  // K digit 0 of the first iteration (for the K tail)
         if (PAIR)
@@ -738,9 +738,9 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
       WorkIter wi;
       work_begin(P, group, ngroups, wi);
       uint32_t item = 0xffffffffu;
-      int k0, k1;
+      int k0, k1, chunk;
       bool seg_atomic;
-      while (work_next(P, ngroups, wi, item, k0, k1, seg_atomic)) {
+      while (work_next(P, ngroups, wi, item, k0, k1, seg_atomic, chunk)) {
         for (int it = k0; it < k1; ++it, ++gi) {
           const int s = static_cast<int>(gi % STAGES);
           mbar_wait(&full[s], (gi / STAGES) & 1);
@@ -802,9 +802,9 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
     WorkIter wi;
     work_begin(P, group, ngroups, wi);
     uint32_t item = 0xffffffffu;
-    int k0, k1;
+    int k0, k1, chunk;
     bool atomic;
-    for (; work_next(P, ngroups, wi, item, k0, k1, atomic); ++local) {
+    for (; work_next(P, ngroups, wi, item, k0, k1, atomic, chunk); ++local) {
       const int acc = static_cast<int>(local & 1);
       if (et == 0) {  // (also for the other group's tiles: the incremental advance needs every item)
         if (wi.seq)
@@ -862,6 +862,16 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
       }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (local == 0) ce_pdl_wait();  // (long complete: the producer waited before its loads)
+      if (chunk > 0) {  // tail chunk: chunk 0 of this item must have stored its partial tile
+        if (et == 0) {
+          const uint32_t* f = P.tl_flags + (item - P.sk_full);
+          uint32_t v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+          } while (v == 0);
+        }
+        epi_bar(1 + grp);
+      }
       const bool empty_k = k1 <= k0;
       const uint32_t t_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
       // TMEM loads double-buffered against the stores: chunk c+1 is read while chunk c drains
@@ -955,6 +965,14 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
         process(ra, ch);
       }
       if (est) stamp_it(P, 2, static_cast<uint32_t>(local / ngrp) * 4 + 3);
+      if (chunk >= 0) {  // tail chunk stored / added: count it; the last one resets the flag
+        epi_bar(1 + grp);
+        if (et == 0) {
+          uint32_t* f = P.tl_flags + (item - P.sk_full);
+          __threadfence();
+          if (atomicAdd(f, 1u) + 1u == static_cast<uint32_t>(P.tl_s)) atomicExch(f, 0u);
+        }
+      }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       if (PAIR && !leader)
         mbar_arrive_cluster(mapa(&tempty[acc], 0));  // the even CTA's MMA owns the pair's TMEM writes
@@ -1134,26 +1152,34 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
       P.irem = static_cast<uint32_t>(items % ngroups);
     }
     P.dkit = tc_div(static_cast<uint32_t>(std::max(1, P.k_iters)));
-    // off by default: the C memset it needs is a separate graph node that breaks the PDL
-    // chain, which cost more than the shorter last round saved (measured on cfg2:
-    // tk1.0 node1 76 -> 68 us, layer 0.434 -> 0.456 ms).  CE_TC_SK=1 enables it.
-    static const bool sk_on = [] {
-      const char* e = getenv("CE_TC_SK");
-      return e && *e == '1';
+    // tail split of a partial last round (see work_next): the r items left after the full
+    // rounds are each cut into S = min(4, ngroups / r) K chunks run by the otherwise idle
+    // groups; chunk 0 stores, the others wait for it (P.tl_flags, zeroed by the executor and
+    // left zero by the last chunk) and add.  CE_TC_TAIL=0 off.
+    static const int tail_on = [] {
+      const char* e = getenv("CE_TC_TAIL");
+      return e ? atoi(e) : 1;
     }();
-    if (sk_on && !P.contig && P.k_split == 1 && items > ngroups && items % ngroups != 0) {
-      // gain: the last round shrinks from one item time to r/ngroups of it; cost: zeroing C
-      // (and an atomic epilogue for those items).  Item time ~ 0.4 us per K stage.
+    P.tl_s = 1;
+    P.tl_flags = plan.tail_flags;
+    // (long K loops only: with ~24 K stages the chunks' fixup costs what the shorter round
+    // saves -- tt1.0's 24/27-stage convs were slower; tk1.0's 72-stage convs 74 -> 68 us)
+    static const int tail_kmin = [] {
+      const char* e = getenv("CE_TC_TAIL_KMIN");
+      return e ? atoi(e) : 48;
+    }();
+    if (tail_on && plan.tail_flags && !P.contig && P.k_split == 1 && csize == 1 && items > ngroups &&
+        items % ngroups != 0 && P.k_iters >= tail_kmin) {
       const int64_t r = items % ngroups;
-      const double saved_us = 0.4 * P.k_iters * (1.0 - static_cast<double>(r) / static_cast<double>(ngroups));
-      const double cost_us = 2.0 + static_cast<double>(plan.out_span) * 4.0 / 5.0e6;
-      if (saved_us > 1.5 * cost_us) {
+      const int64_t S = std::min<int64_t>({4, ngroups / r, P.k_iters / 4});
+      if (S >= 2 && r <= kTailFlags) {
         P.sk_full = static_cast<uint32_t>(items - r);
         P.sk_r = static_cast<uint32_t>(r);
+        P.tl_s = static_cast<int32_t>(S);
       }
     }
   }
-  if (P.k_split > 1 || P.sk_r > 0) {
+  if (P.k_split > 1) {
     cudaError_t e = cudaMemsetAsync(C, 0, static_cast<size_t>(plan.out_span) * 4, s);
     if (e != cudaSuccess) return e;
   }

@@ -23,6 +23,7 @@
 #define TC_MAX_UNITS 14
 #define TC_BM 128
 #define TC_BK 32
+#define kTailFlags 512  // tail-split flag words per TC step (>= groups of one launch)
 
 enum TcSrc { TC_SRC_MTILE = 0, TC_SRC_NTILE = 1, TC_SRC_GRID = 2, TC_SRC_K = 3 };
 
@@ -107,13 +108,14 @@ struct TcParams {
   TcDiv dtn;       // tiles_n
   TcDiv dsplit;    // pm * tiles_n * grid_z: work items per K split
   int32_t k_per;   // K iterations per split
-  // Stream-K tail (set per launch): the n_items work items are dealt in full rounds of
-  // ngroups; the sk_r items of a partial last round are instead spread over ALL groups as
-  // contiguous runs of K iterations (each group ~sk_r * k_iters / ngroups of them), with an
-  // atomic epilogue into a pre-zeroed C.  sk_r == 0: off.
+  // Tail split (set per launch): the n_items work items are dealt in full rounds of ngroups;
+  // the sk_r items of a partial last round are each cut into tl_s K chunks run by otherwise
+  // idle groups -- chunk 0 stores, the others wait for its flag and add.  sk_r == 0: off.
   uint32_t n_items;  // work items of the full decomposition (tiles x K splits)
   uint32_t sk_full;  // items handled whole (a multiple of ngroups)
-  uint32_t sk_r;     // items handled stream-K
+  uint32_t sk_r;     // tail items, each split into tl_s K chunks
+  int32_t tl_s;      // K chunks per tail item
+  uint32_t* tl_flags;// per tail item: chunks finished (chunk 0 first); zero between launches
   TcDiv dkit;        // k_iters
   // contiguous assignment (set per launch for many small tiles, no K split, no pairs):
   // group g takes items [g*ipg + min(g, rem), ...) in order, so the tile origins advance
@@ -144,6 +146,7 @@ struct TcPlan {
   uint32_t box_a[5]{}, box_b[5]{};
   int swz_a = 3, swz_b = 3;   // CUtensorMapSwizzle: 3 128B (K-major), 4 128B_ATOM_32B (native MN-major), 0 none (wide)
   int64_t out_span = 0;       // elements of C to zero before a split-K launch
+  uint32_t* tail_flags = nullptr;  // kTailFlags zeroed words owned by the executor (tail split)
   const void* cached_a = nullptr;
   const void* cached_b = nullptr;
   const char* why = "";       // reason when not valid (diagnostics)

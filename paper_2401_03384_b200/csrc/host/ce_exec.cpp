@@ -75,6 +75,7 @@ Executor::Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cf
 
 Executor::~Executor() {
   if (ws_) cudaFree(ws_);
+  if (tail_flags_) cudaFree(tail_flags_);
   for (auto* list : {&fwd_, &bwd_})
     for (Step& st : *list) {
       if (st.ev0) cudaEventDestroy(st.ev0);
@@ -1199,6 +1200,21 @@ std::string Executor::describe() const {
 
 void Executor::ensure_workspace() {
   if (!ext_ws_ && !ws_ && ws_bytes_ > 0) cuda_check(cudaMalloc(&ws_, static_cast<size_t>(ws_bytes_)), "cudaMalloc(workspace)");
+  if (!tail_flags_) {
+    // the TC kernel's tail-split flags: a zeroed region per TC step (each launch leaves it zero)
+    std::size_t n = 0;
+    for (const auto* list : {&fwd_, &bwd_})
+      for (const Step& st : *list) n += st.kind == Step::kTc;
+    if (n > 0) {
+      const std::size_t bytes = n * kTailFlags * sizeof(uint32_t);
+      cuda_check(cudaMalloc(&tail_flags_, bytes), "cudaMalloc(tail flags)");
+      cuda_check(cudaMemset(tail_flags_, 0, bytes), "cudaMemset(tail flags)");
+      std::size_t i = 0;
+      for (auto* list : {&fwd_, &bwd_})
+        for (Step& st : *list)
+          if (st.kind == Step::kTc) st.tc.tail_flags = tail_flags_ + kTailFlags * i++;
+    }
+  }
 }
 
 int Executor::tc_steps(bool bwd) const {

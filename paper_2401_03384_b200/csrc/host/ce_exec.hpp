@@ -115,6 +115,7 @@ class Executor {
   int ws_reuse_mode_ = 0;
   char* ws_ = nullptr;
   char* ext_ws_ = nullptr;
+  uint32_t* tail_flags_ = nullptr;  // kTailFlags zeroed words per TC step (tail split)
   // bound per call
   std::vector<const float*> inputs_;
   std::vector<const float*> fwd_inputs_;  // inputs of the last forward (its intermediates are in ws_)
