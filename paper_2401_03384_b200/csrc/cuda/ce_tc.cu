@@ -249,6 +249,22 @@ __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
                : "memory");
 }
 
+// Bulk tensor store / reduce-add of a staged shared-memory box (TMA-store epilogue).
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, const void* src, const int c[5], bool add) {
+  if (add)
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.5d.global.shared::cta.add.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(map),
+        "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src))
+        : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(map),
+                 "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src))
+                 : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // Named barrier of one epilogue warp group (ids 1 and 2).
 __device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(32 * kEpiWarps) : "memory"); }
 
@@ -508,6 +524,7 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&Pg.ta) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&Pg.tb) : "memory");
+    if (Pg.c_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(&Pg.tc) : "memory");
   }
   if (warp == 1) {
     if (PAIR) {
@@ -846,6 +863,11 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
       const int64_t ro = row < m_rows ? tile_offset(P, P.mt, P.nm, T.val, row) : -1;
       const int64_t roff = ro < 0 ? -1 : base + ro;  // row offset in C, -1 outside the tile
       rtab[row] = roff;
+      // TMA-store coordinates of this tile, taken while T is stable (thread 0 of the group
+      // rewrites T for the next item as soon as its own chunks are out)
+      int cbase[5];
+#pragma unroll
+      for (int d = 0; d < 5; ++d) cbase[d] = P.c_tma && P.cdim_u[d] >= 0 ? T.val[P.cdim_u[d]] : 0;
       epi_bar(1 + grp);  // tables visible to all epilogue warps
       if ((dbg & 32) && et == 0 && local == 0) stamp(P, 10);
       if (est) stamp_it(P, 2, static_cast<uint32_t>(local / ngrp) * 4 + 1);
@@ -958,11 +980,50 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
       // one 32-column chunk in flight: a second buffer (measured neutral) would hold 32 more
       // registers in a kernel that sits at its 168-register cap
       uint32_t ra[32];
+      if (P.c_tma) {
+        // TMA-store epilogue: this warp's 32 x 32 block of each chunk -> its 4 KB staging
+        // buffer (1024-B aligned) -> one bulk tensor store (reduce-add when accumulating)
+        uint8_t* buf = reinterpret_cast<uint8_t*>(stage_out) + ew * 4096;
 #pragma unroll 1
-      for (int ch = 0; ch < nch; ++ch) {
-        tmem_ld32_issue(t_base + ch * 32, ra);
-        tmem_ld_wait(ra);
-        process(ra, ch);
+        for (int ch = 0; ch < nch; ++ch) {
+          tmem_ld32_issue(t_base + ch * 32, ra);
+          tmem_ld_wait(ra);
+          if (empty_k)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ra[i] = 0;
+          if (lane == 0) bulk_wait_read();  // the previous store has read the buffer
+          __syncwarp();
+          if (P.c_tma == 1) {  // rows innermost: column-major block, lanes write consecutive words
+            float* b = reinterpret_cast<float*>(buf);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) b[i * 32 + lane] = __uint_as_float(ra[i]);
+          } else {  // columns innermost: row-major 128-B rows, 16-B chunks swizzled (SWIZZLE_128B)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                  make_float4(__uint_as_float(ra[4 * j]), __uint_as_float(ra[4 * j + 1]),
+                              __uint_as_float(ra[4 * j + 2]), __uint_as_float(ra[4 * j + 3]));
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            int c[5];
+#pragma unroll
+            for (int d = 0; d < 5; ++d) {
+              const int qd = P.cdim_q[d];
+              c[d] = cbase[d] + (qd == 1 ? q * P.c_slab : qd == 2 ? ch * 32 : 0);
+            }
+            tma_store(&Pg.tc, buf, c, atomic);
+          }
+        }
+        if (chunk >= 0 && lane == 0) bulk_wait_all();  // tail chunk: writes done before its flag
+      } else {
+#pragma unroll 1
+        for (int ch = 0; ch < nch; ++ch) {
+          tmem_ld32_issue(t_base + ch * 32, ra);
+          tmem_ld_wait(ra);
+          process(ra, ch);
+        }
       }
       if (est) stamp_it(P, 2, static_cast<uint32_t>(local / ngrp) * 4 + 3);
       if (chunk >= 0) {  // tail chunk stored / added: count it; the last one resets the flag
@@ -979,6 +1040,7 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
       else
         mbar_arrive(&tempty[acc]);  // accumulator may be overwritten by tile t+2
     }
+    if (P.c_tma && lane == 0) bulk_wait_all();  // bulk stores complete before the CTA exits
     if (threadIdx.x == 64) stamp(P, 5);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1115,6 +1177,16 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
   if (plan.cached_b != B) {
     if (!encode(&P.tb, B, plan.gdim_b, plan.gstride_b, plan.box_b, plan.swz_b)) return cudaErrorInvalidValue;
     plan.cached_b = B;
+  }
+  if (P.c_tma) {
+    // (a caller's output that is not 16-B aligned falls back to the per-thread stores)
+    const bool al = (reinterpret_cast<uintptr_t>(C) & 15u) == 0;
+    if (!al) {
+      P.c_tma = 0;
+    } else if (plan.cached_c != C) {
+      if (!encode(&P.tc, C, plan.gdim_c, plan.gstride_c, plan.box_c, plan.swz_c)) return cudaErrorInvalidValue;
+      plan.cached_c = C;
+    }
   }
   if (static_cast<int64_t>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_split >= (1ll << 32))
     return cudaErrorInvalidConfiguration;

@@ -79,7 +79,17 @@ struct TcOperand {
 struct TcParams {
   CUtensorMap ta;     // 64-byte aligned, first members
   CUtensorMap tb;
+  CUtensorMap tc;     // C, for the TMA-store epilogue (c_tma != 0)
   TcOperand oa, ob;
+  // TMA-store epilogue: each epilogue warp stages its 32-row x 32-column block of a chunk in
+  // shared memory and one lane issues a bulk tensor store (or, for split-K / tail chunks, a
+  // bulk tensor reduce-add) -- asynchronous full-line writes instead of per-thread stores.
+  // c_tma: 0 off, 1 rows innermost in C (block staged column-major), 2 columns innermost
+  // (row-major, 128B swizzle).  TMA dim d of C carries unit cdim_u[d] (-1 none) plus the
+  // warp's row offset (cdim_q[d] == 1) or the chunk's column offset (cdim_q[d] == 2).
+  int32_t c_tma;
+  int32_t cdim_u[5], cdim_q[5];
+  int32_t c_slab;     // rows of the outermost M unit per warp (its coordinate advances by q * c_slab)
   TcUnit u[TC_MAX_UNITS];
   int32_t nunits;
   int32_t nm, mt[3];      // M-tile units, row order fastest first
@@ -145,6 +155,11 @@ struct TcPlan {
   uint64_t gstride_a[5]{}, gstride_b[5]{};  // bytes, [0] unused
   uint32_t box_a[5]{}, box_b[5]{};
   int swz_a = 3, swz_b = 3;   // CUtensorMapSwizzle: 3 128B (K-major), 4 128B_ATOM_32B (native MN-major), 0 none (wide)
+  // C tensor map geometry for the TMA-store epilogue (params.c_tma != 0)
+  uint64_t gdim_c[5]{}, gstride_c[5]{};
+  uint32_t box_c[5]{};
+  int swz_c = 0;
+  const void* cached_c = nullptr;
   int64_t out_span = 0;       // elements of C to zero before a split-K launch
   uint32_t* tail_flags = nullptr;  // kTailFlags zeroed words owned by the executor (tail split)
   const void* cached_a = nullptr;

@@ -1159,9 +1159,9 @@ std::string Executor::describe() const {
       if (st.kind == Step::kTc) {
         const TcParams& P = st.tc.params;
         std::snprintf(line + n, sizeof line - n,
-                      " bn=%d rows=%d cols=%d mma_n=%d tiles=%dx%dx%d split=%d kit=%d amn=%d bmn=%d tr=%d mc=%d\n", st.tc.bn,
+                      " bn=%d rows=%d cols=%d mma_n=%d tiles=%dx%dx%d split=%d kit=%d amn=%d bmn=%d tr=%d mc=%d ctma=%d\n", st.tc.bn,
                       P.m_rows, P.n_cols, P.n_mma, P.tiles_m, P.tiles_n, P.grid_z, P.k_split, P.k_iters, P.oa.mn_major,
-                      P.ob.mn_major, P.transpose_store, P.mcast);
+                      P.ob.mn_major, P.transpose_store, P.mcast, P.c_tma);
         if (std::getenv("CE_DESCRIBE_UNITS")) {
           std::string u = " ";
           n = static_cast<int>(std::strlen(line)) - 1;  // before the newline

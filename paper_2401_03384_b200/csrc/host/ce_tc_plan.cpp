@@ -10,6 +10,7 @@
 // not multiple of 16 B, no unit-stride axis) returns false and the executor uses
 // the SIMT kernels (ce_simt.cu).
 #include <algorithm>
+#include <cstdio>
 #include <functional>
 #include <cstdint>
 #include <cstdlib>
@@ -692,6 +693,81 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     P.dsplit = tc_div(static_cast<uint32_t>(pm * P.tiles_n * P.grid_z));
     P.k_per = (P.k_iters + P.k_split - 1) / P.k_split;
     if (pm * P.tiles_n * P.grid_z * P.k_split >= (1ll << 31)) return fail("too many work items");
+  }
+  // TMA-store epilogue (TcParams::c_tma): C must be a <= 5-D tensor map over the tile units --
+  // the M units (a warp's 32 rows = full boxes of the inner M units times an even share of
+  // the outermost one), one N unit (32-column chunks), the grid units, each unit's vars
+  // chaining in C, and the M or N inner var C's unit-stride axis.  No box may reach into a
+  // neighbouring tile (N tiles multiples of 32 or a single N tile; past the tensor's extent
+  // TMA clips).  CE_TC_CTMA=0 off.
+  {
+    static const bool ctma_on = [] {
+      const char* e = std::getenv("CE_TC_CTMA");
+      return !(e && *e == '0');
+    }();
+    P.c_tma = 0;
+    auto chain = [&](const TcUnit& u) {
+      for (int k = 1; k < u.nv; ++k)
+        if (u.sc[k] != u.sc[k - 1] * u.vext[k - 1]) return false;
+      return true;
+    };
+    bool ok = ctma_on && P.nm >= 1 && P.nn == 1 && P.mcast == 0 && P.nm + 1 + P.ng <= 5;
+    int64_t inner_rows = 1;  // rows of a warp's slab covered by the M units below the last
+    for (int i = 0; ok && i + 1 < P.nm; ++i) inner_rows *= P.u[P.mt[i]].box;
+    const int64_t slab_last = ok ? 32 / std::max<int64_t>(inner_rows, 1) : 0;  // last M unit's share per warp
+    if (ok) {
+      const TcUnit& ul = P.u[P.mt[P.nm - 1]];
+      ok = inner_rows <= 32 && 32 % inner_rows == 0 && slab_last > 0 && ul.box % slab_last == 0 &&
+           inner_rows * ul.box == P.m_rows;
+    }
+    for (int i = 0; ok && i < P.nm; ++i) ok = chain(P.u[P.mt[i]]);
+    const TcUnit& un = P.u[P.nt[0]];
+    ok = ok && chain(un) && (P.n_cols % 32 == 0 || P.tiles_n == 1);
+    for (int i = 0; i < P.ng && ok; ++i) ok = chain(P.u[P.gu[i]]);
+    if (ok) {
+      const TcUnit& um0 = P.u[P.mt[0]];
+      const bool rows_inner = um0.sc[0] == 1 && P.nm == 1;
+      const bool cols_inner = un.sc[0] == 1;
+      ok = rows_inner != cols_inner;
+      // every stride but the inner one 16-B aligned
+      for (int i = 0; ok && i < P.nm; ++i) ok = (rows_inner && i == 0) || P.u[P.mt[i]].sc[0] % 4 == 0;
+      ok = ok && (cols_inner || un.sc[0] % 4 == 0);
+      for (int i = 0; ok && i < P.ng; ++i) ok = P.u[P.gu[i]].sc[0] % 4 == 0;
+      if (ok) {
+        P.c_tma = rows_inner ? 1 : 2;
+        int d = 0;
+        auto put = [&](int unit, int q, uint32_t box) {
+          const TcUnit& u = P.u[unit];
+          P.cdim_u[d] = unit;
+          P.cdim_q[d] = q;
+          plan->gdim_c[d] = static_cast<uint64_t>(u.ext);
+          plan->gstride_c[d] = static_cast<uint64_t>(u.sc[0]) * 4;
+          plan->box_c[d] = box;
+          ++d;
+        };
+        auto put_rows = [&] {  // M units fastest first; the last one carries the warp offset
+          for (int i = 0; i + 1 < P.nm; ++i) put(P.mt[i], 0, static_cast<uint32_t>(P.u[P.mt[i]].box));
+          put(P.mt[P.nm - 1], 1, static_cast<uint32_t>(slab_last));
+        };
+        if (rows_inner) {
+          put_rows();
+          put(P.nt[0], 2, 32);
+        } else {
+          put(P.nt[0], 2, 32);
+          put_rows();
+        }
+        for (int i = 0; i < P.ng; ++i) put(P.gu[i], 0, 1);
+        for (; d < 5; ++d) {
+          P.cdim_u[d] = -1;
+          P.cdim_q[d] = 0;
+          plan->gdim_c[d] = 1;
+          plan->gstride_c[d] = plan->gstride_c[d - 1] * plan->gdim_c[d - 1];
+          plan->box_c[d] = 1;
+        }
+        P.c_slab = static_cast<int32_t>(slab_last);
+        plan->swz_c = rows_inner ? 0 : 3;  // CU_TENSOR_MAP_SWIZZLE_128B for row-major 128-B rows
+      }
+    }
   }
   plan->valid = 1;
   plan->why = "ok";

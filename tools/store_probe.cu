@@ -25,6 +25,22 @@ __global__ void st_rows_v4(float* C, int ncol, long cstride, long tile_stride, i
       *reinterpret_cast<float4*>(base + c * cstride) = make_float4(c, c, c, c);
   }
 }
+// TC epilogue transposed-store pattern: a warp owns 32 rows x NCOL columns of a row-major C
+// (pitch floats); per 32-column chunk, 8 instructions each storing 4 rows x 128 B (lane ->
+// row 4k + lane/8, columns 4*(lane%8)).
+__global__ void st_tr(float* C, int ncol, long pitch, int tiles_per_cta) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int t = 0; t < tiles_per_cta; ++t) {
+    const long row0 = ((long)(blockIdx.x * tiles_per_cta + t) * (blockDim.x / 32) + warp) * 32;
+    for (int ch = 0; ch < ncol / 32; ++ch) {
+#pragma unroll 4
+      for (int k = 0; k < 8; ++k) {
+        const long r = row0 + 4 * k + (lane >> 3);
+        *reinterpret_cast<float4*>(C + r * pitch + ch * 32 + 4 * (lane & 7)) = make_float4(k, k, k, k);
+      }
+    }
+  }
+}
 int main() {
   const long cstride = 196;
   float* C;
@@ -47,6 +63,20 @@ int main() {
         float ms; cudaEventElapsedTime(&ms, a, b);
         double gb = (double)ctas * tiles * warps * 32 * ncol * 4 / 1e9;
         if (it == 2) printf("v4=%d warps=%2d ctas=%3d  %.2f us  %.0f GB/s  per-CTA %.1f GB/s\n", v4, warps, ctas, ms * 1e3, gb / (ms * 1e-3), gb / (ms * 1e-3) / ctas);
+      }
+    }
+  for (int warps : {4, 8})
+    for (int ctas : {148, 296}) {
+      const int ncol = 224, tiles = 1;
+      const long pitch = 232;
+      for (int it = 0; it < 3; ++it) {
+        cudaEventRecord(a);
+        st_tr<<<ctas, 32 * warps>>>(C, ncol, pitch, tiles);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        double gb = (double)ctas * tiles * warps * 32 * ncol * 4 / 1e9;
+        if (it == 2) printf("tr warps=%d ctas=%3d  %.2f us  %.0f GB/s  per-CTA %.1f GB/s\n", warps, ctas, ms * 1e3, gb / (ms * 1e-3), gb / (ms * 1e-3) / ctas);
       }
     }
   return 0;
