@@ -79,13 +79,15 @@ struct Group {
 // Merge var `outer` onto group g if it continues g's innermost-first stride chain
 // in every TMA operand (A, B).  Out strides are not required to chain: the
 // epilogue decomposes units back into vars.
-bool chains(const CeProblem& p, const Group& g, int outer) {
+bool chains(const CeProblem& p, const Group& g, int outer, bool in_c) {
   const int inner = g.vars.back();
   for (const int64_t* s : {p.sa, p.sb}) {
     const bool hi = s[inner] != 0, ho = s[outer] != 0;
     if (hi != ho) return false;
     if (hi && s[outer] != s[inner] * p.ext[inner]) return false;
   }
+  // (in_c: the unit must also be one strided axis of C, so a TMA map can store its tiles)
+  if (in_c && p.sc[inner] && p.sc[outer] != p.sc[inner] * p.ext[inner]) return false;
   return true;
 }
 
@@ -97,7 +99,31 @@ int64_t pow2ceil(int64_t x) {
 
 }  // namespace
 
+namespace {
+bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c);
+}
+
+// The plan proper; short-K launches (stores dominate) whose units do not chain in C are
+// re-planned with units that do, so the TMA-store epilogue can take them (e.g. a [b,t,h,w]
+// output of a rank -> channel GEMM: one [h w] x t tile per sample instead of tiles across b).
 bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
+  if (!tc_plan_impl(p, plan, false)) return false;
+  // opt-in (CE_TC_CTMA_RECHAIN=1): the re-chained tiles (2 per 14x14 sample, one ragged) cost
+  // what the faster stores save -- cfg2 step 1.118-1.125 vs 1.103-1.141 ms (same-box A/B x3)
+  static const bool rechain = [] {
+    const char* e = std::getenv("CE_TC_CTMA_RECHAIN");
+    return e && *e == '1';
+  }();
+  if (rechain && plan->params.c_tma == 0 && plan->params.k_iters <= 8 && plan->params.k_split == 1) {
+    TcPlan alt;
+    const bool ok2 = tc_plan_impl(p, &alt, true);
+    if (ok2 && alt.params.c_tma != 0) *plan = alt;
+  }
+  return true;
+}
+
+namespace {
+bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
   *plan = TcPlan{};
   auto fail = [&](const char* why) {
     plan->valid = 0;
@@ -129,7 +155,7 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
       for (std::size_t gi = 0; gi < groups.size() && !merged; ++gi) {
         Group& g = groups[gi];
         if (g.cls != p.cls[v] || in_gather(p, g.vars.back()) || g.vars.size() >= 4) continue;
-        if (chains(p, g, v)) {
+        if (chains(p, g, v, units_chain_in_c)) {
           g.vars.push_back(v);
           g.ext *= p.ext[v];
           unit_of[static_cast<std::size_t>(v)] = static_cast<int>(gi);
@@ -291,6 +317,9 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
       cand.push_back(u);
     }
     if (cand.empty()) return rows;
+    // (re-planned for the TMA-store epilogue: one M unit, C's unit-stride one when it leads,
+    // so each warp's 32 rows are 128 contiguous bytes of C per column)
+    if (units_chain_in_c && cls == CE_M && cand.size() > 1) cand.erase(cand.begin() + 1, cand.end());
     // Boxes minimising the number of tiles (every tile costs a full M=128 / N MMA), then
     // maximising the rows used: e.g. a 14x14 image stack tiles as [14 w][1 h][9 b] (98%
     // of the rows useful) instead of [14 w][9 h] (77%).
@@ -726,7 +755,7 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
     for (int i = 0; i < P.ng && ok; ++i) ok = chain(P.u[P.gu[i]]);
     if (ok) {
       const TcUnit& um0 = P.u[P.mt[0]];
-      const bool rows_inner = um0.sc[0] == 1 && P.nm == 1;
+      const bool rows_inner = um0.sc[0] == 1;
       const bool cols_inner = un.sc[0] == 1;
       ok = rows_inner != cols_inner;
       // every stride but the inner one 16-B aligned
@@ -773,3 +802,4 @@ bool ce_tc_plan(const CeProblem& p, TcPlan* plan) {
   plan->why = "ok";
   return true;
 }
+}  // namespace
