@@ -218,15 +218,37 @@ RESNET34 = [(3, 64, 7, 112, 1), (64, 64, 3, 56, 6), (64, 128, 3, 28, 1), (128, 1
 
 
 def time_cfg3_stack(ctx, flush, iters=2):
-    """cfg3: tensor-ring reshaped (M=3) ResNet-34 conv stack, batch 256, cr 0.1, fwd+bwd.
-    Each distinct layer shape (stride-2 layers run stride-1 at output resolution) is timed
-    (median of `iters` after a warm-up, L2 flushed) and weighted by its count in the 33 convs."""
+    """cfg3: tensor-ring reshaped (M=3) ResNet-34 conv stack, batch 256, cr 0.1, fwd+bwd."""
+    r = time_stack(ctx, flush, "rtr", 256, 0.1, iters)
+    r["workload"] = "cfg3 RTR (M=3) ResNet-34 conv stack, batch 256, cr 0.1, fwd+bwd, 33 convs"
+    return r
+
+
+def time_cfg4_stack(ctx, flush, iters=2):
+    """cfg4: CP ResNet-34 conv stack, the per-GPU shard of global batch 1024 over 8 GPUs (128),
+    cr 0.1 and 1.0, fwd+bwd (one GPU: the factor-gradient all-reduce is measured by --gpus N)."""
+    out = {"workload": "cfg4 CP ResNet-34 conv stack, per-GPU batch 128 (1024 / 8), fwd+bwd, 33 convs"}
+    for cr in (0.1, 1.0):
+        r = time_stack(ctx, flush, "cp", 128, cr, iters)
+        r["images_per_s_per_gpu"] = round(128 / (r["stack_fwd_bwd_ms"] * 1e-3), 1)
+        out[f"cr{cr}"] = r
+    return out
+
+
+def time_stack(ctx, flush, kind, batch, cr, iters=2):
+    """A ResNet-34 conv stack of `kind` layers: each distinct layer shape (stride-2 layers run
+    stride-1 at output resolution) is timed (median of `iters` after a warm-up, L2 flushed)
+    and weighted by its count in the 33 convs."""
     import torch
     import paper_2401_03384_b200 as ce
     from paper_2401_03384_b200.device import Executor
     tot_ms, tot_fl, per = 0.0, 0.0, {}
     for s, t, k, hp, count in RESNET34:
-        le = ce.expression(ce.LayerSpec("rtr", RTR_FACT[t], RTR_FACT[s], k, k, hp, hp, 256, [1, 1, 1, 1]), 0.1)
+        if kind == "rtr":
+            spec = ce.LayerSpec("rtr", RTR_FACT[t], RTR_FACT[s], k, k, hp, hp, batch, [1, 1, 1, 1])
+        else:
+            spec = ce.LayerSpec(kind, [t], [s], k, k, hp, hp, batch, [1])
+        le = ce.expression(spec, cr)
         plan = ce.optimal(le.expr, le.dims, "same", "training")
         ex = Executor(ctx, plan, backward=True)
         xs = [ctx.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
@@ -252,8 +274,7 @@ def time_cfg3_stack(ctx, flush, iters=2):
         tot_fl += count * fl
         del ex, xs, dout, out
         torch.cuda.empty_cache()
-    return {"workload": "cfg3 RTR (M=3) ResNet-34 conv stack, batch 256, cr 0.1, fwd+bwd, 33 convs",
-            "stack_fwd_bwd_ms": round(tot_ms, 2), "tflops": round(tot_fl / (tot_ms * 1e-3) / 1e12, 2),
+    return {"stack_fwd_bwd_ms": round(tot_ms, 2), "tflops": round(tot_fl / (tot_ms * 1e-3) / 1e12, 2),
             "per_layer_ms": per}
 
 
@@ -283,13 +304,15 @@ def main():
     from paper_2401_03384_b200.device import Context, Executor
     from paper_2401_03384_b200.parallel import allreduce_factor_grads, allreduce_factor_grads_async
 
-    # CE_BENCH_BACKEND=gloo + CE_BENCH_SHARE_GPU=1 exercise the multi-rank path of this
-    # script on a single GPU (test only; the measured path is NCCL, one GPU per rank)
-    if os.environ.get("CE_BENCH_SHARE_GPU") == "1":
+    # CE_BENCH_SHARE_GPU=1 exercises the multi-rank path of this script with more ranks than
+    # GPUs (test only: NCCL refuses two ranks on one device, so the collectives go over gloo;
+    # the measured path is NCCL, one GPU per rank)
+    share = os.environ.get("CE_BENCH_SHARE_GPU") == "1"
+    if share:
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        backend = os.environ.get("CE_BENCH_BACKEND", "nccl")
+        backend = os.environ.get("CE_BENCH_BACKEND", "gloo" if share else "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
@@ -501,12 +524,13 @@ def main():
                        for (n, k, t, fl, by) in kern], f, indent=1)
 
     # ---------------------------------------------------------------- cfg3 stack (largest single-GPU config)
-    cfg3 = None
+    cfg3 = cfg4 = None
     if rank == 0 and world == 1 and not args.no_cfg3:
         for l in layers:
             l.clear()
         torch.cuda.empty_cache()
         cfg3 = time_cfg3_stack(ctx, flush)
+        cfg4 = time_cfg4_stack(ctx, flush)
 
     # ---------------------------------------------------------------- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -537,6 +561,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "cfg3_stack": cfg3,
+            "cfg4_stack": cfg4,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
