@@ -44,8 +44,16 @@ def parse(expr: str):
     return ins, o, [a for a in o if a in cl]
 
 
+def split_mode(mode):
+    """"same" -> ("same", 1); "same/2" -> ("same", 2): the strided extension (ConvModeSpec in
+    csrc/host/ce_ir.hpp; outside the reference's semantics)."""
+    kind, _, st = mode.partition("/")
+    return kind, int(st) if st else 1
+
+
 def conv_output_dim(mode, x, l):
-    return {"full": x + l - 1, "same": x, "valid": x - l + 1, "circular": x}[mode]
+    kind, s = split_mode(mode)
+    return {"full": (x + l - 2) // s + 1, "same": -(-x // s), "valid": (x - l) // s + 1, "circular": -(-x // s)}[kind]
 
 
 def resolve_modes(ins, convs, mode):
@@ -60,6 +68,7 @@ class ConvAxis:
     feature: int
     filter: int
     out: int
+    stride: int = 1
 
 
 @dataclass
@@ -87,7 +96,9 @@ def make_op(left, ldims, right, rdims, keep, modes, result=None) -> Op:
         if a in right:
             dl, dr = ldims[i], rdims[right.index(a)]
             if a in modes:
-                ax = ConvAxis(a, modes[a], dl >= dr, max(dl, dr), min(dl, dr), conv_output_dim(modes[a], max(dl, dr), min(dl, dr)))
+                kind, st = split_mode(modes[a])
+                ax = ConvAxis(a, kind, dl >= dr, max(dl, dr), min(dl, dr),
+                              conv_output_dim(modes[a], max(dl, dr), min(dl, dr)), st)
                 op.conv.append(ax)
                 kept[a] = ax.out
                 continue
@@ -119,7 +130,8 @@ def same_offset(l):
 
 
 def feature_index(ax: ConvAxis, n, k):
-    """Vectorised feature_index (kernels.cpp:298-315): (x, valid)."""
+    """Vectorised feature_index (kernels.cpp:298-315): (x, valid); a strided axis reads s*n."""
+    n = n * ax.stride
     if ax.mode == "full":
         x = n - k
     elif ax.mode == "same":
@@ -267,7 +279,10 @@ def flops_actual(op: Op) -> int:
     for a in op.batch + op.contract + op.lfree + op.rfree:
         f *= op.dim[a]
     for ax in op.conv:
-        if ax.mode in ("full", "circular"):
+        if ax.stride > 1:  # (extension) in-range (n, k) pairs counted directly
+            n_, k_ = np.meshgrid(np.arange(ax.out), np.arange(ax.filter), indexing="ij")
+            f *= int(feature_index(ax, n_, k_)[1].sum())
+        elif ax.mode in ("full", "circular"):
             f *= ax.feature * ax.filter
         elif ax.mode == "valid":
             f *= (ax.feature - ax.filter + 1) * ax.filter

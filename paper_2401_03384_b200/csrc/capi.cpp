@@ -125,7 +125,7 @@ void split_u128(u128 v, uint64_t* lo, uint64_t* hi) {
 // that must name every convolution atom of the expression (and nothing else).
 ConvModeMap modes_arg(const ExpressionSpec& spec, const char* mode) {
   const std::string m(mode ? mode : "");
-  if (m.find('=') == std::string::npos) return resolve_conv_modes(spec, conv_mode_from_string(m));
+  if (m.find('=') == std::string::npos) return resolve_conv_modes(spec, conv_mode_spec_from_string(m));
   ConvModeMap out;
   std::size_t pos = 0;
   while (pos <= m.size()) {
@@ -138,7 +138,7 @@ ConvModeMap modes_arg(const ExpressionSpec& spec, const char* mode) {
     const Atom a(name);
     if (!spec.is_conv(a)) throw ShapeError("mode map names '" + name + "', which is not a convolution atom");
     if (out.count(a)) throw ShapeError("mode map names '" + name + "' twice");
-    out[a] = conv_mode_from_string(item.substr(eq + 1));
+    out[a] = conv_mode_spec_from_string(item.substr(eq + 1));
     pos = end + 1;
   }
   for (const auto& a : spec.conv_atoms)

@@ -1119,16 +1119,60 @@ void Executor::build_backward() {
       const auto id = static_cast<std::size_t>(ids[s]);
       const Adjoint which = s == 0 ? Adjoint::GradLeft : Adjoint::GradRight;
       const std::string label = "grad:" + std::to_string(id);
-      const BufRef a = s == 0 ? gref[cid] : red_ref_[0][jj];
-      const BufRef b = s == 0 ? red_ref_[1][jj] : gref[cid];
+      // Strided conv axes (extension) whose feature is this operand: x = s*n + ... has no
+      // affine inverse, so dC is upsampled (zeros between the s-spaced outputs) and the
+      // gradient lowered as the stride-1 op over the upsampled positions j = s*n.
+      PairwiseOp gop = op;
+      View dcv = gview[cid];
+      BufRef dcr = gref[cid];
+      {
+        std::vector<int64_t> up_dims = dcv.dims;
+        bool any = false;
+        for (ConvAxis& ax : gop.conv_axes) {
+          if (ax.stride == 1 || ax.feature_on_left != (s == 0)) continue;
+          const int r = find_atom(gop.result, ax.atom);
+          // j = s*n < s*out; a circular axis keeps the feature length (its wrap is mod X, and
+          // s*(out-1) < X), so the stride-1 op is exactly the reference's circular map
+          ax.output_dim = ax.mode == ConvMode::Circular ? ax.feature_dim : ax.output_dim * ax.stride;
+          ax.stride = 1;
+          gop.result_dims[static_cast<std::size_t>(r)] = ax.output_dim;
+          const int d = find_atom(dcv.subs, ax.atom);
+          up_dims[static_cast<std::size_t>(d)] = ax.output_dim;
+          any = true;
+        }
+        if (any) {
+          const View up = padded_view(dcv.subs, up_dims, 4);
+          const BufRef upr{BufRef::kWork, alloc(view_span(up))};
+          Step z;
+          z.kind = Step::kZero;
+          z.c = upr;
+          z.zero_elems = view_span(up);
+          z.node = static_cast<int>(id);
+          z.label = label + ":upsample-zero";
+          bwd_.push_back(z);
+          // dC[.., n, ..] -> up[.., s*n, ..]: the up view with the strided atoms' strides scaled
+          View dst = up;
+          dst.dims = dcv.dims;
+          for (const ConvAxis& ax : op.conv_axes)
+            if (ax.stride != 1 && ax.feature_on_left == (s == 0))
+              dst.strides[static_cast<std::size_t>(find_atom(dst.subs, ax.atom))] *= ax.stride;
+          pending_flops_ = 0;
+          add_problem(bwd_, lower_unary(dcv, dst), dcr, {}, upr, static_cast<int>(id), label + ":upsample");
+          pending_flops_ = 2.0 * static_cast<double>(flops_actual(op));
+          dcv = up;
+          dcr = upr;
+        }
+      }
+      const BufRef a = s == 0 ? dcr : red_ref_[0][jj];
+      const BufRef b = s == 0 ? red_ref_[1][jj] : dcr;
       if (selfs[s]->empty()) {
-        add_problem(bwd_, lower_pairwise(op, red_view_[0][jj], red_view_[1][jj], gview[cid], gview[id], which), a, b,
+        add_problem(bwd_, lower_pairwise(gop, red_view_[0][jj], red_view_[1][jj], dcv, gview[id], which), a, b,
                     gref[id], static_cast<int>(id), label);
       } else {
         // d(reduced) then broadcast back over the self-contracted atoms
         View tmp = padded_view(red_view_[s][jj].subs, red_view_[s][jj].dims, 4);
         BufRef tref{BufRef::kWork, alloc(view_span(tmp))};
-        add_problem(bwd_, lower_pairwise(op, red_view_[0][jj], red_view_[1][jj], gview[cid], tmp, which), a, b, tref,
+        add_problem(bwd_, lower_pairwise(gop, red_view_[0][jj], red_view_[1][jj], dcv, tmp, which), a, b, tref,
                     static_cast<int>(id), label);
         pending_flops_ = 0;
         add_problem(bwd_, lower_unary(tmp, gview[id]), tref, {}, gref[id], static_cast<int>(id), label + ":bcast");

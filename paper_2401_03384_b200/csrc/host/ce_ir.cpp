@@ -8,6 +8,7 @@
 #include "ce_ir.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cctype>
 
 namespace ce {
@@ -303,22 +304,33 @@ ConvMode conv_mode_from_string(std::string_view s) {
   throw std::invalid_argument("unknown conv mode: " + std::string(s));
 }
 
-int64_t conv_output_dim(ConvMode mode, int64_t feature, int64_t filter) {
+ConvModeSpec conv_mode_spec_from_string(std::string_view s) {
+  const std::size_t slash = s.find('/');
+  if (slash == std::string_view::npos) return ConvModeSpec(conv_mode_from_string(s));
+  const std::string st(s.substr(slash + 1));
+  char* end = nullptr;
+  const long long v = std::strtoll(st.c_str(), &end, 10);
+  if (st.empty() || *end != '\0' || v < 1) throw std::invalid_argument("bad conv stride in '" + std::string(s) + "'");
+  return ConvModeSpec(conv_mode_from_string(s.substr(0, slash)), v);
+}
+
+int64_t conv_output_dim(ConvMode mode, int64_t feature, int64_t filter, int64_t stride) {
+  const int64_t s = stride;
   switch (mode) {
-    case ConvMode::Full: return feature + filter - 1;
+    case ConvMode::Full: return (feature + filter - 2) / s + 1;
     case ConvMode::Valid:
       if (feature < filter) throw ShapeError("valid convolution requires feature >= filter");
-      return feature - filter + 1;
+      return (feature - filter) / s + 1;
     case ConvMode::Same:
-    case ConvMode::Circular: return feature;
+    case ConvMode::Circular: return (feature + s - 1) / s;
   }
   return 0;
 }
 
-ConvModeMap resolve_conv_modes(const ExpressionSpec& spec, ConvMode requested) {
+ConvModeMap resolve_conv_modes(const ExpressionSpec& spec, ConvModeSpec requested) {
   ConvModeMap m;
   for (const auto& a : spec.conv_atoms)
-    m[a] = spec.occurrence_count(a) >= 3 ? ConvMode::Circular : requested;
+    m[a] = spec.occurrence_count(a) >= 3 ? ConvModeSpec(ConvMode::Circular) : requested;
   return m;
 }
 
@@ -343,11 +355,12 @@ PairwiseOp make_pairwise_op(const Subscripts& left, const std::vector<int64_t>& 
     if (mode != conv_modes.end()) {
       ConvAxis ax;
       ax.atom = a;
-      ax.mode = mode->second;
+      ax.mode = mode->second.mode;
+      ax.stride = mode->second.stride;
       ax.feature_on_left = dl >= dr;
       ax.feature_dim = std::max(dl, dr);
       ax.filter_dim = std::min(dl, dr);
-      ax.output_dim = conv_output_dim(ax.mode, ax.feature_dim, ax.filter_dim);
+      ax.output_dim = conv_output_dim(ax.mode, ax.feature_dim, ax.filter_dim, ax.stride);
       kept_dim[a] = ax.output_dim;
       op.conv_axes.push_back(ax);
       return;
@@ -414,6 +427,18 @@ u128 non_conv_product(const PairwiseOp& op) {
 
 // Number of (n, k) pairs the direct loop visits on one conv axis.
 int64_t conv_pairs(const ConvAxis& ax) {
+  if (ax.stride > 1) {  // (extension) count the in-range feature indices directly
+    if (ax.mode == ConvMode::Circular) return ax.output_dim * ax.filter_dim;
+    const int64_t s = ax.stride, c = ax.mode == ConvMode::Same ? same_offset(ax.filter_dim) : 0;
+    const int64_t sq = ax.mode == ConvMode::Valid ? 1 : -1;
+    int64_t count = 0;
+    for (int64_t n = 0; n < ax.output_dim; ++n)
+      for (int64_t k = 0; k < ax.filter_dim; ++k) {
+        const int64_t x = s * n + c + sq * k;
+        count += x >= 0 && x < ax.feature_dim;
+      }
+    return count;
+  }
   switch (ax.mode) {
     case ConvMode::Full:
     case ConvMode::Circular: return ax.feature_dim * ax.filter_dim;
@@ -437,7 +462,7 @@ int64_t conv_pairs(const ConvAxis& ax) {
 u128 flops_actual(const PairwiseOp& op) {
   u128 f = non_conv_product(op);
   for (const auto& ax : op.conv_axes) {
-    u128 pairs = ax.mode == ConvMode::Same ? static_cast<u128>(conv_pairs(ax))
+    u128 pairs = (ax.mode == ConvMode::Same || ax.stride > 1) ? static_cast<u128>(conv_pairs(ax))
                  : ax.mode == ConvMode::Valid
                      ? mul_checked(static_cast<u128>(ax.feature_dim - ax.filter_dim + 1),
                                    static_cast<u128>(ax.filter_dim))
@@ -463,7 +488,8 @@ CostBreakdown pairwise_cost(const PairwiseOp& op, CostMode mode) {
   for (const auto& ax : op.conv_axes) {
     const u128 x = static_cast<u128>(ax.feature_dim), l = static_cast<u128>(ax.filter_dim),
                xo = static_cast<u128>(ax.output_dim);
-    c.forward = mul_checked(c.forward, mul_checked(x, l));
+    // (a strided axis -- extension -- visits output x filter pairs, not feature x filter)
+    c.forward = mul_checked(c.forward, mul_checked(ax.stride > 1 ? xo : x, l));
     c.g1 = mul_checked(c.g1, mul_checked(xo, l));
     c.g2 = mul_checked(c.g2, mul_checked(x, xo));
   }

@@ -93,9 +93,22 @@ struct SplitMix64 {
 enum class ConvMode { Full, Same, Valid, Circular };
 const char* to_string(ConvMode m);
 ConvMode conv_mode_from_string(std::string_view s);
-int64_t conv_output_dim(ConvMode mode, int64_t feature, int64_t filter);
-using ConvModeMap = std::map<Atom, ConvMode>;
-ConvModeMap resolve_conv_modes(const ExpressionSpec& spec, ConvMode requested);
+// Extension (outside the reference semantics): a conv atom may
+// carry an output stride s ("same/2"): output position n reads feature index s*n + (the
+// stride-1 map's offset), e.g. Same x = s*n + floor((L-1)/2) - k, and the output length
+// becomes Full floor((X+L-2)/s)+1, Same / Circular ceil(X/s), Valid floor((X-L)/s)+1.  Stride 1
+// is exactly the reference's ConvMode (kernels.hpp:15-33), bit-exact everywhere.
+struct ConvModeSpec {
+  ConvMode mode = ConvMode::Same;
+  int64_t stride = 1;
+  ConvModeSpec() = default;
+  ConvModeSpec(ConvMode m, int64_t s = 1) : mode(m), stride(s) {}  // NOLINT: implicit from ConvMode
+  operator ConvMode() const { return mode; }                       // NOLINT
+};
+ConvModeSpec conv_mode_spec_from_string(std::string_view s);  // "same" | "same/2"
+int64_t conv_output_dim(ConvMode mode, int64_t feature, int64_t filter, int64_t stride = 1);
+using ConvModeMap = std::map<Atom, ConvModeSpec>;
+ConvModeMap resolve_conv_modes(const ExpressionSpec& spec, ConvModeSpec requested);
 inline int64_t same_offset(int64_t filter) { return (filter - 1) / 2; }
 
 // ---- pairwise op (kernels.hpp:35-72) --------------------------------------------
@@ -106,6 +119,7 @@ struct ConvAxis {
   int64_t feature_dim = 1;
   int64_t filter_dim = 1;
   int64_t output_dim = 1;
+  int64_t stride = 1;  // extension, see ConvModeSpec
 };
 
 struct PairwiseOp {

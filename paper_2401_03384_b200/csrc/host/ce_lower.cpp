@@ -4,6 +4,8 @@
 #include <cstdlib>
 #include "ce_lower.hpp"
 
+#include <stdexcept>
+
 #include <algorithm>
 #include <numeric>
 
@@ -98,15 +100,17 @@ struct Affine {
   int64_t c;
   bool wrap;
 };
-// x = f(n, k): the forward feature index (kernels.cpp:298-315).
+// x = f(n, k): the forward feature index (kernels.cpp:298-315); a strided axis (extension,
+// ConvModeSpec) scales the output position: x = s*n + ...
 Affine forward_map(const ConvAxis& ax) {
+  const int s = static_cast<int>(ax.stride);
   switch (ax.mode) {
-    case ConvMode::Full: return {1, -1, 0, false};
-    case ConvMode::Same: return {1, -1, same_offset(ax.filter_dim), false};
-    case ConvMode::Valid: return {1, 1, 0, false};
-    case ConvMode::Circular: return {1, -1, 0, true};
+    case ConvMode::Full: return {s, -1, 0, false};
+    case ConvMode::Same: return {s, -1, same_offset(ax.filter_dim), false};
+    case ConvMode::Valid: return {s, 1, 0, false};
+    case ConvMode::Circular: return {s, -1, 0, true};
   }
-  return {1, -1, 0, false};
+  return {s, -1, 0, false};
 }
 // n = g(x, k): which output position a feature element x meets tap k at.
 Affine inverse_map(const ConvAxis& ax) {
@@ -168,6 +172,9 @@ CeProblem lower_pairwise(const PairwiseOp& op, const View& left, const View& rig
     const View& dc = dc_on_a ? *A : *B;
     const View& other = dc_on_a ? *B : *A;
     if (grad_is_feature) {
+      // (a strided axis has no affine inverse: the executor upsamples dC and lowers a
+      // stride-1 op over it, see Executor::build_backward)
+      if (ax.stride != 1) throw std::logic_error("lower_pairwise: strided feature gradient needs an upsampled dC");
       // d feature[x] = sum_k filter[k] * dC[g(x, k)] : p' = x (side of dC), q' = k
       const int pv = b.var(ax.feature_dim, dc_on_a ? CE_M : CE_N);
       const int qv = b.var(ax.filter_dim, CE_K);

@@ -57,7 +57,8 @@ class SubsetTable {
           hi = std::max(hi, o.second);
           lo = std::min(lo, o.second);
         }
-        row.closed_dim = multiway ? hi : conv_output_dim(it->second, hi, lo);
+        if (multiway && it->second.stride != 1) throw PlanError("multi-way conv atom '" + a.name + "' cannot be strided");
+        row.closed_dim = multiway ? hi : conv_output_dim(it->second.mode, hi, lo, it->second.stride);
       } else {
         row.closed_dim = row.occ.front().second;
       }
