@@ -235,6 +235,56 @@ def time_cfg4_stack(ctx, flush, iters=2):
     return out
 
 
+def time_layer_once(ctx, flush, le, backward, iters=3):
+    """Median device ms of one layer (fwd, or fwd+bwd), L2 flushed, after a warm-up."""
+    import torch
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import Executor
+    plan = ce.optimal(le.expr, le.dims, "same", "training" if backward else "inference")
+    ex = Executor(ctx, plan, backward=backward)
+    xs = [ctx.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
+    dout = ctx.fill_random(plan.out_dims, 2000) if backward else None
+    out = torch.empty(plan.out_dims, device=xs[0].device)
+    ex.execute(xs, out)
+    if backward:
+        ex.backward(xs, dout)
+    ts = []
+    for _ in range(iters):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.torch_stream)
+        ex.execute(xs, out)
+        if backward:
+            ex.backward(xs, dout)
+        e1.record(ctx.torch_stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    fl = 2.0 * plan.flops_actual * (3.0 if backward else 1.0)
+    return {"ms": round(ms, 4), "tflops": round(fl / (ms * 1e-3) / 1e12, 2)}
+
+
+def time_cfg1_cfg5(ctx, flush):
+    """cfg1 (CP 3x3, batch 8, 64->64, 32x32, rank 16: forward, the CPU reference's case) and
+    cfg5 (CP/TK/TT/TR compression sweep at the cfg2 shape vs the dense conv through the same
+    executor, fwd+bwd)."""
+    import paper_2401_03384_b200 as ce
+    le1 = ce.expression(ce.LayerSpec("cp", [64], [64], 3, 3, 32, 32, 8, [16]))
+    cfg1 = {"workload": "cfg1 CP 3x3, B8, 64->64, 32x32, R16", "forward": time_layer_once(ctx, flush, le1, False, 10),
+            "fwd_bwd": time_layer_once(ctx, flush, le1, True, 10)}
+    sweep = {}
+    for kind, slots in (("cp", 1), ("tk", 2), ("tt", 3), ("tr", 4)):
+        for cr in (0.05, 0.1, 0.2, 0.3, 0.4, 0.5):
+            le = ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, 128, [1] * slots), cr)
+            sweep[f"{kind}_cr{cr}"] = time_layer_once(ctx, flush, le, True)
+    sweep["dense"] = time_layer_once(ctx, flush,
+                                     ce.expression(ce.LayerSpec("standard", [256], [256], 3, 3, 14, 14, 128, [])), True)
+    return cfg1, {"workload": "cfg5 compression sweep at the cfg2 shape (B128, 256->256, 14x14), fwd+bwd, ms and "
+                              "TF/s per layer; dense = bshw,tshw->bthw|hw on the same executor (no cuBLAS)",
+                  "layers": sweep}
+
+
 def time_stack(ctx, flush, kind, batch, cr, iters=2):
     """A ResNet-34 conv stack of `kind` layers: each distinct layer shape (stride-2 layers run
     stride-1 at output resolution) is timed (median of `iters` after a warm-up, L2 flushed)
@@ -286,7 +336,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-cfg3", action="store_true", help="skip the cfg3 stack extra key")
+    ap.add_argument("--no-cfg3", action="store_true", help="skip the extra keys (cfg1, cfg3 and cfg4 stacks, cfg5 sweep)")
     ap.add_argument("--profile-json", default=None, help="write per-kernel times here")
     args = ap.parse_args()
     if args.gpus > 1 and "RANK" not in os.environ:
@@ -524,13 +574,14 @@ def main():
                        for (n, k, t, fl, by) in kern], f, indent=1)
 
     # ---------------------------------------------------------------- cfg3 stack (largest single-GPU config)
-    cfg3 = cfg4 = None
+    cfg1 = cfg3 = cfg4 = cfg5 = None
     if rank == 0 and world == 1 and not args.no_cfg3:
         for l in layers:
             l.clear()
         torch.cuda.empty_cache()
         cfg3 = time_cfg3_stack(ctx, flush)
         cfg4 = time_cfg4_stack(ctx, flush)
+        cfg1, cfg5 = time_cfg1_cfg5(ctx, flush)
 
     # ---------------------------------------------------------------- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -560,8 +611,10 @@ def main():
             "gpu_launches": launches,
             "roofline": roof,
             "cpu_baseline": cpu,
+            "cfg1": cfg1,
             "cfg3_stack": cfg3,
             "cfg4_stack": cfg4,
+            "cfg5_sweep": cfg5,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -25,7 +25,7 @@ def ncu_page(rep, page):
                           check=True).stdout
 
 
-def main(src, dst):
+def main(src, dst, tag="r02"):
     os.makedirs(dst, exist_ok=True)
     traffic = {"source": "ncu --set full --clock-control none, one launch each (tools/round_artifacts.sh), B200",
                "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch; cold-cache replay", "kernels": {}}
@@ -36,8 +36,8 @@ def main(src, dst):
         short = cap.replace("full_", "")
         details = ncu_page(rep, "details")
         raw = ncu_page(rep, "raw")
-        open(os.path.join(dst, f"ncu_{short}_r01_details.csv"), "w").write(details)
-        open(os.path.join(dst, f"ncu_{short}_r01_raw.csv"), "w").write(raw)
+        open(os.path.join(dst, f"ncu_{short}_{tag}_details.csv"), "w").write(details)
+        open(os.path.join(dst, f"ncu_{short}_{tag}_raw.csv"), "w").write(raw)
         rows = list(csv.reader(io.StringIO(raw)))
         h, units, v = rows[0], rows[1], rows[2]
 
@@ -52,14 +52,14 @@ def main(src, dst):
         rd, wr = m("dram__bytes_read.sum"), m("dram__bytes_write.sum")
         ent = {"dram_bytes_per_launch": int(rd + wr), "dram_read": int(rd), "dram_write": int(wr),
                "duration_us": round(m("gpu__time_duration.sum"), 3), "kernel": v[h.index("Kernel Name")],
-               "capture": f"{cap}.ncu-rep (summarised in profiles/ncu_{short}_r01_*.csv)"}
+               "capture": f"{cap}.ncu-rep (summarised in profiles/ncu_{short}_{tag}_*.csv)"}
         for name, key in [("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor_pipe_active_pct")]:
             if name in h:
                 ent[key] = float(v[h.index(name)].replace(",", ""))
         traffic["kernels"][label] = ent
-    with open(os.path.join(dst, "ncu_traffic_r01.json"), "w") as f:
+    with open(os.path.join(dst, f"ncu_traffic_{tag}.json"), "w") as f:
         json.dump(traffic, f, indent=1)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(*sys.argv[1:4])
