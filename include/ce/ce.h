@@ -124,7 +124,8 @@ typedef struct ce_ctx ce_ctx;
 
 typedef enum {
   CE_MATH_AUTO = 0,      /* tcgen05 TF32 tensor cores where the step maps onto them, FP32 SIMT elsewhere */
-  CE_MATH_FP32_SIMT = 1  /* FP32 CUDA-core kernels only (accuracy anchor) */
+  CE_MATH_FP32_SIMT = 1, /* FP32 CUDA-core kernels only (accuracy anchor) */
+  CE_MATH_3XTF32 = 2     /* tensor cores with split operands: hi*hi + hi*lo + lo*hi, ~FP32 accuracy */
 } ce_math;
 
 typedef struct {

@@ -140,7 +140,7 @@ class Plan:
         """Kernel steps the device executor compiles this plan into (no GPU needed)."""
         buf = ctypes.create_string_buffer(1 << 20)
         wb = int(backward) | (CE_EXEC_RECOMPUTE if recompute else 0)
-        check(lib().ce_plan_describe_steps(self._h, wb, 0 if math in ("auto", "tf32") else 1, buf, len(buf)))
+        check(lib().ce_plan_describe_steps(self._h, wb, {"auto": 0, "tf32": 0, "3xtf32": 2}.get(math, 1), buf, len(buf)))
         return buf.value.decode()
 
     def nodes(self):

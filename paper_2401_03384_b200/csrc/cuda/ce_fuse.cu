@@ -320,3 +320,26 @@ cudaError_t ce_launch_dw2(const CeDw2Desc& d, const float* Y0, const float* Fa, 
   CE_DW2(7)
 #undef CE_DW2
 }
+
+// 3xTF32 operand split (CE_MATH_3XTF32): hi = x rounded to TF32 (cvt.rna), lo = x - hi (exact in
+// FP32); the step then runs as hi*hi + hi*lo + lo*hi on the tensor cores, ~FP32 accuracy.
+namespace {
+__global__ void __launch_bounds__(256) ce_split_tf32_kernel(const float* __restrict__ x, float* __restrict__ hi,
+                                                            float* __restrict__ lo, int64_t n) {
+  ce_pdl_enter();
+  for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n; i += static_cast<int64_t>(gridDim.x) * 256) {
+    const float v = x[i];
+    uint32_t t;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v));
+    const float h = __uint_as_float(t);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+}  // namespace
+
+cudaError_t ce_launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+  return ce_launch(ce_split_tf32_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, x, hi, lo, n);
+}

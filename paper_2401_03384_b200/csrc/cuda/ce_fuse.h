@@ -36,3 +36,6 @@ struct CeDw2Desc {
 bool ce_dw2_plan(const CeProblem& p1, const CeProblem& p2, bool write_mid, CeDw2Desc* out);
 cudaError_t ce_launch_dw2(const CeDw2Desc& d, const float* Y0, const float* Fa, const float* Fb, float* Y1, float* Y2,
                           cudaStream_t s);
+
+// 3xTF32 operand split: hi = TF32(x) (round to nearest), lo = x - hi, n elements.
+cudaError_t ce_launch_split_tf32(const float* x, float* hi, float* lo, int64_t n, cudaStream_t s);

@@ -398,7 +398,7 @@ __device__ __forceinline__ bool work_next(const TcParams& P, uint32_t ngroups, W
     item = it.w++;
     k0 = 0;
     k1 = P.k_iters;
-    atomic = false;
+    atomic = P.acc_out != 0;
     return true;
   }
   const uint32_t whole = P.sk_r > 0 ? P.sk_full : P.n_items;
@@ -408,7 +408,7 @@ __device__ __forceinline__ bool work_next(const TcParams& P, uint32_t ngroups, W
     const int split = static_cast<int>(tc_quo(item, P.dsplit));
     k0 = split * P.k_per;
     k1 = min(P.k_iters, k0 + P.k_per);
-    atomic = P.k_split > 1;
+    atomic = P.k_split > 1 || P.acc_out != 0;
     return true;
   }
   if (it.tail == ~0u) return false;
@@ -1234,13 +1234,14 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
     }();
     P.tl_s = 1;
     P.tl_flags = plan.tail_flags;
+    P.acc_out = plan.accum ? 1 : 0;
     // (long K loops only: with ~24 K stages the chunks' fixup costs what the shorter round
     // saves -- tt1.0's 24/27-stage convs were slower; tk1.0's 72-stage convs 74 -> 68 us)
     static const int tail_kmin = [] {
       const char* e = getenv("CE_TC_TAIL_KMIN");
       return e ? atoi(e) : 48;
     }();
-    if (tail_on && plan.tail_flags && !P.contig && P.k_split == 1 && csize == 1 && items > ngroups &&
+    if (tail_on && !plan.accum && plan.tail_flags && !P.contig && P.k_split == 1 && csize == 1 && items > ngroups &&
         items % ngroups != 0 && P.k_iters >= tail_kmin) {
       const int64_t r = items % ngroups;
       const int64_t S = std::min<int64_t>({4, ngroups / r, P.k_iters / 4});
@@ -1251,7 +1252,7 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
       }
     }
   }
-  if (P.k_split > 1) {
+  if (P.k_split > 1 && !plan.accum) {
     cudaError_t e = cudaMemsetAsync(C, 0, static_cast<size_t>(plan.out_span) * 4, s);
     if (e != cudaSuccess) return e;
   }

@@ -90,6 +90,7 @@ struct TcParams {
   int32_t c_tma;
   int32_t cdim_u[5], cdim_q[5];
   int32_t c_slab;     // rows of the outermost M unit per warp (its coordinate advances by q * c_slab)
+  int32_t acc_out;    // 1: every item adds into C (a 3xTF32 correction launch); no memset, no tail split
   TcUnit u[TC_MAX_UNITS];
   int32_t nunits;
   int32_t nm, mt[3];      // M-tile units, row order fastest first
@@ -162,6 +163,7 @@ struct TcPlan {
   const void* cached_c = nullptr;
   int64_t out_span = 0;       // elements of C to zero before a split-K launch
   uint32_t* tail_flags = nullptr;  // kTailFlags zeroed words owned by the executor (tail split)
+  int accum = 0;                   // add into C instead of storing (3xTF32 correction terms)
   const void* cached_a = nullptr;
   const void* cached_b = nullptr;
   const char* why = "";       // reason when not valid (diagnostics)

@@ -56,7 +56,7 @@ Executor::Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cf
   // (recompute first: the forward pass's intermediates are then read by no backward step,
   // so a fused forward pair need not store its intermediate)
   if (want_backward_ && cfg_.recompute) add_recompute();
-  if (fuse_on && cfg_.math == 0) {
+  if (fuse_on && tc_math()) {
     fuse_chains(fwd_);
     fuse_chains(bwd_);
   }
@@ -627,7 +627,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
     }
     return false;
   };
-  if (cfg_.math == 0 && !p.unary && !tiny_k) {
+  if (tc_math() && !p.unary && !tiny_k) {
     {
       // an N = 1 convolution (input gradient over every factor index) is memory-bound on the
       // tensor cores with the taps as shifted boxes (each dZ element read once per tap):
@@ -636,6 +636,83 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       for (int v = 0; v < p.nv; ++v)
         if (p.cls[v] == CE_N) n_ext *= static_cast<double>(p.ext[v]);
       if (n_ext == 1 && p.ng_a + p.ng_b > 0 && try_col2im()) return;
+    }
+    // Circular (wrap-around) gathers -- the reference's multi-way conv atoms, kernels.cpp:38-43,
+    // 298-315 -- cannot be TMA boxes: the operand is first copied with its wrapped axes
+    // unrolled (E[i] = A[(i + lo) mod X] over the whole index range the step reads), after
+    // which the step is an ordinary shifted-box convolution.  CE_TC_UNWRAP=0: SIMT instead.
+    static const bool unwrap_on = [] {
+      const char* e = std::getenv("CE_TC_UNWRAP");
+      return !(e && *e == '0');
+    }();
+    for (int side = 0; side < 2 && unwrap_on; ++side) {
+      const int ng = side ? p.ng_b : p.ng_a;
+      CeGather* gs = side ? p.gb : p.ga;
+      bool wraps = false;
+      for (int g = 0; g < ng; ++g) wraps |= gs[g].wrap != 0;
+      if (!wraps || p.nv + ng + 1 > CE_MAX_VARS) continue;
+      int64_t* ss = side ? p.sb : p.sa;
+      struct Ax { int64_t stride, ext; int var, g; };
+      std::vector<Ax> ax;
+      for (int v = 0; v < p.nv; ++v)
+        if (ss[v]) ax.push_back({ss[v], p.ext[v], v, -1});
+      std::vector<int64_t> lo(static_cast<std::size_t>(ng), 0), ext_g(static_cast<std::size_t>(ng), 0);
+      for (int g = 0; g < ng; ++g) {
+        const CeGather& G = gs[g];
+        const int64_t P = p.ext[G.pv] - 1, Q = p.ext[G.qv] - 1;
+        const int64_t l = G.c + std::min<int64_t>(0, G.sp * P) + std::min<int64_t>(0, G.sq * Q);
+        const int64_t h = G.c + std::max<int64_t>(0, G.sp * P) + std::max<int64_t>(0, G.sq * Q);
+        lo[static_cast<std::size_t>(g)] = G.wrap ? l : 0;
+        ext_g[static_cast<std::size_t>(g)] = G.wrap ? h - l + 1 : G.extent;
+        ax.push_back({G.stride, ext_g[static_cast<std::size_t>(g)], -1, g});
+      }
+      std::stable_sort(ax.begin(), ax.end(), [](const Ax& x, const Ax& y) { return x.stride < y.stride; });
+      CeProblem pk{};
+      pk.unary = 1;
+      const int dummy = pk.nv++;  // the copy's (extent-1) K var every gather pairs with
+      pk.ext[dummy] = 1;
+      pk.cls[dummy] = CE_K;
+      int64_t acc = 1;
+      for (std::size_t i = 0; i < ax.size(); ++i) {
+        if (i == 1) acc = (acc + 3) / 4 * 4;  // 16-B rows (TMA stride legality)
+        const int v = pk.nv++;
+        pk.ext[v] = ax[i].ext;
+        pk.cls[v] = CE_M;
+        pk.sc[v] = acc;
+        if (ax[i].var >= 0) {
+          pk.sa[v] = ax[i].stride;
+          ss[ax[i].var] = acc;
+        } else {
+          CeGather& G = gs[ax[i].g];
+          CeGather E{};
+          E.pv = v;
+          E.qv = dummy;
+          E.sp = 1;
+          E.sq = 0;
+          E.c = lo[static_cast<std::size_t>(ax[i].g)];
+          E.extent = G.extent;
+          E.stride = G.stride;
+          E.wrap = G.wrap;
+          pk.ga[pk.ng_a++] = E;
+          if (G.wrap) {
+            G.c -= E.c;
+            G.extent = ax[i].ext;
+            G.wrap = 0;
+          }
+          G.stride = acc;
+        }
+        acc *= ax[i].ext;
+      }
+      Step es;
+      es.kind = Step::kDirect;
+      es.desc = simt_desc(pk);
+      es.a = side ? b : a;
+      es.c = {BufRef::kWork, alloc(acc)};
+      es.node = node;
+      es.label = label + (side ? ":unwrapB" : ":unwrapA");
+      es.bytes = 4.0 * static_cast<double>(acc) + 4.0 * operand_elems(pk, 0);
+      (side ? b : a) = es.c;
+      list.push_back(es);
     }
     bool ok = ce_tc_plan(p, &st.tc);
     if (!ok) {
@@ -912,6 +989,47 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       st.desc = simt_desc(p);
       st.flops = pending_flops_;
       st.bytes = problem_bytes(p);
+      if (cfg_.math == 2) {
+        // 3xTF32: both operands split into TF32-exact hi and FP32 remainder lo (same layouts), then
+        // C = hi*hi + hi*lo + lo*hi -- the dropped lo*lo term is ~2^-22 relative (FP32-level)
+        auto span = [&](bool side_b) {
+          const int64_t* ss = side_b ? p.sb : p.sa;
+          const CeGather* g = side_b ? p.gb : p.ga;
+          const int ng = side_b ? p.ng_b : p.ng_a;
+          int64_t n = 1;
+          for (int v = 0; v < p.nv; ++v)
+            if (ss[v]) n += (p.ext[v] - 1) * ss[v];
+          for (int i = 0; i < ng; ++i) n += (g[i].extent - 1) * g[i].stride;
+          return n;
+        };
+        BufRef hi[2], lo[2];
+        for (int side = 0; side < 2; ++side) {
+          const int64_t n = span(side == 1);
+          Step sp;
+          sp.kind = Step::kSplit;
+          sp.a = side ? b : a;
+          sp.c = hi[side] = {BufRef::kWork, alloc(n)};
+          sp.c2 = lo[side] = {BufRef::kWork, alloc(n)};
+          sp.zero_elems = n;
+          sp.node = node;
+          sp.label = label + (side ? ":splitB" : ":splitA");
+          sp.bytes = 12.0 * static_cast<double>(n);
+          list.push_back(sp);
+        }
+        const BufRef pa[3] = {hi[0], hi[0], lo[0]}, pb[3] = {hi[1], lo[1], hi[1]};
+        for (int t = 0; t < 3; ++t) {
+          Step s3 = st;
+          s3.a = pa[t];
+          s3.b = pb[t];
+          s3.tc.accum = t > 0 ? 1 : 0;
+          if (t > 0) {
+            s3.flops = 0;  // (the algorithmic FLOPs are credited once)
+            s3.label = label + (t == 1 ? ":3xtf32-hl" : ":3xtf32-lh");
+          }
+          list.push_back(s3);
+        }
+        return;
+      }
       list.push_back(st);
       return;
     }
@@ -1194,7 +1312,7 @@ float* Executor::resolve(const BufRef& r) const {
 }
 
 std::string Executor::describe() const {
-  static const char* kinds[] = {"direct", "tiled", "tc", "zero", "reduce", "permute", "dw2"};
+  static const char* kinds[] = {"direct", "tiled", "tc", "zero", "reduce", "permute", "dw2", "split"};
   std::string out;
   char line[512];
   for (const auto* list : {&fwd_, &bwd_})
@@ -1378,6 +1496,7 @@ void Executor::launch_step(Step& st, cudaStream_t s) {
       case Step::kReduce: e = ce_launch_reduce(exact(st), A, B, C, st.zero_elems, s); break;
       case Step::kPermute: e = ce_launch_permute(st.desc.p, A, C, s); break;
       case Step::kDw2: e = ce_launch_dw2(st.dw2, A, B, resolve(st.b2), C, resolve(st.c2), s); break;
+      case Step::kSplit: e = ce_launch_split_tf32(A, C, resolve(st.c2), st.zero_elems, s); break;
     }
     cuda_check(e, st.label.c_str());
     if (profiling_) cuda_check(cudaEventRecordWithFlags(st.ev1, s, cudaEventRecordExternal), "cudaEventRecord");

@@ -25,7 +25,7 @@ struct BufRef {
 };
 
 struct Step {
-  enum Kind { kDirect, kTiled, kTc, kZero, kReduce, kPermute, kDw2 } kind = kDirect;
+  enum Kind { kDirect, kTiled, kTc, kZero, kReduce, kPermute, kDw2, kSplit } kind = kDirect;
   CeSimtDesc desc{};
   int a_kfast = 0, b_kfast = 0;
   TcPlan tc{};
@@ -46,7 +46,7 @@ struct Step {
 };
 
 struct ExecConfig {
-  int math = 0;  // 0 auto (tensor cores where mappable), 1 FP32 SIMT only
+  int math = 0;  // 0 auto (TF32 tensor cores where mappable), 1 FP32 SIMT only, 2 3xTF32 tensor cores
   // gradient checkpointing: the forward pass keeps no
   // intermediates; the backward pass recomputes them first (one extra forward's work)
   bool recompute = false;
@@ -97,6 +97,7 @@ class Executor {
   void assign_offsets();
   void fuse_chains(std::vector<Step>& list);
   void add_recompute();
+  bool tc_math() const { return cfg_.math == 0 || cfg_.math == 2; }
   bool overlap(const BufRef& x, const BufRef& y) const;
   float* resolve(const BufRef& r) const;
 

@@ -14,7 +14,7 @@ from . import _lib
 from ._lib import check, lib
 from .api import Plan, _dims_arg
 
-MATH = {"auto": 0, "tf32": 0, "fp32": 1, "simt": 1}
+MATH = {"auto": 0, "tf32": 0, "fp32": 1, "simt": 1, "3xtf32": 2}
 
 
 class Context:
