@@ -434,6 +434,41 @@ bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
   plan->bn = P.n_mma <= 64 ? 64 : P.n_mma <= 128 ? 128 : 256;
   if (b_mn == 1 && P.n_cols % 32) return fail("MN-major B tile must be a multiple of 32");
 
+  // Store-completing traversal: when a grid unit continues C's unit-stride run past the tile
+  // (RTR's dZ: the N tile holds r3, C's 10-float inner run, and t1 -- stride 10 -- is a grid
+  // unit), consecutive work items should cover that unit's values so the pieces of each
+  // 32-B sector are written close together in time (one CTA, back to back, in contiguous
+  // mode) instead of by tiles far apart, which left partial sectors for L2 to write back.  The
+  // unit becomes the fastest M digit with a box of 1 (no change to the tile's rows).
+  // CE_TC_GFIRST=0 off.
+  {
+    static const bool gfirst_on = [] {
+      const char* e = std::getenv("CE_TC_GFIRST");
+      return !(e && *e == '0');
+    }();
+    int64_t run = 0;  // C-contiguous elements covered by the tile unit holding C's unit-stride var
+    for (int pass = 0; pass < 2 && gfirst_on && run == 0; ++pass)
+      for (int i = 0; i < (pass ? P.nn : P.nm); ++i) {
+        const TcUnit& u = U[static_cast<std::size_t>(pass ? P.nt[i] : P.mt[i])];
+        if (u.nv < 1 || u.sc[0] != 1) continue;
+        run = u.vext[0];
+        for (int k = 1; k < u.nv && u.sc[k] == run; ++k) run *= u.vext[k];
+        if (u.box < u.ext) run = 0;  // the tile cuts the run itself
+      }
+    if (run > 0 && run < 8 * 4 && P.nm < 3) {  // (runs of >= 32 floats already fill whole sectors)
+      for (std::size_t i = 0; i < U.size(); ++i) {
+        TcUnit& g = U[i];
+        if (g.src != TC_SRC_GRID || g.nv < 1 || g.sc[0] != run || g.ext < 2) continue;
+        for (int j = P.nm; j > 0; --j) P.mt[j] = P.mt[j - 1];
+        P.mt[0] = static_cast<int32_t>(i);
+        ++P.nm;
+        g.src = TC_SRC_MTILE;
+        g.box = 1;
+        break;
+      }
+    }
+  }
+
   // grid / K-loop units
   for (std::size_t i = 0; i < U.size(); ++i) {
     if (U[i].src == TC_SRC_GRID) P.gu[P.ng++] = static_cast<int32_t>(i);
