@@ -479,6 +479,20 @@ std::vector<int64_t> pack_signature(const CeProblem& pk) {
   return sig;
 }
 
+// Family (c) tile / block permute kernels for large tensors; below CE_PERM_SMALL elements
+// (default 2^20) the one-thread-per-output stream kernel (coalesced writes, gathered reads
+// served by L2) finishes sooner than the tiled kernels' fixed cost.
+bool use_permute(const CeProblem& pk) {
+  static const double small = [] {
+    const char* e = std::getenv("CE_PERM_SMALL");
+    return e ? std::atof(e) : 1048576.0;
+  }();
+  double n = 1;
+  for (int v = 0; v < pk.nv; ++v)
+    if (pk.cls[v] != CE_K) n *= static_cast<double>(pk.ext[v]);
+  return n >= small && ce_permute_supported(pk);
+}
+
 int inner_var(const CeProblem& p, bool side_b) {
   const int64_t* s = side_b ? p.sb : p.sa;
   for (int v = 0; v < p.nv; ++v)
@@ -795,7 +809,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
             continue;
           }
           Step ps;
-          ps.kind = ce_permute_supported(best_pks[side]) ? Step::kPermute : Step::kDirect;
+          ps.kind = use_permute(best_pks[side]) ? Step::kPermute : Step::kDirect;
           ps.desc = simt_desc(best_pks[side]);
           ps.a = src;
           ps.c = {BufRef::kWork, alloc(best_spans[side])};
@@ -865,7 +879,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
           list.push_back(es);
           if (pack_partner) {
             Step ps2;
-            ps2.kind = ce_permute_supported(ppk) ? Step::kPermute : Step::kDirect;
+            ps2.kind = use_permute(ppk) ? Step::kPermute : Step::kDirect;
             ps2.desc = simt_desc(ppk);
             ps2.a = side ? a : b;
             ps2.c = {BufRef::kWork, alloc(pspan)};
@@ -903,7 +917,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
         TcPlan t;
         if (ce_tc_plan(q, &t) && !t.params.ob.mn_major) {
           Step ps;
-          ps.kind = ce_permute_supported(pk) ? Step::kPermute : Step::kDirect;
+          ps.kind = use_permute(pk) ? Step::kPermute : Step::kDirect;
           ps.desc = simt_desc(pk);
           ps.a = b;
           ps.c = {BufRef::kWork, alloc(span)};
@@ -965,7 +979,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
           }
           if (!reused) {
             Step ps;
-            ps.kind = ce_permute_supported(pk) ? Step::kPermute : Step::kDirect;
+            ps.kind = use_permute(pk) ? Step::kPermute : Step::kDirect;
             ps.desc = simt_desc(pk);
             ps.a = src;
             ps.c = {BufRef::kWork, alloc(span)};
@@ -978,6 +992,79 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
           }
           p = q;
           st.tc = t;
+        }
+      }
+    }
+    // Split-K steps whose output layout admits neither vectorised nor TMA reductions (a filter
+    // gradient whose unit-stride axis is a tap, e.g. dW[r1][r2][h][w] with the taps as grid
+    // units) would add every partial tile with scalar atomics.  When the output is small they
+    // reduce instead into a staging buffer laid out [M vars][N vars][rest] (M innermost, in
+    // A's order, so the tile rows chain and bulk reduce-adds take them) that one permute then
+    // writes in the caller's layout.  CE_TC_STAGE_SPLITK=0 off.
+    static const bool stage_on = [] {
+      const char* e = std::getenv("CE_TC_STAGE_SPLITK");
+      return !(e && *e == '0');
+    }();
+    if (ok && stage_on && cfg_.math == 0 && st.tc.params.k_split > 1 && st.tc.params.c_tma == 0) {
+      double out_elems = 1;
+      for (int v = 0; v < p.nv; ++v)
+        if (p.cls[v] != CE_K) out_elems *= static_cast<double>(p.ext[v]);
+      if (out_elems <= 16.0 * 1048576.0) {
+        CeProblem q = p;
+        std::vector<int> vs;
+        for (int cls : {CE_M, CE_N, CE_Z}) {
+          std::vector<int> part;
+          for (int v = 0; v < p.nv; ++v)
+            if (p.cls[v] == cls && p.ext[v] > 1) part.push_back(v);
+          // (vars plain in the operand first, by its strides: they form the tile units; vars
+          // only reached through a gather -- the filter taps -- outermost)
+          const int64_t* op = cls == CE_N ? p.sb : p.sa;
+          auto key = [&](int v) { return op[v] ? op[v] : INT64_MAX; };
+          std::stable_sort(part.begin(), part.end(), [&](int x, int y) { return key(x) < key(y); });
+          vs.insert(vs.end(), part.begin(), part.end());
+        }
+        int64_t acc = 1;
+        for (std::size_t i = 0; i < vs.size(); ++i) {
+          if (i == 1) acc = (acc + 3) / 4 * 4;
+          q.sc[vs[i]] = acc;
+          acc *= p.ext[vs[i]];
+        }
+        for (int v = 0; v < q.nv; ++v)
+          if (q.cls[v] != CE_K && q.ext[v] == 1) q.sc[v] = 0;
+        TcPlan t;
+        if (ce_tc_plan(q, &t) && t.params.c_tma != 0 && t.params.k_split > 1) {
+          const BufRef tmp{BufRef::kWork, alloc(acc)};
+          Step ts = st;
+          ts.kind = Step::kTc;
+          ts.tc = t;
+          ts.a = a;
+          ts.b = b;
+          ts.c = tmp;
+          ts.desc = simt_desc(q);
+          ts.flops = pending_flops_;
+          ts.bytes = problem_bytes(q);
+          list.push_back(ts);
+          // staging -> the caller's layout (a unary permute over the output vars)
+          CeProblem pk{};
+          pk.unary = 1;
+          for (int v = 0; v < p.nv; ++v) {
+            if (p.cls[v] == CE_K || p.ext[v] == 1) continue;
+            const int u = pk.nv++;
+            pk.ext[u] = p.ext[v];
+            pk.cls[u] = CE_M;
+            pk.sa[u] = q.sc[v];
+            pk.sc[u] = p.sc[v];
+          }
+          Step ps;
+          ps.kind = use_permute(pk) ? Step::kPermute : Step::kDirect;
+          ps.desc = simt_desc(pk);
+          ps.a = tmp;
+          ps.c = c;
+          ps.node = node;
+          ps.label = label + ":unstage";
+          ps.bytes = 8.0 * out_elems;
+          list.push_back(ps);
+          return;
         }
       }
     }
@@ -1042,7 +1129,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
   st.bytes = problem_bytes(p);
   const CeSimtDesc& d = st.desc;
   const int64_t outs = d.Z * d.M * d.N;
-  if (p.unary && ce_permute_supported(p)) {
+  if (p.unary && use_permute(p)) {
     st.kind = Step::kPermute;
   } else if (d.K >= 1024 && outs < 148 * 256 && (p.unary || d.K <= 32 || d.M < 16 || d.N < 16 || outs < 4096)) {
     st.kind = Step::kReduce;
