@@ -410,6 +410,19 @@ def main():
         one_step()
     torch.cuda.synchronize()
 
+    # One GPU: the whole step (4 layers, forward + backward) is captured once as a CUDA graph
+    # and replayed -- how a training loop would run it; the executors launch their steps
+    # straight into the capture.  (N > 1 keeps eager launches: the NCCL all-reduces.)
+    # CE_BENCH_STEP_GRAPH=0: eager.
+    step_graph = None
+    step_launches = 0
+    if world == 1 and os.environ.get("CE_BENCH_STEP_GRAPH", "1") != "0":
+        step_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(step_graph, stream=stream):
+            step_launches = one_step()
+        step_graph.replay()
+        torch.cuda.synchronize()
+
     times = []
     launches = 0
     with ClockSampler(local) as clk:
@@ -420,7 +433,11 @@ def main():
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            launches = one_step()
+            if step_graph is not None:
+                step_graph.replay()
+                launches = step_launches
+            else:
+                launches = one_step()
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
@@ -602,6 +619,8 @@ def main():
                        "global_batch": PER_GPU_BATCH * world, "per_gpu_batch": PER_GPU_BATCH,
                        "parallelism": f"batch-sharded x{world}, factor-grad NCCL all-reduce" if world > 1 else "1 GPU",
                        "l2": "flushed (256 MiB write) between timed steps",
+                       "launch": "whole step replayed as one CUDA graph" if step_graph is not None
+                                 else "eager (per-executor CUDA graphs)",
                        "flops_per_step_per_gpu": step_flops},
             "layer_fwd_bwd_ms": lat,
             "e2e": {"value": round(e2e_value, 3), "unit": "TFLOP/s", "ms_per_step": round(e2e_ms, 4),

@@ -247,7 +247,11 @@ void Executor::launch_pass(std::vector<Step>& steps, const std::vector<char>* ne
     cudaGraphDestroy(graph);
     return;
   }
-  if (!use_graphs_) {
+  // inside a caller's stream capture (a whole training step captured as one CUDA graph) the
+  // steps are launched directly, so they become nodes of the caller's graph
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(s, &cap), "cudaStreamIsCapturing");
+  if (!use_graphs_ || cap != cudaStreamCaptureStatusNone) {
     run(steps, need, s);
     return;
   }
