@@ -329,6 +329,46 @@ def time_stack(ctx, flush, kind, batch, cr, iters=2):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def time_step_math(local, flush, math, iters=3):
+    """The cfg2 step (4 layers, fwd+bwd, batch 128) in another math mode of the same executor:
+    "fp32" = FP32 SIMT kernels (the accuracy anchor), "3xtf32" = split operands on the tensor
+    cores (~FP32 accuracy).  Eager, L2 flushed, median of `iters` after one warm-up step."""
+    import torch
+    import paper_2401_03384_b200 as ce
+    from paper_2401_03384_b200.device import Context, Executor
+    ctx = Context(local, math)
+    torch.cuda.set_stream(ctx.torch_stream)
+    ls, flops = [], 0.0
+    for kind, cr in LAYERS:
+        le = layer_expr(kind, cr, PER_GPU_BATCH)
+        plan = ce.optimal(le.expr, le.dims, "same", "training")
+        xs = [ctx.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
+        ls.append((Executor(ctx, plan, backward=True), xs, ctx.fill_random(plan.out_dims, 2000),
+                   torch.empty(plan.out_dims, device=xs[0].device)))
+        flops += 6.0 * plan.flops_actual
+
+    def step():
+        for ex, xs, dout, out in ls:
+            ex.execute(xs, out)
+            ex.backward(xs, dout)
+
+    step()
+    ts = []
+    for _ in range(iters):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.torch_stream)
+        step()
+        e1.record(ctx.torch_stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    del ls
+    torch.cuda.synchronize()
+    return {"ms_per_step": round(ms, 4), "tflops": round(flops / (ms * 1e-3) / 1e12, 2), "launch": "eager"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -592,10 +632,17 @@ def main():
 
     # ---------------------------------------------------------------- cfg3 stack (largest single-GPU config)
     cfg1 = cfg3 = cfg4 = cfg5 = None
+    precision = None
     if rank == 0 and world == 1 and not args.no_cfg3:
         for l in layers:
             l.clear()
         torch.cuda.empty_cache()
+        # the same step in the FP32 SIMT anchor and 3xTF32 modes, beside the TF32 headline
+        precision = {"tf32": {"ms_per_step": round(ms, 4), "tflops": round(value, 2),
+                              "launch": "graph" if step_graph is not None else "eager"},
+                     "3xtf32": time_step_math(local, flush, "3xtf32"),
+                     "fp32_simt": time_step_math(local, flush, "fp32")}
+        torch.cuda.set_stream(stream)
         cfg3 = time_cfg3_stack(ctx, flush)
         cfg4 = time_cfg4_stack(ctx, flush)
         cfg1, cfg5 = time_cfg1_cfg5(ctx, flush)
@@ -630,6 +677,7 @@ def main():
             "gpu_launches": launches,
             "roofline": roof,
             "cpu_baseline": cpu,
+            "precision_modes": precision,
             "cfg1": cfg1,
             "cfg3_stack": cfg3,
             "cfg4_stack": cfg4,

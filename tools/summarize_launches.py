@@ -21,7 +21,10 @@ def main(path):
         d[r[12]] = float(r[14].replace(",", ""))
     order = sorted(ids)
     flush = [i for i in order if "elementwise" in ids[i]["name"] or "at::" in ids[i]["name"]]
-    lo, hi = flush[0] + 1, flush[1] - 1
+    # the first pair of flush fills with a step between them (other torch fills, e.g. the
+    # warm-up's output buffers, sit back to back)
+    k = next(j for j in range(len(flush) - 1) if flush[j + 1] - flush[j] > 20)
+    lo, hi = flush[k] + 1, flush[k + 1] - 1
     step = [i for i in order if lo <= i <= hi]
     tot = sum(ids[i]["gpu__time_duration.sum"] for i in step) / 1e3
     longest = max(step, key=lambda i: ids[i]["gpu__time_duration.sum"])
