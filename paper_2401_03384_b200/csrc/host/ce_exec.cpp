@@ -750,11 +750,16 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       {
         // both operands repacked with one K order (contiguous, so the K vars merge)
         std::vector<int> order = shared_k_order(p, a_ok ? false : true);
+        const std::vector<int> all = order;
         if (!a_ok && !b_ok) {
           std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p.ext[x] > p.ext[y]; });
           if (!order.empty()) order.resize(1);
         }
         attempts.push_back({true, true, order});
+        // or every shared K var innermost in both (one merged K unit: RTR 64->64's X * W over
+        // s1 s2 s3 = 64 instead of a 4-wide unit padded to 32; scored after, so ties keep the
+        // single-var layout)
+        if (!a_ok && !b_ok && all.size() > 1) attempts.push_back({true, true, all});
       }
       // every layout that the tensor cores accept is scored (stages at ~0.25 us per SM plus
       // pack traffic at ~3 TB/s; a pack the forward pass already made is free): the first
