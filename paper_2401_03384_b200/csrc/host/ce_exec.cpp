@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <string>
 #include <stdexcept>
 
@@ -49,6 +50,11 @@ Executor::Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cf
   }
   build_forward();
   if (want_backward_) build_backward();
+  if (hoist_packs()) {
+    reset_build();
+    build_forward();
+    if (want_backward_) build_backward();
+  }
   static const bool fuse_on = [] {  // CE_FUSE=0: no node fusion
     const char* e = std::getenv("CE_FUSE");
     return !(e && *e == '0');
@@ -71,6 +77,84 @@ Executor::Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cf
   }
   if (const char* e = std::getenv("CE_CONCURRENT"); e && *e == '0') concurrent_ = false;
   if (const char* dbg = std::getenv("CE_DEBUG"); dbg && *dbg == '1') std::fputs(describe().c_str(), stderr);
+}
+
+void Executor::reset_build() {
+  fwd_.clear();
+  bwd_.clear();
+  packs_.clear();
+  pack_log_.clear();
+  buf_bytes_.clear();
+  buf_owner_.clear();
+  id_view_.resize(static_cast<std::size_t>(n_));
+  id_ref_.resize(static_cast<std::size_t>(n_));
+  for (int s = 0; s < 2; ++s) {
+    red_view_[s].clear();
+    red_ref_[s].clear();
+  }
+  pending_flops_ = 0;
+}
+
+// Layout hoisting (CE_HOIST: 0 off, 1 (default) node results, 2 also gradient buffers:
+// measured worse on RTR 64->128, 44 -> 52 ms, the gradient producers' stores fragment).
+// A repack of a buffer our own step produced costs a full HBM round trip of it (RTR's 5-GB
+// intermediates: 2.5-3.2 ms each); writing the buffer in the packed layout in the first
+// place costs only the producer's epilogue pattern.  The first pack of each such buffer
+// names its layout: each atom's output stride is read off the pack's axis that holds it
+// (atoms merged into one pack axis keep their relative strides).  Returns whether any
+// layout changed (the caller rebuilds the steps).
+bool Executor::hoist_packs() {
+  static const int mode = [] {
+    const char* e = std::getenv("CE_HOIST");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (mode <= 0 || !tc_math()) return false;
+  bool changed = false;
+  std::set<std::pair<int, bool>> seen;
+  for (const PackLog& r : pack_log_) {
+    if (r.src.kind != BufRef::kWork || r.pk.ng_a != 0) continue;
+    const auto it = buf_owner_.find(r.src.index);
+    if (it == buf_owner_.end()) continue;
+    const int id = it->second.first;
+    const bool grad = it->second.second;
+    if (grad ? mode < 2 : mode < 1) continue;
+    std::map<int, View>& lay = grad ? grad_layout_ : res_layout_;
+    // only the buffer's first pack (its first consumer's layout) is a candidate
+    if (!seen.insert({id, grad}).second) continue;
+    const View& v = id_view_[static_cast<std::size_t>(id)];
+    double elems = 1, pk_elems = 1;
+    for (int64_t d : v.dims) elems *= static_cast<double>(d);
+    for (int k = 0; k < r.pk.nv; ++k) pk_elems *= static_cast<double>(r.pk.ext[k]);
+    if (elems != pk_elems) continue;  // not a pure permute of the whole buffer
+    // only buffers whose round trip matters (>= 64 MB): small packs are cheap, and their
+    // consumers' tile plans are tuned to the padded result order
+    if (elems < 16.0 * 1024 * 1024) continue;
+    View nv = v;
+    bool ok = true;
+    for (std::size_t i = 0; i < v.dims.size() && ok; ++i) {
+      if (v.dims[i] == 1) continue;
+      const int64_t st = v.strides[i];
+      ok = false;
+      for (int k = 0; k < r.pk.nv; ++k) {
+        const int64_t s0 = r.pk.sa[k];
+        if (s0 <= 0 || st < s0 || st % s0 != 0 || (st / s0) * v.dims[i] > r.pk.ext[k]) continue;
+        nv.strides[i] = r.pk.sc[k] * (st / s0);
+        ok = true;
+        break;
+      }
+    }
+    if (!ok) continue;
+    // the producer's epilogue writes runs along the new unit-stride atom: under 8 floats
+    // (32-B sectors) its stores fragment (RTR's N0 with s1 = 4 innermost: node0 2.5 ->
+    // 5.7 ms and dW4 0.9 -> 7.1 ms, measured), so such layouts are not hoisted
+    int64_t inner = 0;
+    for (std::size_t i = 0; i < nv.dims.size(); ++i)
+      if (nv.dims[i] > 1 && nv.strides[i] == 1) inner = nv.dims[i];
+    if (inner < 8) continue;
+    lay[id] = nv;
+    changed = true;
+  }
+  return changed;
 }
 
 Executor::~Executor() {
@@ -733,7 +817,14 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       list.push_back(es);
     }
     bool ok = ce_tc_plan(p, &st.tc);
-    if (!ok) {
+    // A legal plan whose K units are fragmented (both operands K-major but their K vars
+    // chain differently, e.g. a hoisted [.. r0 s1] intermediate against a factor stored
+    // [r0 r1 t1 s1]: 10 K units of 4 padded to 32) is scored against the repacks below.
+    double k_elems = 1;
+    for (int v = 0; v < p.nv; ++v)
+      if (p.cls[v] == CE_K) k_elems *= static_cast<double>(p.ext[v]);
+    const bool k_waste = ok && static_cast<double>(st.tc.params.k_iters) * 32.0 > 2.0 * k_elems + 64.0;
+    if (!ok || k_waste) {
       // tf32 tensor cores need both operands K-major over the same K unit: repack
       // the operand(s) whose unit-stride axis is not a shared K var, mirroring the
       // partner's K order so contiguous K vars still merge into one unit.
@@ -745,8 +836,8 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
         std::vector<int> order;
       };
       std::vector<Attempt> attempts;
-      if (a_ok && !(b_ok && ib == ia)) attempts.push_back({false, true, shared_k_order(p, false)});
-      if (b_ok && !a_ok) attempts.push_back({true, false, shared_k_order(p, true)});
+      if (a_ok && (k_waste || !(b_ok && ib == ia))) attempts.push_back({false, true, shared_k_order(p, false)});
+      if (b_ok && (k_waste || !a_ok)) attempts.push_back({true, false, shared_k_order(p, true)});
       {
         // both operands repacked with one K order (contiguous, so the K vars merge)
         std::vector<int> order = shared_k_order(p, a_ok ? false : true);
@@ -777,6 +868,10 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       };
       double best_us = 1e300;
       int best = -1;
+      if (k_waste) {  // the legal plan as it is
+        const TcParams& P = st.tc.params;
+        best_us = static_cast<double>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_iters * 0.25 / 148.0;
+      }
       CeProblem best_q{}, best_pks[2];
       int64_t best_spans[2] = {0, 0};
       TcPlan best_t;
@@ -827,6 +922,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
           ps.bytes = 8.0 * operand_elems(best_pks[side], 0);
           (side ? b : a) = ps.c;
           if (&list == &fwd_) packs_.push_back({src, best_pks[side], ps.c});
+          pack_log_.push_back({src, best_pks[side], &list == &fwd_});
           list.push_back(ps);
         }
         p = best_q;
@@ -896,6 +992,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
             ps2.label = label + (side ? ":packA" : ":packB");
             ps2.bytes = 8.0 * operand_elems(ppk, 0);
             (side ? a : b) = ps2.c;
+            pack_log_.push_back({ps2.a, ppk, &list == &fwd_});
             list.push_back(ps2);
           }
           p = q;
@@ -934,6 +1031,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
           ps.label = label + ":packB";
           ps.bytes = 8.0 * operand_elems(pk, 0);
           b = ps.c;
+          pack_log_.push_back({ps.a, pk, &list == &fwd_});
           list.push_back(ps);
           p = q;
           st.tc = t;
@@ -997,6 +1095,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
             ps.bytes = 8.0 * operand_elems(pk, 0);
             (side_b ? b : a) = ps.c;
             if (&list == &fwd_) packs_.push_back({src, pk, ps.c});
+            pack_log_.push_back({src, pk, &list == &fwd_});
             list.push_back(ps);
           }
           p = q;
@@ -1289,8 +1388,11 @@ void Executor::build_forward() {
       red_ref_[s][j] = ref;
     }
     const bool last = j + 1 == plan_.nodes.size();
-    View res = last ? out_view : padded_view(op.result, op.result_dims, 4);
+    const int rid = n_ + static_cast<int>(j);
+    View res = last ? out_view
+                    : res_layout_.count(rid) ? res_layout_.at(rid) : padded_view(op.result, op.result_dims, 4);
     BufRef res_ref = last ? BufRef{BufRef::kOutput, 0} : BufRef{BufRef::kWork, alloc(view_span(res))};
+    if (!last) buf_owner_[res_ref.index] = {rid, false};
     pending_flops_ = 2.0 * static_cast<double>(flops_actual(op));
     add_problem(fwd_, lower_pairwise(op, red_view_[0][j], red_view_[1][j], res, res, Adjoint::Forward),
                 red_ref_[0][j], red_ref_[1][j], res_ref, static_cast<int>(j), "node" + std::to_string(j));
@@ -1318,8 +1420,11 @@ void Executor::build_backward() {
       gview[id] = dout_view;
       gref[id] = {BufRef::kDOut, 0};
     } else {
-      gview[id] = id_view_[id];  // same padded layout as the forward result
+      // the forward result's layout unless a hoisted gradient layout was chosen
+      const int gid = static_cast<int>(id);
+      gview[id] = grad_layout_.count(gid) ? grad_layout_.at(gid) : id_view_[id];
       gref[id] = {BufRef::kWork, alloc(view_span(gview[id]))};
+      buf_owner_[gref[id].index] = {gid, true};
     }
   }
   for (std::size_t jj = plan_.nodes.size(); jj-- > 0;) {

@@ -8,7 +8,9 @@
 
 #include <cuda_runtime.h>
 
+#include <map>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../cuda/ce_device.h"
@@ -133,6 +135,19 @@ class Executor {
     BufRef dst;
   };
   std::vector<PackRecord> packs_;  // forward repacks, reusable by later steps
+  // Layout hoisting: a workspace buffer one of our own steps writes (a node result or its
+  // gradient) that a consumer repacks is instead written in the packed layout by its
+  // producer (operand id -> view; the other readers take the new strides), see hoist_packs
+  struct PackLog {
+    BufRef src;
+    CeProblem pk;
+    bool fwd;
+  };
+  std::vector<PackLog> pack_log_;
+  std::map<int, View> res_layout_, grad_layout_;
+  std::map<int64_t, std::pair<int, bool>> buf_owner_;  // workspace buffer -> (operand id, gradient?)
+  void reset_build();
+  bool hoist_packs();
   // CUDA-graph replay of a pass: valid while the bound pointers are unchanged
   struct GraphCache {
     std::vector<const void*> key;

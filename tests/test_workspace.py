@@ -63,3 +63,31 @@ def test_recompute_steps():
     assert any("store_mid=1" in l for l in fwd_keep) and all("store_mid=1" not in l for l in fwd_rec)
     recomputed = [l for l in rec if l.startswith("bwd recompute:")]
     assert len(recomputed) == len(fwd_rec) - 1  # every forward step but the root node
+
+
+def _steps(kind, tf, sf, k, hp, batch, cr):
+    slots = {"cp": 1, "tk": 2, "tt": 3, "tr": 4, "rtr": 4}[kind]
+    le = ce.expression(ce.LayerSpec(kind, tf, sf, k, k, hp, hp, batch, [1] * slots), cr)
+    plan = ce.optimal(le.expr, le.dims, "same", "training")
+    return plan.describe_steps(True, "auto")
+
+
+def test_layout_hoisting_removes_intermediate_repacks():
+    """cfg3 64->128 @28 (B=256): node1's 5-GB result N1 is written by its producer in the
+    layout its consumer (node3) would repack it into, so node3 and the filter gradient that
+    re-read it run without a repack; N0's packed layout (a 4-wide innermost axis) is not
+    hoisted (its producer's stores would fragment)."""
+    steps = _steps("rtr", [4, 4, 8], [4, 4, 4], 3, 28, 256, 0.1)
+    assert "node3:packA" not in steps and "grad:7:packA" not in steps, steps
+    assert "node1:packA" in steps
+    # below the 64-MB threshold nothing is hoisted (small packs are cheap)
+    assert "node3:packA" in _steps("rtr", [4, 4, 8], [4, 4, 4], 3, 28, 1, 0.1)
+
+
+def test_both_operand_repack_merges_shared_k():
+    """RTR 64->64 @56: X (channels-first) against the contracted kernel [t1 s1 t2 s2 t3 s3 h w]
+    -- neither operand K-major -- is repacked with s1 s2 s3 innermost in both, one 64-wide K
+    unit (18 K stages over the 9 taps) instead of a 4-wide unit padded to 32 (144)."""
+    steps = _steps("rtr", [4, 4, 4], [4, 4, 4], 3, 56, 256, 0.1)
+    node3 = [l for l in steps.splitlines() if l.startswith("fwd node3 tc")][0]
+    assert " kit=18 " in node3, node3
