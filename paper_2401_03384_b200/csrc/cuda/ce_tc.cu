@@ -1006,14 +1006,45 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
+          int wrap_tail = 32;  // first row of this warp's slab past the wrapped unit's inner extent
           if (lane == 0) {
             int c[5];
+            int wrap_d = -1;
 #pragma unroll
             for (int d = 0; d < 5; ++d) {
               const int qd = P.cdim_q[d];
               c[d] = cbase[d] + (qd == 1 ? q * P.c_slab : qd == 2 ? ch * 32 : 0);
+              if (qd == 3) wrap_d = d;
+            }
+            if (wrap_d >= 0) {  // flat row index -> (inner, outer) of the wrapped M unit
+              const int f = cbase[wrap_d] + q * 32;
+              const int io = f / P.c_wrap;
+              const int ii = f - io * P.c_wrap;
+#pragma unroll
+              for (int d = 0; d < 5; ++d) {
+                if (P.cdim_q[d] == 3) c[d] = ii;
+                if (P.cdim_q[d] == 4) c[d] = io;
+              }
+              wrap_tail = min(32, P.c_wrap - ii);  // TMA clips the rows past the inner extent
             }
             tma_store(&Pg.tc, buf, c, atomic);
+          }
+          if (P.c_wrap) {
+            // rows that cross into the next outer index: per-thread stores of this lane's row
+            // (a second box would need a negative start coordinate, which bulk stores reject)
+            wrap_tail = __shfl_sync(0xffffffffu, wrap_tail, 0);
+            const int64_t rt = rtab[q * 32 + lane];
+            if (lane >= wrap_tail && rt >= 0) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const int64_t co = cols[ch * 32 + i];
+                if (co < 0) continue;
+                if (atomic)
+                  atomicAdd(C + rt + co, __uint_as_float(ra[i]));
+                else
+                  C[rt + co] = __uint_as_float(ra[i]);
+              }
+            }
           }
         }
         if (chunk >= 0 && lane == 0) bulk_wait_all();  // tail chunk: writes done before its flag

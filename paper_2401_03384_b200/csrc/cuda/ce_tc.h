@@ -90,6 +90,11 @@ struct TcParams {
   int32_t c_tma;
   int32_t cdim_u[5], cdim_q[5];
   int32_t c_slab;     // rows of the outermost M unit per warp (its coordinate advances by q * c_slab)
+  // c_wrap > 0: the single M unit is [inner vars chaining in C, flat extent c_wrap][outer vars]
+  // (e.g. [w h][b] of an NCHW output, b not contiguous with h w): C dim cdim_q == 3 takes the
+  // inner index and cdim_q == 4 the outer one; a warp's 32 rows that cross into the next outer
+  // index are stored twice, the second box at inner coordinate - c_wrap (TMA clips both)
+  int32_t c_wrap;
   int32_t acc_out;    // 1: every item adds into C (a 3xTF32 correction launch); no memset, no tail split
   TcUnit u[TC_MAX_UNITS];
   int32_t nunits;

@@ -770,6 +770,7 @@ bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
       return !(e && *e == '0');
     }();
     P.c_tma = 0;
+    P.c_wrap = 0;
     auto chain = [&](const TcUnit& u) {
       for (int k = 1; k < u.nv; ++k)
         if (u.sc[k] != u.sc[k - 1] * u.vext[k - 1]) return false;
@@ -784,15 +785,45 @@ bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
       ok = inner_rows <= 32 && 32 % inner_rows == 0 && slab_last > 0 && ul.box % slab_last == 0 &&
            inner_rows * ul.box == P.m_rows;
     }
-    for (int i = 0; ok && i < P.nm; ++i) ok = chain(P.u[P.mt[i]]);
+    // a single M unit whose vars chain in C only in two groups (inner vars, then outer vars:
+    // [w h][b] of an NCHW output, the tile's 128 flat rows crossing b) is stored as two C dims,
+    // a warp slab crossing into the next outer index with a second, shifted box (c_wrap)
+    int wrap_split = 0;  // number of inner vars
+    int64_t wrap_ext = 0;
+    // opt-in (CE_TC_CWRAP=1): on cfg2's [w h][b] NCHW outputs the bulk stores of 32-row x
+    // 32-column boxes (32 separate 128-B rows each) were slower than the warps' coalesced
+    // per-column stores: step 1.008 -> 1.09 ms (same-box A/B x3)
+    static const bool wrap_on = [] {
+      const char* e = std::getenv("CE_TC_CWRAP");
+      return e && *e == '1';
+    }();
+    if (ok && wrap_on && P.nm == 1 && !chain(P.u[P.mt[0]]) && P.nm + 2 + P.ng <= 5) {
+      const TcUnit& u = P.u[P.mt[0]];
+      int j = 1;
+      int64_t e = u.vext[0];
+      while (j < u.nv && u.sc[j] == u.sc[j - 1] * u.vext[j - 1]) e *= u.vext[j++];
+      bool outer_chain = true;
+      for (int k = j + 1; k < u.nv; ++k) outer_chain = outer_chain && u.sc[k] == u.sc[k - 1] * u.vext[k - 1];
+      if (j < u.nv && outer_chain && e >= 32 && u.sc[j] % 4 == 0 && e * (u.ext / e) == u.ext) {
+        wrap_split = j;
+        wrap_ext = e;
+      }
+    }
+    for (int i = 0; ok && i < P.nm; ++i) ok = wrap_split > 0 || chain(P.u[P.mt[i]]);
     const TcUnit& un = P.u[P.nt[0]];
     ok = ok && chain(un) && (P.n_cols % 32 == 0 || P.tiles_n == 1);
     for (int i = 0; i < P.ng && ok; ++i) ok = chain(P.u[P.gu[i]]);
+    if (ok && wrap_split > 0 && P.nm + 2 + P.ng > 5) ok = false;
     if (ok) {
       const TcUnit& um0 = P.u[P.mt[0]];
       const bool rows_inner = um0.sc[0] == 1;
       const bool cols_inner = un.sc[0] == 1;
       ok = rows_inner != cols_inner;
+      static const bool rows_mode = [] {  // CE_TC_CTMA=2: only the columns-innermost mode
+        const char* e = std::getenv("CE_TC_CTMA");
+        return !(e && *e == '2');
+      }();
+      ok = ok && (rows_mode || cols_inner);
       // every stride but the inner one 16-B aligned
       for (int i = 0; ok && i < P.nm; ++i) ok = (rows_inner && i == 0) || P.u[P.mt[i]].sc[0] % 4 == 0;
       ok = ok && (cols_inner || un.sc[0] % 4 == 0);
@@ -810,6 +841,22 @@ bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
           ++d;
         };
         auto put_rows = [&] {  // M units fastest first; the last one carries the warp offset
+          if (wrap_split > 0) {  // inner vars (flat extent wrap_ext) and outer vars as two dims
+            const TcUnit& u = P.u[P.mt[0]];
+            P.cdim_u[d] = P.mt[0];
+            P.cdim_q[d] = 3;
+            plan->gdim_c[d] = static_cast<uint64_t>(wrap_ext);
+            plan->gstride_c[d] = static_cast<uint64_t>(u.sc[0]) * 4;
+            plan->box_c[d] = 32;
+            ++d;
+            P.cdim_u[d] = P.mt[0];
+            P.cdim_q[d] = 4;
+            plan->gdim_c[d] = static_cast<uint64_t>(u.ext / wrap_ext);
+            plan->gstride_c[d] = static_cast<uint64_t>(u.sc[wrap_split]) * 4;
+            plan->box_c[d] = 1;
+            ++d;
+            return;
+          }
           for (int i = 0; i + 1 < P.nm; ++i) put(P.mt[i], 0, static_cast<uint32_t>(P.u[P.mt[i]].box));
           put(P.mt[P.nm - 1], 1, static_cast<uint32_t>(slab_last));
         };
@@ -829,6 +876,7 @@ bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
           plan->box_c[d] = 1;
         }
         P.c_slab = static_cast<int32_t>(slab_last);
+        P.c_wrap = static_cast<int32_t>(wrap_split > 0 ? wrap_ext : 0);
         plan->swz_c = rows_inner ? 0 : 3;  // CU_TENSOR_MAP_SWIZZLE_128B for row-major 128-B rows
       }
     }
