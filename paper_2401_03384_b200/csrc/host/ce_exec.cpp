@@ -605,15 +605,54 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
   Step st;
   st.node = node;
   st.label = label;
+  if (std::getenv("CE_DESCRIBE_PROBLEMS")) {  // diagnostics: the lowered problem of every step
+    static const char* cn = "ZMNK";
+    std::fprintf(stderr, "[%s] nv=%d unary=%d acc=%d\n", label.c_str(), p.nv, p.unary, p.accumulate);
+    for (int v = 0; v < p.nv; ++v)
+      std::fprintf(stderr, "  v%d %c ext=%lld sa=%lld sb=%lld sc=%lld\n", v, cn[p.cls[v]], (long long)p.ext[v],
+                   (long long)p.sa[v], (long long)p.sb[v], (long long)p.sc[v]);
+    for (int side = 0; side < 2; ++side)
+      for (int g = 0; g < (side ? p.ng_b : p.ng_a); ++g) {
+        const CeGather& G = side ? p.gb[g] : p.ga[g];
+        std::fprintf(stderr, "  g%c%d pv=%d qv=%d sp=%d sq=%d c=%lld extent=%lld stride=%lld wrap=%d\n", side ? 'B' : 'A',
+                     g, G.pv, G.qv, G.sp, G.sq, (long long)G.c, (long long)G.extent, (long long)G.stride, G.wrap);
+      }
+  }
   // Tiny contractions (K <= 8, e.g. ResNet conv1's 3 input channels) with a large output
   // are output-bandwidth problems: the streaming SIMT kernel writes them with float4
   // stores and no per-tile epilogue, where the TC path would pad K to 32 and pay a
   // ~5 us epilogue for every 128-row tile.
+  // plane convolutions with few channels (RTR conv1's X * W4 and its adjoints, ce_pconv.cu):
+  // staged-window SIMT kernels instead of a 49x tap expansion / col2im split.  CE_PCONV=0 off.
+  static const bool pconv_on = [] {
+    const char* e = std::getenv("CE_PCONV");
+    return !(e && *e == '0');
+  }();
+  if (pconv_on && ce_pconv_plan(p, &st.pconv)) {
+    st.kind = Step::kPconv;
+    st.a = a;
+    st.b = b;
+    st.c = c;
+    st.flops = pending_flops_;
+    st.bytes = problem_bytes(p);
+    if (st.pconv.kind == 1) {
+      int64_t span = 0;
+      for (int v = 0; v < p.nv; ++v)
+        if (p.cls[v] != CE_K) span += (p.ext[v] - 1) * p.sc[v];
+      st.zero_elems = span + 1;
+    }
+    list.push_back(st);
+    return;
+  }
   const bool tiny_k = [&] {
     int64_t k = 1, outs = 1;
     for (int v = 0; v < p.nv; ++v) (p.cls[v] == CE_K ? k : outs) *= p.ext[v];
     for (int g = 0; g < p.ng_a; ++g) k *= 1;  // gathered taps are K vars already counted
-    return k <= 8 && outs >= (1ll << 20);
+    static const int64_t kmax = [] {  // CE_TINYK: K bound of this rule (experiment knob)
+      const char* e = std::getenv("CE_TINYK");
+      return e ? std::atoll(e) : 8;
+    }();
+    return k <= kmax && outs >= (1ll << 20);
   }();
   auto try_col2im = [&]() -> bool {
     static const bool col2im_on = [] {  // CE_COL2IM=0: no col2im split
@@ -1513,7 +1552,7 @@ float* Executor::resolve(const BufRef& r) const {
 }
 
 std::string Executor::describe() const {
-  static const char* kinds[] = {"direct", "tiled", "tc", "zero", "reduce", "permute", "dw2", "split"};
+  static const char* kinds[] = {"direct", "tiled", "tc", "zero", "reduce", "permute", "dw2", "split", "pconv"};
   std::string out;
   char line[512];
   for (const auto* list : {&fwd_, &bwd_})
@@ -1541,6 +1580,10 @@ std::string Executor::describe() const {
           }
           std::snprintf(line + n, sizeof line - n, "%s\n", u.c_str());
         }
+      } else if (st.kind == Step::kPconv) {
+        const CePconvDesc& q = st.pconv;
+        std::snprintf(line + n, sizeof line - n, " kind=%d planes=%lld pos=%dx%d taps=%dx%d signs=%d,%d ci=%d co=%d\n",
+                      q.kind, static_cast<long long>(q.P), q.OY, q.OX, q.KH, q.KW, q.sgn_h, q.sgn_w, q.Ci, q.Co);
       } else if (st.kind == Step::kDw2) {
         std::snprintf(line + n, sizeof line - n, " fused taps=%d J=%d signs=%d,%d store_mid=%d\n", st.dw2.KT, st.dw2.J,
                       st.dw2.SA, st.dw2.SB, st.dw2.write_mid);
@@ -1698,6 +1741,10 @@ void Executor::launch_step(Step& st, cudaStream_t s) {
       case Step::kPermute: e = ce_launch_permute(st.desc.p, A, C, s); break;
       case Step::kDw2: e = ce_launch_dw2(st.dw2, A, B, resolve(st.b2), C, resolve(st.c2), s); break;
       case Step::kSplit: e = ce_launch_split_tf32(A, C, resolve(st.c2), st.zero_elems, s); break;
+      case Step::kPconv:
+        if (st.pconv.kind == 1) e = cudaMemsetAsync(C, 0, static_cast<size_t>(st.zero_elems) * 4, s);
+        if (e == cudaSuccess) e = ce_launch_pconv(st.pconv, A, B, C, s);
+        break;
     }
     cuda_check(e, st.label.c_str());
     if (profiling_) cuda_check(cudaEventRecordWithFlags(st.ev1, s, cudaEventRecordExternal), "cudaEventRecord");

@@ -41,6 +41,7 @@ CASES = [
     ("cfg4 CP conv5_x cr0.1 B128", "cp", [512], [512], 3, 7, 128, 0.1),
     ("cfg4 CP conv1 cr1.0 B16", "cp", [64], [3], 7, 112, 16, 1.0),
     ("cfg3 RTR 64->128 @28 B64", "rtr", [4, 4, 8], [4, 4, 4], 3, 28, 64, 0.1),
+    ("cfg3 RTR conv1 @112 B32", "rtr", [4, 4, 4], [1, 1, 3], 7, 112, 32, 0.1),  # plane-conv kernels
     ("cfg3 RTR 256 @14 cr1.0 B256", "rtr", [4, 8, 8], [4, 8, 8], 3, 14, 256, 1.0),
 ]
 
