@@ -9,3 +9,7 @@ timeout 600 $NCU -k regex:ce_dwgrad_kernel -o gpurun_out/full_cp10_dwgrad python
 timeout 600 $NCU -k regex:ce_dw2_kernel -o gpurun_out/full_cp01_dw2 python $L2 > gpurun_out/ncuf3.log 2>&1
 timeout 600 $NCU -k regex:ce_transpose -o gpurun_out/full_tk10_permute python tools/run_layer.py tk 1.0 1 > gpurun_out/ncuf4.log 2>&1
 timeout 600 $NCU -k regex:ce_stream -o gpurun_out/full_cp_conv1_stream python tools/run_layer.py cp 1.0 1 64 3 7 112 32 > gpurun_out/ncuf5.log 2>&1
+# plane-conv kernels (ce_pconv.cu) on cfg3's RTR conv1 (B=256): forward and filter gradient
+L3="tools/prof_layer.py rtr 4,4,4 1,1,3 7 112 256 0.1"
+timeout 600 $NCU -k regex:ce_pconv_kernel -o gpurun_out/full_rtr_conv1_pconv python $L3 > gpurun_out/ncuf6.log 2>&1
+timeout 600 $NCU -k regex:ce_pconv_wgrad -o gpurun_out/full_rtr_conv1_pconv_wgrad python $L3 > gpurun_out/ncuf7.log 2>&1

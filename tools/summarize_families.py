@@ -17,6 +17,8 @@ CAPTURES = {
     "full_cp01_dw2": ("fused h+w stencil pair (ce_dw2_kernel, F1)", "CP conv2_x cr0.1 (R=27), forward pair"),
     "full_tk10_permute": ("permute (ce_transpose_kernel)", "cfg2 TK cr1.0, first transpose launch"),
     "full_cp_conv1_stream": ("stream, tiny K (ce_stream_blk_kernel)", "CP conv1 3->64 @112 B32 cr1.0, node0 (K=3)"),
+    "full_rtr_conv1_pconv": ("plane conv (ce_pconv_kernel)", "cfg3 RTR conv1 3->64 @112 B256, X * W4 (7x7, 9 channels)"),
+    "full_rtr_conv1_pconv_wgrad": ("plane-conv filter grad (ce_pconv_wgrad_kernel)", "same layer, dW4"),
 }
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
