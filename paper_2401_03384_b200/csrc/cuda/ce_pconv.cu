@@ -23,6 +23,7 @@
 #include "ce_pconv.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace {
@@ -404,8 +405,11 @@ bool ce_pconv_plan(const CeProblem& p, CePconvDesc* out) {
   d.tiles_y = kind == 0 ? (d.OY + kTY0 - 1) / kTY0 : (d.OY + kTY1 - 1) / kTY1;
   d.tiles_x = kind == 0 ? (d.OX + kTX0 - 1) / kTX0 : (d.OX + kTX1 - 1) / kTX1;
   // worth it only for large planes (the TC path's expansion / col2im costs scale with them)
+  // (CE_PCONV_MIN: the position threshold, read per plan so tests can lower it)
+  const char* mn = std::getenv("CE_PCONV_MIN");
+  const double min_pos = mn ? std::atof(mn) : static_cast<double>(1 << 20);
   const double positions = static_cast<double>(d.P) * d.OY * d.OX;
-  if (positions < (1 << 20) || d.OX < 16) return false;
+  if (positions < min_pos || d.OX < 16) return false;
   if (kind == 0) {
     if (co_instance(d.Co) < 0 || fwd_smem(d) > 200 * 1024) return false;
     int64_t cmax = 0;
