@@ -1283,7 +1283,7 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
       }
     }
   }
-  if (P.k_split > 1 && !plan.accum) {
+  if (P.k_split > 1 && !plan.accum && !plan.zeroed) {
     cudaError_t e = cudaMemsetAsync(C, 0, static_cast<size_t>(plan.out_span) * 4, s);
     if (e != cudaSuccess) return e;
   }

@@ -169,6 +169,7 @@ struct TcPlan {
   int64_t out_span = 0;       // elements of C to zero before a split-K launch
   uint32_t* tail_flags = nullptr;  // kTailFlags zeroed words owned by the executor (tail split)
   int accum = 0;                   // add into C instead of storing (3xTF32 correction terms)
+  int zeroed = 0;                  // split-K: C is zeroed by a separate (earlier) executor step
   const void* cached_a = nullptr;
   const void* cached_b = nullptr;
   const char* why = "";       // reason when not valid (diagnostics)

@@ -1190,7 +1190,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
           ts.desc = simt_desc(q);
           ts.flops = pending_flops_;
           ts.bytes = problem_bytes(q);
-          list.push_back(ts);
+          push_tc(list, ts);
           // staging -> the caller's layout (a unary permute over the output vars)
           CeProblem pk{};
           pk.unary = 1;
@@ -1264,7 +1264,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
         }
         return;
       }
-      list.push_back(st);
+      push_tc(list, st);
       return;
     }
   }
@@ -1392,6 +1392,37 @@ void Executor::add_recompute() {
   }
   for (Step& st : bwd_) remap(st);
   bwd_.insert(bwd_.begin(), pre.begin(), pre.end());
+}
+
+void Executor::push_tc(std::vector<Step>& list, Step& st) {
+  // CE_SPLITK_ZERO_STEP=0: the launch zeroes C itself (a memset node right before the kernel,
+  // which also ends the PDL chain)
+  static const bool zero_step = [] {
+    const char* e = std::getenv("CE_SPLITK_ZERO_STEP");
+    return !(e && *e == '0');
+  }();
+  if (zero_step && st.kind == Step::kTc && st.tc.params.k_split > 1 && !st.tc.accum && st.tc.out_span > 0) {
+    Step z;
+    z.kind = Step::kZero;
+    z.c = st.c;
+    z.zero_elems = st.tc.out_span;
+    z.node = st.node;
+    z.label = st.label + ":zero";
+    auto touches = [&](const Step& x) {
+      for (const BufRef* r : {&x.a, &x.b, &x.c, &x.b2, &x.c2})
+        if (r->kind == st.c.kind && r->index == st.c.index && r->kind != BufRef::kNone) return true;
+      return false;
+    };
+    std::size_t at = 0;
+    for (std::size_t i = list.size(); i-- > 0;)
+      if (touches(list[i])) {
+        at = i + 1;
+        break;
+      }
+    list.insert(list.begin() + static_cast<std::ptrdiff_t>(at), z);
+    st.tc.zeroed = 1;
+  }
+  list.push_back(st);
 }
 
 void Executor::build_forward() {

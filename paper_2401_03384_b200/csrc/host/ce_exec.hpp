@@ -92,6 +92,9 @@ class Executor {
   void ensure_workspace();
   void add_problem(std::vector<Step>& list, const CeProblem& p, BufRef a, BufRef b, BufRef c, int node,
                    const std::string& label);
+  // split-K TC step: its C memset becomes a kZero step placed right after the last earlier
+  // step touching C, so it runs off the critical path (on a side stream)
+  void push_tc(std::vector<Step>& list, Step& st);
   void build_forward();
   void build_backward();
   void run(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s);

@@ -17,3 +17,11 @@ timeout 600 $NCU --launch-skip 4 -o gpurun_out/full_tt10_grad6 python tools/run_
 timeout 600 $NCU --launch-skip 1 -o gpurun_out/full_tt10_node1 python tools/run_layer.py tt 1.0 1 > gpurun_out/ncu5.log 2>&1
 bash tools/ncu_families.sh
 timeout 1800 python tools/bench_configs.py --out gpurun_out/configs_$TAG.json > gpurun_out/configs.log 2>&1
+# summaries on the box (the .ncu-rep files can exceed gpurun's 64 MiB copy-back limit)
+mkdir -p gpurun_out/prof
+python tools/summarize_launches.py gpurun_out/launches.csv > gpurun_out/prof/ncu_launches_${TAG}_summary.txt 2>&1
+cp gpurun_out/launches.csv gpurun_out/prof/ncu_launches_${TAG}.csv
+python tools/summarize_ncu_full.py gpurun_out gpurun_out/prof $TAG > gpurun_out/prof/summarize_full.log 2>&1
+python tools/summarize_families.py gpurun_out gpurun_out/prof $TAG > gpurun_out/prof/summarize_families.log 2>&1
+du -sh gpurun_out/*.ncu-rep > gpurun_out/prof/rep_sizes.txt 2>&1
+rm -f gpurun_out/*.ncu-rep
