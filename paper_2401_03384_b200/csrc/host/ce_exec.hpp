@@ -95,6 +95,7 @@ class Executor {
   // split-K TC step: its C memset becomes a kZero step placed right after the last earlier
   // step touching C, so it runs off the critical path (on a side stream)
   void push_tc(std::vector<Step>& list, Step& st);
+  void early_packs(std::vector<Step>& list);
   void build_forward();
   void build_backward();
   void run(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s);
