@@ -1539,7 +1539,16 @@ void Executor::build_backward() {
     const std::size_t cid = static_cast<std::size_t>(n_) + jj;
     const int ids[2] = {node.left, node.right};
     const Subscripts* selfs[2] = {&op.left_self, &op.right_self};
-    for (int s = 0; s < 2; ++s) {
+    // the gradient that continues the chain (w.r.t. an intermediate) is issued before the
+    // leaf gradient (w.r.t. an input) when only the right operand is an intermediate.
+    // CE_CHAIN_FIRST=0: always left first.
+    static const bool chain_first = [] {
+      const char* e = std::getenv("CE_CHAIN_FIRST");
+      return !(e && *e == '0');
+    }();
+    const bool swap = chain_first && ids[0] < n_ && ids[1] >= n_;
+    for (int si = 0; si < 2; ++si) {
+      const int s = swap ? 1 - si : si;
       pending_flops_ = 2.0 * static_cast<double>(flops_actual(op));
       const auto id = static_cast<std::size_t>(ids[s]);
       const Adjoint which = s == 0 ? Adjoint::GradLeft : Adjoint::GradRight;
