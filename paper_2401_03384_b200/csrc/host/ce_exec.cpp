@@ -78,6 +78,7 @@ Executor::Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cf
     compute_deps(bwd_);
   }
   if (const char* e = std::getenv("CE_CONCURRENT"); e && *e == '0') concurrent_ = false;
+  if (const char* e = std::getenv("CE_STREAMS")) n_streams_ = std::max(2, std::min(kMaxStreams, std::atoi(e)));
   if (const char* dbg = std::getenv("CE_DEBUG"); dbg && *dbg == '1') std::fputs(describe().c_str(), stderr);
 }
 
@@ -172,7 +173,7 @@ Executor::~Executor() {
   for (auto* list : {&fwd_, &bwd_})
     for (Step& st : *list)
       if (st.done) cudaEventDestroy(st.done);
-  for (int k = 0; k < kStreams - 1; ++k) {
+  for (int k = 0; k < kMaxStreams - 1; ++k) {
     if (aux_[k]) cudaStreamDestroy(aux_[k]);
     if (join_ev_[k]) cudaEventDestroy(join_ev_[k]);
   }
@@ -1549,6 +1550,7 @@ void Executor::build_backward() {
     const bool swap = chain_first && ids[0] < n_ && ids[1] >= n_;
     for (int si = 0; si < 2; ++si) {
       const int s = swap ? 1 - si : si;
+      std::vector<Step>& gl = bwd_;
       pending_flops_ = 2.0 * static_cast<double>(flops_actual(op));
       const auto id = static_cast<std::size_t>(ids[s]);
       const Adjoint which = s == 0 ? Adjoint::GradLeft : Adjoint::GradRight;
@@ -1600,16 +1602,16 @@ void Executor::build_backward() {
       const BufRef a = s == 0 ? dcr : red_ref_[0][jj];
       const BufRef b = s == 0 ? red_ref_[1][jj] : dcr;
       if (selfs[s]->empty()) {
-        add_problem(bwd_, lower_pairwise(gop, red_view_[0][jj], red_view_[1][jj], dcv, gview[id], which), a, b,
+        add_problem(gl, lower_pairwise(gop, red_view_[0][jj], red_view_[1][jj], dcv, gview[id], which), a, b,
                     gref[id], static_cast<int>(id), label);
       } else {
         // d(reduced) then broadcast back over the self-contracted atoms
         View tmp = padded_view(red_view_[s][jj].subs, red_view_[s][jj].dims, 4);
         BufRef tref{BufRef::kWork, alloc(view_span(tmp))};
-        add_problem(bwd_, lower_pairwise(gop, red_view_[0][jj], red_view_[1][jj], dcv, tmp, which), a, b, tref,
+        add_problem(gl, lower_pairwise(gop, red_view_[0][jj], red_view_[1][jj], dcv, tmp, which), a, b, tref,
                     static_cast<int>(id), label);
         pending_flops_ = 0;
-        add_problem(bwd_, lower_unary(tmp, gview[id]), tref, {}, gref[id], static_cast<int>(id), label + ":bcast");
+        add_problem(gl, lower_unary(tmp, gview[id]), tref, {}, gref[id], static_cast<int>(id), label + ":bcast");
       }
     }
   }
@@ -1720,16 +1722,17 @@ void Executor::run(std::vector<Step>& steps, const std::vector<char>* need, cuda
 }
 
 void Executor::run_concurrent(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s) {
-  for (int k = 0; k < kStreams - 1; ++k)
+  for (int k = 0; k < n_streams_ - 1; ++k)
     if (!aux_[k]) {
       cuda_check(cudaStreamCreateWithFlags(&aux_[k], cudaStreamNonBlocking), "cudaStreamCreate");
       cuda_check(cudaEventCreateWithFlags(&join_ev_[k], cudaEventDisableTiming), "cudaEventCreate");
     }
   if (!fork_ev_) cuda_check(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming), "cudaEventCreate");
-  cudaStream_t streams[kStreams] = {s};
+  const int kStreams = n_streams_;
+  cudaStream_t streams[kMaxStreams] = {s};
   for (int k = 1; k < kStreams; ++k) streams[k] = aux_[k - 1];
-  int last[kStreams];
-  bool joined[kStreams] = {true};
+  int last[kMaxStreams];
+  bool joined[kMaxStreams] = {true};
   for (int k = 0; k < kStreams; ++k) last[k] = -1;
   for (int k = 1; k < kStreams; ++k) joined[k] = false;
   bool forked = false;

@@ -164,10 +164,11 @@ class Executor {
   bool use_graphs_ = false;
   // independent steps (e.g. the input- and factor-gradient of one node, a repack and the
   // step before it) run on side streams, forked from and joined back into the caller's
-  static constexpr int kStreams = 4;
+  static constexpr int kMaxStreams = 8;
+  int n_streams_ = 4;  // CE_STREAMS (2..8): the caller's stream + side streams
   bool concurrent_ = true;
-  cudaStream_t aux_[kStreams - 1] = {};
-  cudaEvent_t fork_ev_ = nullptr, join_ev_[kStreams - 1] = {};
+  cudaStream_t aux_[kMaxStreams - 1] = {};
+  cudaEvent_t fork_ev_ = nullptr, join_ev_[kMaxStreams - 1] = {};
   void launch_pass(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s, int which);
 
  public:
