@@ -736,8 +736,15 @@ bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
   {
     const int64_t csize = P.mcast ? 2 : 1;
     const int64_t ctas = (tm + csize - 1) / csize * csize * tn * gz;
+    // CE_SPLITK_SMS: SMs a split-K launch may fill (default all 148; the leaf gradients it
+    // serves run beside the backward chain)
+    static const int64_t sk_sms = [] {
+      const char* e = std::getenv("CE_SPLITK_SMS");
+      return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t{148};
+    }();
     int split = 1;
-    if (ctas < 148 && ki >= 16) split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 / ctas, ki / 8)));
+    if (ctas < 148 && ki >= 16)
+      split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sk_sms / ctas, ki / 8)));
     if (gz * split > 65535) return fail("grid z too large");
     P.k_split = split;
   }
