@@ -823,6 +823,18 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
     bool atomic;
     for (; work_next(P, ngroups, wi, item, k0, k1, atomic, chunk); ++local) {
       const int acc = static_cast<int>(local & 1);
+      // the CTA's last item: once its accumulator is full every MMA (and every smem read of
+      // the operand ring) is done and no load follows, so its TMA-store chunks may each take
+      // their own staging buffer in the ring instead of waiting for the previous chunk's
+      // store to release the warp's single buffer
+      bool last_item = false;
+      if (!PAIR && P.c_tma) {
+        WorkIter nx = wi;
+        uint32_t it2;
+        int a2, b2, c2;
+        bool at2;
+        last_item = !work_next(P, ngroups, nx, it2, a2, b2, at2, c2);
+      }
       if (et == 0) {  // (also for the other group's tiles: the incremental advance needs every item)
         if (wi.seq)
           advance_tile(P, T);
@@ -983,15 +995,16 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
       if (P.c_tma) {
         // TMA-store epilogue: this warp's 32 x 32 block of each chunk -> its 4 KB staging
         // buffer (1024-B aligned) -> one bulk tensor store (reduce-add when accumulating)
-        uint8_t* buf = reinterpret_cast<uint8_t*>(stage_out) + ew * 4096;
+        uint8_t* buf1 = reinterpret_cast<uint8_t*>(stage_out) + ew * 4096;
 #pragma unroll 1
         for (int ch = 0; ch < nch; ++ch) {
+          uint8_t* buf = last_item ? smem + (ew * (BN / 32) + ch) * 4096 : buf1;
           tmem_ld32_issue(t_base + ch * 32, ra);
           tmem_ld_wait(ra);
           if (empty_k)
 #pragma unroll
             for (int i = 0; i < 32; ++i) ra[i] = 0;
-          if (lane == 0) bulk_wait_read();  // the previous store has read the buffer
+          if (lane == 0 && !last_item) bulk_wait_read();  // the previous store has read the buffer
           __syncwarp();
           if (P.c_tma == 1) {  // rows innermost: column-major block, lanes write consecutive words
             float* b = reinterpret_cast<float*>(buf);
@@ -1154,6 +1167,11 @@ cudaError_t launch(const TcParams& P, float* C, cudaStream_t s, int per_sm = 1) 
       static_cast<int>(sizeof(TcParams)) + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static_assert(!LEAN || smem <= 113 * 1024, "LEAN: two CTAs per SM");
+  // the last item's TMA-store chunks are staged in the operand ring (one 4 KB buffer per warp
+  // and 32-column chunk, see the epilogue)
+  static_assert(STAGES * (TC_BM * 128 + (PAIR ? BN * 64 : BN * 128)) >=
+                    ((BN == 64 && !LEAN) ? 2 : 1) * kEpiWarps * (BN / 32) * 4096,
+                "operand ring too small for the last item's staging");
   // the dynamic-smem opt-in is a per-device function attribute
   static bool configured[kMaxDevices] = {};
   const int dev = current_device();
