@@ -1160,7 +1160,7 @@ int sm_count() {
 }
 
 template <int BN, int STAGES, bool PAIR, bool LEAN = false>
-cudaError_t launch(const TcParams& P, float* C, cudaStream_t s, int per_sm = 1) {
+cudaError_t launch(const TcParams& P, float* C, cudaStream_t s, int per_sm, int sms) {
   constexpr int smem =
       STAGES * (TC_BM * 128 + (PAIR ? BN * 64 : BN * 128)) + ((BN == 64 && !LEAN) ? 2 : 1) * kEpiWarps * 32 * kStagePitch * 4 +
       (2 * BN + 2 * (BN / 4) + 2 * TC_BM) * 8 + 4 * static_cast<int>(sizeof(Tile)) + 8 * (3 * STAGES + 4) + 16 + 64 +
@@ -1186,7 +1186,7 @@ cudaError_t launch(const TcParams& P, float* C, cudaStream_t s, int per_sm = 1) 
   }
   const int csize = P.mcast ? 2 : 1;
   const int64_t groups = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
-  const int64_t max_groups = static_cast<int64_t>(sm_count()) * per_sm / csize;
+  const int64_t max_groups = std::max<int64_t>(1, static_cast<int64_t>(sms) * per_sm / csize);
   const int grid = static_cast<int>((groups < max_groups ? groups : max_groups) * csize);
   (void)grid;
   return ce_launch_cluster(ce_tc_kernel<BN, STAGES, PAIR, LEAN>, dim3(grid), dim3(LEAN ? 64 + 32 * kEpiWarps : kThreads),
@@ -1254,11 +1254,12 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
   const bool lean = lean_mode > 0 && !P.mcast && plan.bn <= 128 && P.k_per <= lean_kmax &&
                     (P.native_mn || (!P.oa.mn_major && !P.ob.mn_major)) && !(P.oa.mn_major && P.oa.wide);
   const int per_sm = lean ? (lean_mode >= 2 ? 2 : 1) : 1;
+  const int sms = plan.sm_budget > 0 ? std::min(plan.sm_budget, sm_count()) : sm_count();
   {
     // stream-K tail of a partial last round (see TcParams::sk_r)
     const int64_t csize = P.mcast ? 2 : 1;
     const int64_t items = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
-    const int64_t ngroups = std::min<int64_t>(items, static_cast<int64_t>(sm_count()) * per_sm / csize);
+    const int64_t ngroups = std::min<int64_t>(items, std::max<int64_t>(1, static_cast<int64_t>(sms) * per_sm / csize));
     P.n_items = static_cast<uint32_t>(items);
     P.sk_full = 0;
     P.sk_r = 0;
@@ -1307,19 +1308,19 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
   }
   if (P.mcast == 2) {
     switch (plan.bn) {
-      case 64: return launch<64, 9, true>(P, C, s);
-      case 128: return launch<128, 8, true>(P, C, s);
-      default: return launch<256, 6, true>(P, C, s);
+      case 64: return launch<64, 9, true>(P, C, s, 1, sms);
+      case 128: return launch<128, 8, true>(P, C, s, 1, sms);
+      default: return launch<256, 6, true>(P, C, s, 1, sms);
     }
   }
   if (lean) {
-    if (plan.bn == 64) return launch<64, 3, false, true>(P, C, s, per_sm);
-    return launch<128, 2, false, true>(P, C, s, per_sm);
+    if (plan.bn == 64) return launch<64, 3, false, true>(P, C, s, per_sm, sms);
+    return launch<128, 2, false, true>(P, C, s, per_sm, sms);
   }
   switch (plan.bn) {
-    case 64: return launch<64, 7, false>(P, C, s);
-    case 128: return launch<128, 6, false>(P, C, s);
-    default: return launch<256, 4, false>(P, C, s);
+    case 64: return launch<64, 7, false>(P, C, s, 1, sms);
+    case 128: return launch<128, 6, false>(P, C, s, 1, sms);
+    default: return launch<256, 4, false>(P, C, s, 1, sms);
   }
 }
 

@@ -170,6 +170,7 @@ struct TcPlan {
   uint32_t* tail_flags = nullptr;  // kTailFlags zeroed words owned by the executor (tail split)
   int accum = 0;                   // add into C instead of storing (3xTF32 correction terms)
   int zeroed = 0;                  // split-K: C is zeroed by a separate (earlier) executor step
+  int sm_budget = 0;               // > 0: SMs this launch may occupy (it co-runs with a sibling step)
   const void* cached_a = nullptr;
   const void* cached_b = nullptr;
   const char* why = "";       // reason when not valid (diagnostics)

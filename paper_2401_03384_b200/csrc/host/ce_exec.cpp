@@ -72,6 +72,7 @@ Executor::Executor(const EvaluationPlan& plan, bool want_backward, ExecConfig cf
   // under), then again once buffers share memory (those extra edges are already implied)
   compute_deps(fwd_);
   compute_deps(bwd_);
+  share_sms(bwd_);
   assign_offsets();
   if (ws_reuse_mode_ >= 2) {  // (mode 1 shares only along edges the identity hazards already imply)
     compute_deps(fwd_);
@@ -1431,6 +1432,81 @@ void Executor::early_packs(std::vector<Step>& list) {
   for (Step& st : rest) list.push_back(std::move(st));
 }
 
+// Sibling TC steps (consecutive in the list, neither depending on the other -- a node's two
+// adjoints) run concurrently on two streams; each persistent grid would otherwise take every
+// SM and the second would wait for the first's CTAs to drain.  They get SM budgets
+// proportional to their MMA work (tiles x K stages x MMA width) so both finish together.
+// CE_SM_SHARE=0 off.
+void Executor::share_sms(std::vector<Step>& steps) {
+  static const int mode = [] {  // 0 off, 1 proportional to the MMA work, 2 min-max rounds model
+    const char* e = std::getenv("CE_SM_SHARE");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (mode <= 0) return;
+  const std::size_t n = steps.size();
+  std::vector<std::vector<char>> reach(n, std::vector<char>(n, 0));  // reach[i][j]: i after j
+  for (std::size_t i = 0; i < n; ++i)
+    for (int j : steps[i].deps) {
+      reach[i][static_cast<std::size_t>(j)] = 1;
+      for (std::size_t k = 0; k < n; ++k)
+        if (reach[static_cast<std::size_t>(j)][k]) reach[i][k] = 1;
+    }
+  // the plan node whose adjoint a backward step computes: the consumer of its operand id
+  std::vector<int> consumer(static_cast<std::size_t>(n_) + plan_.nodes.size(), -1);
+  for (std::size_t jj = 0; jj < plan_.nodes.size(); ++jj) {
+    consumer[static_cast<std::size_t>(plan_.nodes[jj].left)] = static_cast<int>(jj);
+    consumer[static_cast<std::size_t>(plan_.nodes[jj].right)] = static_cast<int>(jj);
+  }
+  auto pnode = [&](const Step& st) {
+    return st.node >= 0 && static_cast<std::size_t>(st.node) < consumer.size() ? consumer[static_cast<std::size_t>(st.node)]
+                                                                               : -1;
+  };
+  auto work = [](const Step& st) {
+    const TcParams& P = st.tc.params;
+    return static_cast<double>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_iters * P.n_mma;
+  };
+  for (std::size_t i = 0; i < n; ++i) {
+    if (steps[i].kind != Step::kTc || steps[i].tc.sm_budget) continue;
+    std::size_t k = i + 1;
+    while (k < n && steps[k].kind != Step::kTc) ++k;
+    if (k >= n || steps[k].tc.sm_budget || reach[k][i] || pnode(steps[i]) < 0 || pnode(steps[k]) != pnode(steps[i]))
+      continue;
+    // budgets minimising the later finish: rounds of items x per-item time (K stages x MMA
+    // width); kept only if that beats running each on all SMs one after the other
+    auto items = [](const Step& st) {
+      const TcParams& P = st.tc.params;
+      return static_cast<int64_t>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_split;
+    };
+    auto per_item = [](const Step& st) {
+      const TcParams& P = st.tc.params;
+      return static_cast<double>((P.k_iters + P.k_split - 1) / P.k_split) * P.n_mma;
+    };
+    const int64_t ia = items(steps[i]), ib = items(steps[k]);
+    const double ta = per_item(steps[i]), tb = per_item(steps[k]);
+    auto rounds = [](int64_t it, int64_t sms) { return static_cast<double>((it + sms - 1) / sms); };
+    const double serial = rounds(ia, 148) * ta + rounds(ib, 148) * tb;
+    double best = 1e300;
+    int ba = 0;
+    for (int x = 8; x <= 140; ++x) {
+      const double c = std::max(rounds(ia, x) * ta, rounds(ib, 148 - x) * tb);
+      if (c < best) {
+        best = c;
+        ba = x;
+      }
+    }
+    if (mode == 1) {
+      const double wa = work(steps[i]), wb = work(steps[k]);
+      ba = std::max(16, std::min(132, static_cast<int>(148.0 * wa / (wa + wb) + 0.5)));
+      best = 0;
+    }
+    if (ba > 0 && best < 0.9 * serial) {
+      steps[i].tc.sm_budget = ba;
+      steps[k].tc.sm_budget = 148 - ba;
+    }
+    i = k;
+  }
+}
+
 void Executor::push_tc(std::vector<Step>& list, Step& st) {
   // CE_SPLITK_ZERO_STEP=0: the launch zeroes C itself (a memset node right before the kernel,
   // which also ends the PDL chain)
@@ -1639,9 +1715,10 @@ std::string Executor::describe() const {
       if (st.kind == Step::kTc) {
         const TcParams& P = st.tc.params;
         std::snprintf(line + n, sizeof line - n,
-                      " bn=%d rows=%d cols=%d mma_n=%d tiles=%dx%dx%d split=%d kit=%d amn=%d bmn=%d tr=%d mc=%d ctma=%d\n", st.tc.bn,
+                      " bn=%d rows=%d cols=%d mma_n=%d tiles=%dx%dx%d split=%d kit=%d amn=%d bmn=%d tr=%d mc=%d ctma=%d%s\n", st.tc.bn,
                       P.m_rows, P.n_cols, P.n_mma, P.tiles_m, P.tiles_n, P.grid_z, P.k_split, P.k_iters, P.oa.mn_major,
-                      P.ob.mn_major, P.transpose_store, P.mcast, P.c_tma);
+                      P.ob.mn_major, P.transpose_store, P.mcast, P.c_tma,
+                      st.tc.sm_budget ? (" sms=" + std::to_string(st.tc.sm_budget)).c_str() : "");
         if (std::getenv("CE_DESCRIBE_UNITS")) {
           std::string u = " ";
           n = static_cast<int>(std::strlen(line)) - 1;  // before the newline

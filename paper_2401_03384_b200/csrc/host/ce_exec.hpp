@@ -96,6 +96,7 @@ class Executor {
   // step touching C, so it runs off the critical path (on a side stream)
   void push_tc(std::vector<Step>& list, Step& st);
   void early_packs(std::vector<Step>& list);
+  void share_sms(std::vector<Step>& steps);
   void build_forward();
   void build_backward();
   void run(std::vector<Step>& steps, const std::vector<char>* need, cudaStream_t s);
