@@ -1495,7 +1495,11 @@ void Executor::share_sms(std::vector<Step>& steps) {
       }
     }
     if (mode == 1) {
-      const double wa = work(steps[i]), wb = work(steps[k]);
+      static const double bias = [] {  // CE_SM_BIAS: weight of the first (chain) sibling's work
+        const char* e = std::getenv("CE_SM_BIAS");
+        return e ? std::atof(e) : 1.0;
+      }();
+      const double wa = bias * work(steps[i]), wb = work(steps[k]);
       ba = std::max(16, std::min(132, static_cast<int>(148.0 * wa / (wa + wb) + 0.5)));
       best = 0;
     }
