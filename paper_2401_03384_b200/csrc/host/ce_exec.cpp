@@ -1908,7 +1908,7 @@ void Executor::launch_step(Step& st, cudaStream_t s) {
     }
     cuda_check(e, st.label.c_str());
     if (profiling_) cuda_check(cudaEventRecordWithFlags(st.ev1, s, cudaEventRecordExternal), "cudaEventRecord");
-    ++last_launches_;
+    if (st.kind != Step::kZero) ++last_launches_;  // (kernels only: a zero step is a memset)
   }
 }
 
