@@ -132,7 +132,11 @@ bool Executor::hoist_packs() {
     if (elems != pk_elems) continue;  // not a pure permute of the whole buffer
     // only buffers whose round trip matters (>= 64 MB): small packs are cheap, and their
     // consumers' tile plans are tuned to the padded result order
-    if (elems < 16.0 * 1024 * 1024) continue;
+    static const double min_elems = [] {  // CE_HOIST_MIN_MB (default 64)
+      const char* e = std::getenv("CE_HOIST_MIN_MB");
+      return (e ? std::atof(e) : 64.0) * 1024.0 * 1024.0 / 4.0;
+    }();
+    if (elems < min_elems) continue;
     View nv = v;
     bool ok = true;
     for (std::size_t i = 0; i < v.dims.size() && ok; ++i) {
