@@ -1442,9 +1442,12 @@ void Executor::early_packs(std::vector<Step>& list) {
 // proportional to their MMA work (tiles x K stages x MMA width) so both finish together.
 // CE_SM_SHARE=0 off.
 void Executor::share_sms(std::vector<Step>& steps) {
-  static const int mode = [] {  // 0 off, 1 proportional to the MMA work, 2 min-max rounds model
+  // Opt-in: cfg2 step 0.969 -> 0.956 ms, but cfg3 72.6 -> 96.6 ms and cfg4 8.4 -> 10.6 ms
+  // (one-round split-K siblings then need several rounds), and every budgeted kernel runs on a
+  // fraction of the GPU.  0 off (default), 1 proportional to the MMA work, 2 min-max rounds.
+  static const int mode = [] {
     const char* e = std::getenv("CE_SM_SHARE");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   if (mode <= 0) return;
   const std::size_t n = steps.size();
