@@ -418,7 +418,7 @@ __device__ __forceinline__ bool work_next(const TcParams& P, uint32_t ngroups, W
   item = P.sk_full + t;
   k0 = chunk * P.k_iters / P.tl_s;
   k1 = (chunk + 1) * P.k_iters / P.tl_s;
-  atomic = chunk > 0;
+  atomic = chunk > 0 || P.tl_zeroed;
   return true;
 }
 
@@ -896,7 +896,7 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
       }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (local == 0) ce_pdl_wait();  // (long complete: the producer waited before its loads)
-      if (chunk > 0) {  // tail chunk: chunk 0 of this item must have stored its partial tile
+      if (chunk > 0 && !P.tl_zeroed) {  // tail chunk: chunk 0 of this item must have stored its partial tile
         if (et == 0) {
           const uint32_t* f = P.tl_flags + (item - P.sk_full);
           uint32_t v;
@@ -1060,7 +1060,7 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
             }
           }
         }
-        if (chunk >= 0 && lane == 0) bulk_wait_all();  // tail chunk: writes done before its flag
+        if (chunk >= 0 && !P.tl_zeroed && lane == 0) bulk_wait_all();  // tail chunk: writes done before its flag
       } else {
 #pragma unroll 1
         for (int ch = 0; ch < nch; ++ch) {
@@ -1070,7 +1070,7 @@ __global__ void __launch_bounds__(LEAN ? 64 + 32 * kEpiWarps : kThreads, LEAN ? 
         }
       }
       if (est) stamp_it(P, 2, static_cast<uint32_t>(local / ngrp) * 4 + 3);
-      if (chunk >= 0) {  // tail chunk stored / added: count it; the last one resets the flag
+      if (chunk >= 0 && !P.tl_zeroed) {  // tail chunk stored / added: count it; the last one resets the flag
         epi_bar(1 + grp);
         if (et == 0) {
           uint32_t* f = P.tl_flags + (item - P.sk_full);
@@ -1206,6 +1206,78 @@ int debug_flags() {
 
 }  // namespace
 
+namespace {
+// Launch shape of a plan on the current device: LEAN instance and CTAs per SM, SMs used, work
+// items, groups (persistent CTAs, or CTA pairs), and the tail split of a partial last round
+// (r items cut into S K chunks; S = 1: none).
+struct TcShape {
+  bool lean;
+  int per_sm, sms;
+  int64_t items, ngroups;
+  bool contig;
+  int64_t r;
+  int S;
+};
+TcShape tc_shape(const TcPlan& plan) {
+  const TcParams& P = plan.params;
+  static const int lean_mode = [] {
+    const char* e = getenv("CE_TC_LEAN");
+    return e ? atoi(e) : 2;
+  }();
+  static const int lean_kmax = [] {
+    const char* e = getenv("CE_TC_LEAN_KMAX");
+    return e ? atoi(e) : 24;
+  }();
+  static const bool contig_on = [] {
+    const char* e = getenv("CE_TC_CONTIG");
+    return !(e && *e == '0');
+  }();
+  static const int tail_on = [] {
+    const char* e = getenv("CE_TC_TAIL");
+    return e ? atoi(e) : 1;
+  }();
+  // (long K loops only when chunk 0 stores and the others wait for it: with ~24 K stages that
+  // fixup costs what the shorter round saves -- tt1.0's 24/27-stage convs were slower,
+  // tk1.0's 72-stage convs 74 -> 68 us; with C zeroed beforehand every chunk just adds)
+  static const int tail_kmin = [] {
+    const char* e = getenv("CE_TC_TAIL_KMIN");
+    return e ? atoi(e) : 48;
+  }();
+  static const int tail_zkmin = [] {
+    const char* e = getenv("CE_TC_TAIL_ZKMIN");
+    return e ? atoi(e) : 16;
+  }();
+  TcShape t{};
+  t.lean = lean_mode > 0 && !P.mcast && plan.bn <= 128 && P.k_per <= lean_kmax &&
+           (P.native_mn || (!P.oa.mn_major && !P.ob.mn_major)) && !(P.oa.mn_major && P.oa.wide);
+  t.per_sm = t.lean ? (lean_mode >= 2 ? 2 : 1) : 1;
+  t.sms = plan.sm_budget > 0 ? std::min(plan.sm_budget, sm_count()) : sm_count();
+  const int64_t csize = P.mcast ? 2 : 1;
+  t.items = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
+  t.ngroups = std::min<int64_t>(t.items, std::max<int64_t>(1, static_cast<int64_t>(t.sms) * t.per_sm / csize));
+  t.contig = contig_on && csize == 1 && P.k_split == 1 && t.items >= 4 * t.ngroups;
+  t.r = 0;
+  t.S = 1;
+  const int kmin = plan.tail_zeroed ? tail_zkmin : tail_kmin;
+  if (tail_on && !plan.accum && (plan.tail_flags || plan.tail_zeroed) && !t.contig && P.k_split == 1 && csize == 1 &&
+      t.items > t.ngroups && t.items % t.ngroups != 0 && P.k_iters >= kmin) {
+    const int64_t r = t.items % t.ngroups;
+    const int64_t S = std::min<int64_t>({4, t.ngroups / r, P.k_iters / 4});
+    if (S >= 2 && r <= kTailFlags) {
+      t.r = r;
+      t.S = static_cast<int>(S);
+    }
+  }
+  return t;
+}
+}  // namespace
+
+bool ce_tc_tail_split(const TcPlan& plan) {
+  TcPlan q = plan;
+  q.tail_zeroed = 1;  // (the flags buffer is bound at run time; the zeroed mode needs none)
+  return tc_shape(q).S > 1;
+}
+
 cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C, cudaStream_t s) {
   if (!plan.valid) return cudaErrorInvalidValue;
   TcParams& P = plan.params;
@@ -1243,63 +1315,35 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
   // and no in-smem transposes.  CE_TC_LEAN: 0 off, 1 one CTA of this launch per SM (the
   // second slot takes the next kernel's set-up), 2 (default) two CTAs of this launch per SM.
   // cfg2 step (same-box A/B x3): off 1.127-1.131, 1 1.131-1.138, 2 1.119-1.121 ms.
-  static const int lean_mode = [] {
-    const char* e = getenv("CE_TC_LEAN");
-    return e ? atoi(e) : 2;
-  }();
-  static const int lean_kmax = [] {
-    const char* e = getenv("CE_TC_LEAN_KMAX");
-    return e ? atoi(e) : 24;
-  }();
-  const bool lean = lean_mode > 0 && !P.mcast && plan.bn <= 128 && P.k_per <= lean_kmax &&
-                    (P.native_mn || (!P.oa.mn_major && !P.ob.mn_major)) && !(P.oa.mn_major && P.oa.wide);
-  const int per_sm = lean ? (lean_mode >= 2 ? 2 : 1) : 1;
-  const int sms = plan.sm_budget > 0 ? std::min(plan.sm_budget, sm_count()) : sm_count();
+  const TcShape sh = tc_shape(plan);
+  const bool lean = sh.lean;
+  const int per_sm = sh.per_sm;
+  const int sms = sh.sms;
   {
-    // stream-K tail of a partial last round (see TcParams::sk_r)
-    const int64_t csize = P.mcast ? 2 : 1;
-    const int64_t items = (static_cast<int64_t>(P.tiles_m) + csize - 1) / csize * P.tiles_n * P.grid_z * P.k_split;
-    const int64_t ngroups = std::min<int64_t>(items, std::max<int64_t>(1, static_cast<int64_t>(sms) * per_sm / csize));
-    P.n_items = static_cast<uint32_t>(items);
+    P.n_items = static_cast<uint32_t>(sh.items);
     P.sk_full = 0;
     P.sk_r = 0;
     P.contig = 0;
-    static const bool contig_on = [] {
-      const char* e = getenv("CE_TC_CONTIG");
-      return !(e && *e == '0');
-    }();
-    if (contig_on && csize == 1 && P.k_split == 1 && items >= 4 * ngroups) {
+    if (sh.contig) {
       P.contig = 1;
-      P.ipg = static_cast<uint32_t>(items / ngroups);
-      P.irem = static_cast<uint32_t>(items % ngroups);
+      P.ipg = static_cast<uint32_t>(sh.items / sh.ngroups);
+      P.irem = static_cast<uint32_t>(sh.items % sh.ngroups);
     }
     P.dkit = tc_div(static_cast<uint32_t>(std::max(1, P.k_iters)));
     // tail split of a partial last round (see work_next): the r items left after the full
     // rounds are each cut into S = min(4, ngroups / r) K chunks run by the otherwise idle
     // groups; chunk 0 stores, the others wait for it (P.tl_flags, zeroed by the executor and
-    // left zero by the last chunk) and add.  CE_TC_TAIL=0 off.
-    static const int tail_on = [] {
-      const char* e = getenv("CE_TC_TAIL");
-      return e ? atoi(e) : 1;
-    }();
+    // left zero by the last chunk) and add -- or, when the executor zeroed C beforehand
+    // (plan.tail_zeroed), every chunk adds without a handshake.  CE_TC_TAIL=0 off.
     P.tl_s = 1;
     P.tl_flags = plan.tail_flags;
+    P.tl_zeroed = 0;
     P.acc_out = plan.accum ? 1 : 0;
-    // (long K loops only: with ~24 K stages the chunks' fixup costs what the shorter round
-    // saves -- tt1.0's 24/27-stage convs were slower; tk1.0's 72-stage convs 74 -> 68 us)
-    static const int tail_kmin = [] {
-      const char* e = getenv("CE_TC_TAIL_KMIN");
-      return e ? atoi(e) : 48;
-    }();
-    if (tail_on && !plan.accum && plan.tail_flags && !P.contig && P.k_split == 1 && csize == 1 && items > ngroups &&
-        items % ngroups != 0 && P.k_iters >= tail_kmin) {
-      const int64_t r = items % ngroups;
-      const int64_t S = std::min<int64_t>({4, ngroups / r, P.k_iters / 4});
-      if (S >= 2 && r <= kTailFlags) {
-        P.sk_full = static_cast<uint32_t>(items - r);
-        P.sk_r = static_cast<uint32_t>(r);
-        P.tl_s = static_cast<int32_t>(S);
-      }
+    if (sh.S > 1) {
+      P.sk_full = static_cast<uint32_t>(sh.items - sh.r);
+      P.sk_r = static_cast<uint32_t>(sh.r);
+      P.tl_s = sh.S;
+      P.tl_zeroed = plan.tail_zeroed ? 1 : 0;
     }
   }
   if (P.k_split > 1 && !plan.accum && !plan.zeroed) {

@@ -132,6 +132,7 @@ struct TcParams {
   uint32_t sk_r;     // tail items, each split into tl_s K chunks
   int32_t tl_s;      // K chunks per tail item
   uint32_t* tl_flags;// per tail item: chunks finished (chunk 0 first); zero between launches
+  int32_t tl_zeroed; // 1: C was zeroed beforehand -- every tail chunk adds, no flag handshake
   TcDiv dkit;        // k_iters
   // contiguous assignment (set per launch for many small tiles, no K split, no pairs):
   // group g takes items [g*ipg + min(g, rem), ...) in order, so the tile origins advance
@@ -171,6 +172,7 @@ struct TcPlan {
   int accum = 0;                   // add into C instead of storing (3xTF32 correction terms)
   int zeroed = 0;                  // split-K: C is zeroed by a separate (earlier) executor step
   int sm_budget = 0;               // > 0: SMs this launch may occupy (it co-runs with a sibling step)
+  int tail_zeroed = 0;             // the executor zeroes C before the launch (tail chunks all add)
   const void* cached_a = nullptr;
   const void* cached_b = nullptr;
   const char* why = "";       // reason when not valid (diagnostics)
@@ -178,4 +180,7 @@ struct TcPlan {
 
 // Decides whether a lowered problem maps onto the tcgen05 kernel and fills the plan.
 bool ce_tc_plan(const CeProblem& p, TcPlan* out);
+// Whether the launch of this plan will split a partial last round into K chunks (tail split,
+// see ce_tc.cu) on the current device -- the executor then zeroes C beforehand.
+bool ce_tc_tail_split(const TcPlan& plan);
 cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C, cudaStream_t s);

@@ -1525,7 +1525,19 @@ void Executor::push_tc(std::vector<Step>& list, Step& st) {
     const char* e = std::getenv("CE_SPLITK_ZERO_STEP");
     return !(e && *e == '0');
   }();
-  if (zero_step && st.kind == Step::kTc && st.tc.params.k_split > 1 && !st.tc.accum && st.tc.out_span > 0) {
+  // Opt-in (CE_TC_TAIL_ZERO=1): a TC launch that will split its partial last round into K
+  // chunks gets C zeroed by the same kind of early zero step, so every chunk adds without the
+  // chunk-0-first flag handshake (and the split then also applies from 16 K stages,
+  // CE_TC_TAIL_ZKMIN).  Measured: 0.964 -> 0.989 ms with the 16-stage threshold (tt1.0's
+  // 24/27-stage convs), 0.966 -> 0.968 ms at 48 stages -- not kept.
+  static const bool tail_zero = [] {
+    const char* e = std::getenv("CE_TC_TAIL_ZERO");
+    return e && *e == '1';
+  }();
+  const bool tail = tail_zero && st.kind == Step::kTc && st.tc.params.k_split == 1 && !st.tc.accum &&
+                    st.tc.out_span > 0 && ce_tc_tail_split(st.tc);
+  if (tail) st.tc.tail_zeroed = 1;
+  if (zero_step && st.kind == Step::kTc && (st.tc.params.k_split > 1 || tail) && !st.tc.accum && st.tc.out_span > 0) {
     Step z;
     z.kind = Step::kZero;
     z.c = st.c;
