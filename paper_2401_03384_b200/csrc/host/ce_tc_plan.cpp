@@ -417,6 +417,15 @@ bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
       if (p.cls[v] == CE_N) n_elems *= static_cast<double>(p.ext[v]);
     }
     if (n_elems > 128 && k_elems <= static_cast<double>(shortk_kmax) * TC_BK) ncap = std::min(ncap, 128);
+    // experiment (CE_TC_N3=<K stages>): 257..384 columns in three <=128-wide tiles when the K
+    // loop is short enough for the LEAN instances (tt1.0's N = 273 convs: 392 tiles over 148
+    // SMs = 2.65 rounds, or 588 over 296 LEAN slots = 1.99)
+    static const int n3_kmax = [] {
+      const char* e = std::getenv("CE_TC_N3");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (n3_kmax > 0 && n_elems > 256 && n_elems <= 384 && k_elems <= static_cast<double>(n3_kmax) * TC_BK)
+      ncap = std::min(ncap, 128);
   }
   P.n_cols = tile(B, b_mn == 1, CE_N, ncap, P.nt, &P.nn, TC_SRC_NTILE);
   if (P.nm == 0) return fail("no M tile unit");
