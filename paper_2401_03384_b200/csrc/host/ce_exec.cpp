@@ -596,6 +596,29 @@ int inner_var(const CeProblem& p, bool side_b) {
   return -1;
 }
 
+// An operand of `q` read from an existing repack of its buffer instead: every var (and
+// gathered axis) stride is mapped through the pack's axes (atoms merged into one pack axis
+// keep their relative strides).  False if a stride has no image.
+bool remap_operand(CeProblem& q, bool side_b, const CeProblem& pk) {
+  auto map = [&](int64_t st, int64_t ext, int64_t* out) {
+    for (int k = 0; k < pk.nv; ++k) {
+      const int64_t s0 = pk.sa[k];
+      if (s0 <= 0 || st < s0 || st % s0 != 0 || (st / s0) * ext > pk.ext[k]) continue;
+      *out = pk.sc[k] * (st / s0);
+      return true;
+    }
+    return false;
+  };
+  int64_t* s = side_b ? q.sb : q.sa;
+  CeGather* g = side_b ? q.gb : q.ga;
+  const int ng = side_b ? q.ng_b : q.ng_a;
+  for (int v = 0; v < q.nv; ++v)
+    if (s[v] && q.ext[v] > 1 && !map(s[v], q.ext[v], &s[v])) return false;
+  for (int i = 0; i < ng; ++i)
+    if (!map(g[i].stride, g[i].extent, &g[i].stride)) return false;
+  return true;
+}
+
 // Plain K vars shared by A and B, ordered by their stride in `side` (ascending).
 std::vector<int> shared_k_order(const CeProblem& p, bool by_b) {
   std::vector<int> v;
@@ -948,6 +971,85 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
           best_t = t;
         }
       }
+      // or read one operand from a repack of its buffer an earlier step already made (free;
+      // e.g. RTR 64->128's dW1 reads N0 and dN1 in the layouts node1 and dN0's step packed
+      // them into), the other as it is or repacked to match.  CE_PACK_REUSE=0 off.
+      static const bool reuse_on = [] {
+        const char* e = std::getenv("CE_PACK_REUSE");
+        return !(e && *e == '0');
+      }();
+      int reuse_side = -1;
+      const PackRecord* reuse_rec = nullptr;
+      bool reuse_pack_other = false;
+      CeProblem reuse_pk{};
+      int64_t reuse_span = 0;
+      for (int side = 0; side < 2 && reuse_on && !first_legal; ++side) {
+        const BufRef src = side ? b : a;
+        for (const PackRecord& r : packs_) {
+          if (r.src.kind != src.kind || r.src.index != src.index) continue;
+          // (large buffers only: the stage model above does not price the MN-major reads a
+          // reused layout often implies -- with small ones, RTR 64->64 went 1.9 -> 2.9 ms)
+          static const double min_elems = [] {  // CE_PACK_REUSE_MIN_MB (default 256)
+            const char* e = std::getenv("CE_PACK_REUSE_MIN_MB");
+            return (e ? std::atof(e) : 256.0) * 1024.0 * 1024.0 / 4.0;
+          }();
+          if (operand_elems(r.pk, 0) < min_elems) continue;
+          CeProblem q = p;
+          if (!remap_operand(q, side == 1, r.pk)) continue;
+          for (int other = 0; other < 2; ++other) {
+            CeProblem q2 = q;
+            CeProblem pk2{};
+            int64_t span2 = 0;
+            if (other) {
+              std::vector<int> order = shared_k_order(q, side == 1);
+              if (order.empty()) continue;
+              pk2 = repack(q2, side == 0, order, &span2, side ? q.sb : q.sa);
+            }
+            TcPlan t;
+            if (!ce_tc_plan(q2, &t)) continue;
+            const TcParams& P = t.params;
+            double us = static_cast<double>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_iters * 0.25 / 148.0;
+            if (other && !reusable(side ? a : b, pk2)) us += 8.0 * operand_elems(pk2, 0) / 3.0e6;
+            if (us < best_us) {
+              best_us = us;
+              best = -1;
+              reuse_side = side;
+              reuse_rec = &r;
+              reuse_pack_other = other == 1;
+              reuse_pk = pk2;
+              reuse_span = span2;
+              best_q = q2;
+              best_t = t;
+            }
+          }
+        }
+      }
+      if (reuse_side >= 0) {
+        (reuse_side ? b : a) = reuse_rec->dst;
+        if (reuse_pack_other) {
+          const int side = 1 - reuse_side;
+          const BufRef src = side ? b : a;
+          if (const PackRecord* r = reusable(src, reuse_pk)) {
+            (side ? b : a) = r->dst;
+          } else {
+            Step ps;
+            ps.kind = use_permute(reuse_pk) ? Step::kPermute : Step::kDirect;
+            ps.desc = simt_desc(reuse_pk);
+            ps.a = src;
+            ps.c = {BufRef::kWork, alloc(reuse_span)};
+            ps.node = node;
+            ps.label = label + (side ? ":packB" : ":packA");
+            ps.bytes = 8.0 * operand_elems(reuse_pk, 0);
+            (side ? b : a) = ps.c;
+            packs_.push_back({src, reuse_pk, ps.c});
+            pack_log_.push_back({src, reuse_pk, &list == &fwd_});
+            list.push_back(ps);
+          }
+        }
+        p = best_q;
+        st.tc = best_t;
+        ok = true;
+      }
       if (best >= 0) {
         const Attempt& at = attempts[static_cast<std::size_t>(best)];
         for (int side = 0; side < 2; ++side) {
@@ -968,7 +1070,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
           ps.label = label + (side ? ":packB" : ":packA");
           ps.bytes = 8.0 * operand_elems(best_pks[side], 0);
           (side ? b : a) = ps.c;
-          if (&list == &fwd_) packs_.push_back({src, best_pks[side], ps.c});
+          packs_.push_back({src, best_pks[side], ps.c});
           pack_log_.push_back({src, best_pks[side], &list == &fwd_});
           list.push_back(ps);
         }
@@ -1141,7 +1243,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
             ps.label = label + (side_b ? ":packB" : ":packA");
             ps.bytes = 8.0 * operand_elems(pk, 0);
             (side_b ? b : a) = ps.c;
-            if (&list == &fwd_) packs_.push_back({src, pk, ps.c});
+            packs_.push_back({src, pk, ps.c});
             pack_log_.push_back({src, pk, &list == &fwd_});
             list.push_back(ps);
           }

@@ -91,3 +91,11 @@ def test_both_operand_repack_merges_shared_k():
     steps = _steps("rtr", [4, 4, 4], [4, 4, 4], 3, 56, 256, 0.1)
     node3 = [l for l in steps.splitlines() if l.startswith("fwd node3 tc")][0]
     assert " kit=18 " in node3, node3
+
+
+def test_backward_reuses_large_forward_repack():
+    """cfg3 64->128 @28 (B=256): dW1 = sum N0 * dN1 reads N0 in the layout node1's forward
+    repack already wrote (5 GB) instead of repacking N0 again for the backward."""
+    steps = _steps("rtr", [4, 4, 8], [4, 4, 4], 3, 28, 256, 0.1)
+    assert "node1:packA" in steps
+    assert "grad:1:packA" not in steps, steps
