@@ -980,6 +980,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       }();
       int reuse_side = -1;
       const PackRecord* reuse_rec = nullptr;
+      const PackRecord* reuse_rec2 = nullptr;  // the other operand's reused repack (both reused)
       bool reuse_pack_other = false;
       CeProblem reuse_pk{};
       int64_t reuse_span = 0;
@@ -996,11 +997,24 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
           if (operand_elems(r.pk, 0) < min_elems) continue;
           CeProblem q = p;
           if (!remap_operand(q, side == 1, r.pk)) continue;
-          for (int other = 0; other < 2; ++other) {
+          for (int other = 0; other < 3; ++other) {
             CeProblem q2 = q;
             CeProblem pk2{};
             int64_t span2 = 0;
-            if (other) {
+            const PackRecord* r2 = nullptr;
+            if (other == 2) {  // the other operand from an existing repack too
+              const BufRef osrc = side ? a : b;
+              for (const PackRecord& x : packs_)
+                if (x.src.kind == osrc.kind && x.src.index == osrc.index && operand_elems(x.pk, 0) >= min_elems) {
+                  CeProblem q3 = q;
+                  if (remap_operand(q3, side == 0, x.pk)) {
+                    q2 = q3;
+                    r2 = &x;
+                    break;
+                  }
+                }
+              if (!r2) continue;
+            } else if (other) {
               std::vector<int> order = shared_k_order(q, side == 1);
               if (order.empty()) continue;
               pk2 = repack(q2, side == 0, order, &span2, side ? q.sb : q.sa);
@@ -1009,12 +1023,13 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
             if (!ce_tc_plan(q2, &t)) continue;
             const TcParams& P = t.params;
             double us = static_cast<double>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_iters * 0.25 / 148.0;
-            if (other && !reusable(side ? a : b, pk2)) us += 8.0 * operand_elems(pk2, 0) / 3.0e6;
+            if (other == 1 && !reusable(side ? a : b, pk2)) us += 8.0 * operand_elems(pk2, 0) / 3.0e6;
             if (us < best_us) {
               best_us = us;
               best = -1;
               reuse_side = side;
               reuse_rec = &r;
+              reuse_rec2 = r2;
               reuse_pack_other = other == 1;
               reuse_pk = pk2;
               reuse_span = span2;
@@ -1026,6 +1041,7 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
       }
       if (reuse_side >= 0) {
         (reuse_side ? b : a) = reuse_rec->dst;
+        if (reuse_rec2) (reuse_side ? a : b) = reuse_rec2->dst;
         if (reuse_pack_other) {
           const int side = 1 - reuse_side;
           const BufRef src = side ? b : a;
