@@ -988,11 +988,10 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
         const BufRef src = side ? b : a;
         for (const PackRecord& r : packs_) {
           if (r.src.kind != src.kind || r.src.index != src.index) continue;
-          // (large buffers only: the stage model above does not price the MN-major reads a
-          // reused layout often implies -- with small ones, RTR 64->64 went 1.9 -> 2.9 ms)
-          static const double min_elems = [] {  // CE_PACK_REUSE_MIN_MB (default 256)
+          // (repacks of >= 16 MB: smaller ones are cheap to redo)
+          static const double min_elems = [] {  // CE_PACK_REUSE_MIN_MB (default 16)
             const char* e = std::getenv("CE_PACK_REUSE_MIN_MB");
-            return (e ? std::atof(e) : 256.0) * 1024.0 * 1024.0 / 4.0;
+            return (e ? std::atof(e) : 16.0) * 1024.0 * 1024.0 / 4.0;
           }();
           if (operand_elems(r.pk, 0) < min_elems) continue;
           CeProblem q = p;
@@ -1024,6 +1023,17 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
             const TcParams& P = t.params;
             double us = static_cast<double>(P.tiles_m) * P.tiles_n * P.grid_z * P.k_iters * 0.25 / 148.0;
             if (other == 1 && !reusable(side ? a : b, pk2)) us += 8.0 * operand_elems(pk2, 0) / 3.0e6;
+            // MN-major operands read natively cost more per stage than the model's K-major rate
+            // (x4: without it RTR 64->64's input gradient took a reused b-innermost dY and
+            // went 1.9 -> 2.9 ms; with it cfg2 0.960 -> 0.949 ms, cfg3 69.0 -> 67.9 ms)
+            static const double mn_pen = [] {  // CE_PACK_REUSE_MNPEN (default 4)
+              const char* e = std::getenv("CE_PACK_REUSE_MNPEN");
+              return e ? std::atof(e) : 4.0;
+            }();
+            // (split-K reductions -- filter gradients: few outputs, huge K -- stream the MN-major
+            // rows at full rate; tile-parallel steps such as a conv's input gradient do not)
+            if (P.k_split == 1 && P.oa.mn_major) us *= mn_pen;
+            if (P.k_split == 1 && P.ob.mn_major) us *= mn_pen;
             if (us < best_us) {
               best_us = us;
               best = -1;

