@@ -675,6 +675,22 @@ void Executor::add_problem(std::vector<Step>& list, const CeProblem& p0, BufRef 
     list.push_back(st);
     return;
   }
+  // row GEMMs with few columns over millions of rows (ce_rowgemm.cu): one thread per row.
+  // CE_ROWGEMM=0 off.
+  static const bool row_on = [] {
+    const char* e = std::getenv("CE_ROWGEMM");
+    return !(e && *e == '0');
+  }();
+  if (row_on && ce_rowgemm_plan(p, &st.row)) {
+    st.kind = Step::kRow;
+    st.a = a;
+    st.b = b;
+    st.c = c;
+    st.flops = pending_flops_;
+    st.bytes = problem_bytes(p);
+    list.push_back(st);
+    return;
+  }
   const bool tiny_k = [&] {
     int64_t k = 1, outs = 1;
     for (int v = 0; v < p.nv; ++v) (p.cls[v] == CE_K ? k : outs) *= p.ext[v];
@@ -1857,7 +1873,7 @@ float* Executor::resolve(const BufRef& r) const {
 }
 
 std::string Executor::describe() const {
-  static const char* kinds[] = {"direct", "tiled", "tc", "zero", "reduce", "permute", "dw2", "split", "pconv"};
+  static const char* kinds[] = {"direct", "tiled", "tc", "zero", "reduce", "permute", "dw2", "split", "pconv", "row"};
   std::string out;
   char line[512];
   for (const auto* list : {&fwd_, &bwd_})
@@ -1886,6 +1902,9 @@ std::string Executor::describe() const {
           }
           std::snprintf(line + n, sizeof line - n, "%s\n", u.c_str());
         }
+      } else if (st.kind == Step::kRow) {
+        std::snprintf(line + n, sizeof line - n, " rows=%lld K=%d N=%d\n", static_cast<long long>(st.row.M), st.row.K,
+                      st.row.N);
       } else if (st.kind == Step::kPconv) {
         const CePconvDesc& q = st.pconv;
         std::snprintf(line + n, sizeof line - n, " kind=%d planes=%lld pos=%dx%d taps=%dx%d signs=%d,%d ci=%d co=%d\n",
@@ -2048,6 +2067,7 @@ void Executor::launch_step(Step& st, cudaStream_t s) {
       case Step::kPermute: e = ce_launch_permute(st.desc.p, A, C, s); break;
       case Step::kDw2: e = ce_launch_dw2(st.dw2, A, B, resolve(st.b2), C, resolve(st.c2), s); break;
       case Step::kSplit: e = ce_launch_split_tf32(A, C, resolve(st.c2), st.zero_elems, s); break;
+      case Step::kRow: e = ce_launch_rowgemm(st.row, A, B, C, s); break;
       case Step::kPconv:
         if (st.pconv.kind == 1) e = cudaMemsetAsync(C, 0, static_cast<size_t>(st.zero_elems) * 4, s);
         if (e == cudaSuccess) e = ce_launch_pconv(st.pconv, A, B, C, s);

@@ -16,6 +16,7 @@
 #include "../cuda/ce_device.h"
 #include "../cuda/ce_fuse.h"
 #include "../cuda/ce_pconv.h"
+#include "../cuda/ce_rowgemm.h"
 #include "../cuda/ce_tc.h"
 #include "ce_lower.hpp"
 #include "ce_plan.hpp"
@@ -28,7 +29,7 @@ struct BufRef {
 };
 
 struct Step {
-  enum Kind { kDirect, kTiled, kTc, kZero, kReduce, kPermute, kDw2, kSplit, kPconv } kind = kDirect;
+  enum Kind { kDirect, kTiled, kTc, kZero, kReduce, kPermute, kDw2, kSplit, kPconv, kRow } kind = kDirect;
   CeSimtDesc desc{};
   int a_kfast = 0, b_kfast = 0;
   TcPlan tc{};
@@ -38,6 +39,7 @@ struct Step {
   CeDw2Desc dw2{};
   BufRef b2, c2;
   CePconvDesc pconv{};  // kPconv (ce_pconv.h); kind 1 zeroes zero_elems of C first
+  CeRowDesc row{};      // kRow (ce_rowgemm.h)
   int64_t zero_elems = 0;
   double flops = 0;   // algorithmic FLOPs (2 x flops_actual of the node / adjoint)
   double bytes = 0;   // compulsory bytes (|A| + |B| + |C|) x 4

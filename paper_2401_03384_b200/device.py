@@ -217,7 +217,7 @@ class Executor:
         check(lib().ce_executor_profile(self._h, int(backward), n_max, ctypes.byref(n), labels, len(labels), kinds,
                                         ms, fl, by))
         names = labels.value.decode().split("\n")
-        kind_names = ["direct", "tiled", "tc", "memset", "reduce", "permute", "fused", "split", "pconv"]
+        kind_names = ["direct", "tiled", "tc", "memset", "reduce", "permute", "fused", "split", "pconv", "row"]
         return [(names[i], kind_names[kinds[i]], float(ms[i]), float(fl[i]), float(by[i])) for i in range(n.value)]
 
     def execute_host(self, host_inputs: Sequence["numpy.ndarray"], host_out: "numpy.ndarray"):  # noqa: F821
