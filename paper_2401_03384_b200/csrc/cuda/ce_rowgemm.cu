@@ -111,6 +111,9 @@ bool ce_rowgemm_plan(const CeProblem& p, CeRowDesc* out) {
   };
   if (!table(ks, d.ka, p.sa, d.kb, p.sb, &d.K)) return false;
   if (!table(ns, d.nb, p.sb, d.nc, p.sc, &d.N)) return false;
+  // every row costs (padded K) x (padded N) FMAs and shared-memory reads: beyond 256 the
+  // kernel is instruction-bound (RTR 64->128's K = N = 40 rows: 4.2 -> 272 ms)
+  if (round_up(d.K) * round_up(d.N) > 256) return false;
   // (only where the tensor cores do badly: millions of rows, a few columns)
   const char* mn = std::getenv("CE_ROWGEMM_MIN");
   const double min_rows = mn ? std::atof(mn) : static_cast<double>(1 << 20);
@@ -127,8 +130,5 @@ cudaError_t ce_launch_rowgemm(const CeRowDesc& d, const float* A, const float* B
   if (kt == 8 && nt == 32) return launch<8, 32>(d, A, B, C, s);
   if (kt == 16 && nt == 8) return launch<16, 8>(d, A, B, C, s);
   if (kt == 16 && nt == 16) return launch<16, 16>(d, A, B, C, s);
-  if (kt == 16 && nt == 32) return launch<16, 32>(d, A, B, C, s);
-  if (kt == 32 && nt == 8) return launch<32, 8>(d, A, B, C, s);
-  if (kt == 32 && nt == 16) return launch<32, 16>(d, A, B, C, s);
-  return launch<32, 32>(d, A, B, C, s);
+  return launch<32, 8>(d, A, B, C, s);  // (kt * nt <= 256: 32 x 8 is the last shape)
 }

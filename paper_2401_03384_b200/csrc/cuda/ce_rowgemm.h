@@ -1,5 +1,5 @@
 // Row GEMMs with few contracted and few output columns (see ce_rowgemm.cu): out[m, n] =
-// sum_k A[m, k] B[k, n] over millions of rows m with K, N <= 32 and a small B -- the rank
+// sum_k A[m, k] B[k, n] over millions of rows m with K, N <= 32 (K x N <= 256) and a small B -- the rank
 // contractions of the reshaped-ring layers' pixel tensors (RTR conv1: 3.2M pixels x 4, K = 9,
 // N = 16).  On the tensor cores each 128-row tile pads K to 32 and pays an epilogue for a
 // handful of columns.
