@@ -392,6 +392,17 @@ __device__ __forceinline__ void advance_tile(const TcParams& P, Tile& T) {
 __device__ __forceinline__ bool work_next(const TcParams& P, uint32_t ngroups, WorkIter& it, uint32_t& item, int& k0,
                                           int& k1, bool& atomic, int& chunk) {
   chunk = -1;
+  if (P.tl_first && it.tail != ~0u) {  // the tail chunk first (see TcParams::tl_first)
+    const uint32_t t = it.tail / static_cast<uint32_t>(P.tl_s);
+    chunk = static_cast<int>(it.tail - t * static_cast<uint32_t>(P.tl_s));
+    it.tail = ~0u;
+    item = P.sk_full + t;
+    it.seq = false;
+    k0 = chunk * P.k_iters / P.tl_s;
+    k1 = (chunk + 1) * P.k_iters / P.tl_s;
+    atomic = chunk > 0 || P.tl_zeroed;
+    return true;
+  }
   if (P.contig) {
     if (it.w >= it.wend) return false;
     it.seq = item == it.w - 1 && it.w != 0;
@@ -1338,6 +1349,11 @@ cudaError_t ce_launch_tc(TcPlan& plan, const float* A, const float* B, float* C,
     P.tl_s = 1;
     P.tl_flags = plan.tail_flags;
     P.tl_zeroed = 0;
+    static const bool tail_first = [] {  // CE_TC_TAIL_FIRST=0: tail chunks after the whole items
+      const char* e = getenv("CE_TC_TAIL_FIRST");
+      return !(e && *e == '0');
+    }();
+    P.tl_first = tail_first ? 1 : 0;
     P.acc_out = plan.accum ? 1 : 0;
     if (sh.S > 1) {
       P.sk_full = static_cast<uint32_t>(sh.items - sh.r);

@@ -133,6 +133,8 @@ struct TcParams {
   int32_t tl_s;      // K chunks per tail item
   uint32_t* tl_flags;// per tail item: chunks finished (chunk 0 first); zero between launches
   int32_t tl_zeroed; // 1: C was zeroed beforehand -- every tail chunk adds, no flag handshake
+  int32_t tl_first;  // 1: a group runs its tail chunk before its whole items (the chunks' store /
+                     // flag / add handshake then overlaps the whole items' mainloops)
   TcDiv dkit;        // k_iters
   // contiguous assignment (set per launch for many small tiles, no K split, no pairs):
   // group g takes items [g*ipg + min(g, rem), ...) in order, so the tile origins advance
