@@ -399,6 +399,32 @@ bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
     // (a long K loop is split across CTAs instead: split-K fills the machine)
     if (cols >= 128 && k_elems <= 64.0 * TC_BK && out_elems / (static_cast<double>(P.m_rows) * cols) < 74)
       ncap = 128;
+  }
+  {
+    // factor-only GEMMs (e.g. TT's core x factor products, 273 x 256 x 3 outputs): a dozen or
+    // two work items whose epilogues drain one 128 x 256 tile per CTA at per-CTA store speed.
+    // Halve the N tile (down to 64 columns, either B orientation) while the launch has fewer
+    // items than a quarter of the SMs: tt1.0's six factor GEMMs 18 -> 45-65 items, cfg2 step
+    // 0.948 -> 0.939 ms (same-box A/B x3), cfg3 / cfg4 plans unchanged.  CE_TC_FEW_ITEMS=0 off.
+    static const int few = [] {
+      const char* e = std::getenv("CE_TC_FEW_ITEMS");
+      return e ? std::atoi(e) : 1;
+    }();
+    if (few > 0 && ncap_env == 256) {
+      double out_elems = 1, k_elems = 1;
+      for (int v = 0; v < p.nv; ++v) (p.cls[v] != CE_K ? out_elems : k_elems) *= static_cast<double>(p.ext[v]);
+      if (k_elems <= 64.0 * TC_BK) {
+        const std::vector<TcUnit> U0 = U;
+        while (ncap > 64) {
+          int32_t nt0[TC_MAX_UNITS];
+          int32_t nn0 = 0;
+          const int cols = tile(B, b_mn == 1, CE_N, ncap, nt0, &nn0, TC_SRC_NTILE);
+          U = U0;
+          if (out_elems / (static_cast<double>(P.m_rows) * cols) >= 37) break;
+          ncap /= 2;
+        }
+      }
+    }
     // store-bound launches (a K loop of a few stages, e.g. the rank -> channel 1x1 GEMMs writing
     // a [b,t,h,w] activation): half-width N tiles run on the LEAN instances, two CTAs per SM,
     // so two epilogues drain per SM.  CE_TC_SHORTK_NCAP=0 off.

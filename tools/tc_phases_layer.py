@@ -1,5 +1,6 @@
 """Phase + per-iteration stamps of ONE TC launch inside a cfg2 layer's fwd+bwd (graphs off).
-usage: CE_TC_DBG=544 CE_TC_DBG_AT=<n-th TC launch> python tools/tc_phases_layer.py tk 1.0
+usage: CE_TC_DBG=544 CE_TC_DBG_AT=<n-th TC launch> python tools/tc_phases_layer.py tk 1.0 [T-factors S-factors K HP B]
+       (default shape: the cfg2 layer 256 256 3 14 128; e.g. rtr 0.1 4,4,8 4,4,4 3 28 256)
 Needs the debug build of the TC kernel (flags and stamps are compiled out otherwise):
   rm -rf build && make -C paper_2401_03384_b200/csrc TC_DEBUG=1   (rebuild normally afterwards)
 """
@@ -16,11 +17,16 @@ from paper_2401_03384_b200 import _lib  # noqa: E402
 from paper_2401_03384_b200.device import Context, Executor  # noqa: E402
 
 kind, cr = sys.argv[1], float(sys.argv[2])
-SL = {"cp": 1, "tk": 2, "tt": 3, "tr": 4}
+SL = {"cp": 1, "tk": 2, "tt": 3, "tr": 4, "rtr": 4, "rcp": 1, "rtk": 2, "rtt": 3}
 ctx = Context(0, "auto", graphs=False)
 torch.cuda.set_stream(ctx.torch_stream)
 slots = SL[kind]
-le = ce.expression(ce.LayerSpec(kind, [256], [256], 3, 3, 14, 14, 128, [1] * slots), cr)
+if len(sys.argv) > 7:
+    tf, sf = ([int(x) for x in a.split(",")] for a in sys.argv[3:5])
+    k, hp, B = (int(x) for x in sys.argv[5:8])
+else:
+    tf, sf, k, hp, B = [256], [256], 3, 14, 128
+le = ce.expression(ce.LayerSpec(kind, tf, sf, k, k, hp, hp, B, [1] * slots), cr)
 plan = ce.optimal(le.expr, le.dims, "same", "training")
 ex = Executor(ctx, plan, backward=True)
 xs = [ctx.fill_random(d, 1000 + i) for i, d in enumerate(le.dims)]
@@ -53,5 +59,5 @@ if (a > 0).any():
     if len(e):
         e = (e - base) / 1.9e3
         print("epi [start, tables, tfull, stored] per tile:")
-        for row in e[:16]:
+        for row in e[:int(os.environ.get("EPI_ROWS", "16"))]:
             print("   ", " ".join(f"{x:8.2f}" for x in row))
