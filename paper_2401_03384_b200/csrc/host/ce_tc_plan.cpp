@@ -737,13 +737,22 @@ bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
     return !(e && *e == '0');
   }();
   P.mcast = 0;
-  // CTA pairs (cta_group::2 + B multicast) are opt-in (CE_TC_PAIR=1): once the kernel ran
+  // CTA pairs (cta_group::2 + B multicast) for every launch (CE_TC_PAIR=1): once the kernel ran
   // below its register cap, single-CTA launches measured faster on the cfg2 step (1.195 vs
-  // 1.216 ms, same-box A/B x3) and equal or better on every layer profiled
-  static const bool pair_enabled = [] {
+  // 1.216 ms, same-box A/B x3) and equal or better on most layers profiled
+  // Default (CE_TC_PAIR=3): pairs only for wide (> 128 column) tile-parallel launches with 25..47
+  // K stages -- above the LEAN instances, below the tail split (which the pair path lacks) --
+  // where halving each CTA's B bytes per stage relieves the L2-fed N=256 mainloop: tt1.0's
+  // node3 / dN1 convs 53.7 -> 45.6 us, cfg2 step 0.938 -> 0.929 ms (same-box A/B x4), cfg3
+  // unchanged.  CE_TC_PAIR=2: every wide launch of >= 16 stages (tk1.0's convs lose their tail
+  // split and TMA store: 59.9 -> 72.2 us); 1: every eligible launch; 0: none.
+  static const int pair_mode = [] {
     const char* e = std::getenv("CE_TC_PAIR");
-    return e && *e == '1';
+    return e ? std::atoi(e) : 3;
   }();
+  const bool pair_enabled = pair_mode == 1 ||
+                            (pair_mode == 2 && P.n_cols > 128 && ki >= 16 && tm * tn * gz >= 148) ||
+                            (pair_mode == 3 && P.n_cols > 128 && ki > 24 && ki < 48 && tm * tn * gz >= 148);
   // (CE_TC_PAIR=0 now means no cluster at all: the older single-CTA multicast variant
   // (mcast 1) hung on a CP 64->64 @56 layer's split-K launch and is no longer planned)
   if (mcast_enabled && pair_enabled && b_mn == 0 && P.nn == 1 && P.tiles_m >= 2 && P.n_cols >= 64 &&
