@@ -1235,9 +1235,11 @@ TcShape tc_shape(const TcPlan& plan) {
     const char* e = getenv("CE_TC_LEAN");
     return e ? atoi(e) : 2;
   }();
+  // (32 since the end of round 2: cfg3's 256->512 @7 layer 1.38 -> 0.90 ms, stack 62.55 ->
+  // 62.13 ms, cfg2 / cfg4 unchanged (same-box A/B x2-3); 40 loses on cfg3)
   static const int lean_kmax = [] {
     const char* e = getenv("CE_TC_LEAN_KMAX");
-    return e ? atoi(e) : 24;
+    return e ? atoi(e) : 32;
   }();
   static const bool contig_on = [] {
     const char* e = getenv("CE_TC_CONTIG");
