@@ -460,11 +460,12 @@ CeProblem repack(CeProblem& p, bool side_b, const std::vector<int>& inner_order,
   // the output vars among the rest take their slots in C's stride order: the tile units they
   // form then enumerate columns / rows in C order, so the epilogue's 4-column groups are
   // contiguous in C (float4 stores) -- K vars keep their slots (same K units)
-  // Opt-in (CE_PACK_CORDER=1): RTR 64->128 layer 64.3 -> 60.9 ms, but conv1 17.0 -> 17.4 ms
-  // and the cfg2 step +0.3% (3 A/B pairs), so not the default.
+  // Default since the end of round 2 (CE_PACK_CORDER=0 off): cfg3 stack 62.15 -> 61.49 ms (RTR
+  // 64->128 26.08 -> 25.41 ms), cfg2 step and cfg4 unchanged within noise (same-box A/B x2-3).
+  // (Round 1, before the row GEMMs / plane convolutions: conv1 17.0 -> 17.4 ms, cfg2 +0.3%.)
   static const bool c_order = [] {
     const char* e = std::getenv("CE_PACK_CORDER");
-    return e && *e == '1';
+    return !(e && *e == '0');
   }();
   if (c_order || out_c_order) {
     std::vector<std::size_t> slots;
@@ -1489,10 +1490,12 @@ void Executor::fuse_chains(std::vector<Step>& list) {
       // reads it) fusion saves only its re-read, and the two stencil launches stream at
       // ~4.8 TB/s against ~3 TB/s for the fused tile kernel: fuse those pairs only while the
       // intermediate is small enough for the saved launch to dominate (CP cr 0.1 layers:
-      // conv1 1.23 -> 1.15 ms; R = 275 @56: 376 -> 432 us, not fused).  CE_FUSE_MAX_MB.
+      // conv1 1.23 -> 1.15 ms; R = 275 @56: 376 -> 432 us, not fused).  CE_FUSE_MAX_MB: 96 ->
+      // 256 at the end of round 2 (cfg4 cr 1.0 stack 36.20 -> 35.62 ms: the 128 @28 and 256 @14
+      // layers fuse; cfg2 / cfg3 / cfg4 cr 0.1 unchanged, same-box A/B x2).
       static const double max_mb = [] {
         const char* e = std::getenv("CE_FUSE_MAX_MB");
-        return e ? std::atof(e) : 96.0;
+        return e ? std::atof(e) : 256.0;
       }();
       if (write_mid && 4.0 * operand_elems(si.desc.p, 2) > max_mb * 1048576.0) break;
       CeDw2Desc d{};
