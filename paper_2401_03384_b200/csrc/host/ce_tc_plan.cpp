@@ -405,7 +405,7 @@ bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
     // two work items whose epilogues drain one 128 x 256 tile per CTA at per-CTA store speed.
     // Halve the N tile (down to 64 columns, either B orientation) while the launch has fewer
     // items than a quarter of the SMs: tt1.0's six factor GEMMs 18 -> 45-65 items, cfg2 step
-    // 0.948 -> 0.939 ms (same-box A/B x3), cfg3 / cfg4 plans unchanged.  CE_TC_FEW_ITEMS=0 off.
+    // 0.948 -> 0.939 ms (same-box A/B x3), cfg3 / cfg4 plans unchanged.  CE_TC_FEW_ITEMS=0 off, >1: the item threshold.
     static const int few = [] {
       const char* e = std::getenv("CE_TC_FEW_ITEMS");
       return e ? std::atoi(e) : 1;
@@ -420,7 +420,7 @@ bool tc_plan_impl(const CeProblem& p, TcPlan* plan, bool units_chain_in_c) {
           int32_t nn0 = 0;
           const int cols = tile(B, b_mn == 1, CE_N, ncap, nt0, &nn0, TC_SRC_NTILE);
           U = U0;
-          if (out_elems / (static_cast<double>(P.m_rows) * cols) >= 37) break;
+          if (out_elems / (static_cast<double>(P.m_rows) * cols) >= (few > 1 ? few : 37)) break;
           ncap /= 2;
         }
       }
